@@ -1,0 +1,122 @@
+"""CPU oracle for the FP64 Cholesky + adjoint hot path (arXiv:1907.01063).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and
+``bench.py``'s ``cpu_baseline`` / ``--impl reference`` legs may import this
+package.  The product path (``paper_1907_01063_b200``) never imports it, and
+the two share no code.
+
+The arithmetic lives in ``oracle.c`` (plain C99, single thread, binary64,
+``-O2 -ffp-contract=off``); this module only compiles it and marshals numpy
+arrays through ctypes.  See ``oracle.c`` for the per-function citations.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+CFLAGS = ["-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    """Compile oracle.c -> liboracle.so (gcc).  Returns the library path."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *CFLAGS, "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        lib = ctypes.CDLL(build())
+        P = ctypes.c_void_p
+        I64 = ctypes.c_int64
+        D = ctypes.c_double
+        lib.oracle_se_cov.argtypes = [I64, P, D, D, D, P]
+        lib.oracle_se_cov.restype = None
+        for name in ("oracle_cholesky", "oracle_cholesky_ld"):
+            getattr(lib, name).argtypes = [I64, P, P]
+            getattr(lib, name).restype = ctypes.c_int
+        lib.oracle_cholesky_adjoint.argtypes = [I64, P, P, P]
+        lib.oracle_cholesky_adjoint.restype = ctypes.c_int
+        _lib = lib
+    return _lib
+
+
+def _c(a: np.ndarray) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.float64)
+    return a
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.c_void_p)
+
+
+class NotPositiveDefinite(ValueError):
+    def __init__(self, info: int):
+        super().__init__(f"matrix not positive definite: first failing pivot at row {info - 1}")
+        self.info = info
+
+
+def se_cov(x, alpha: float = 1.0, rho: float = 1.0, jitter: float = 1e-6) -> np.ndarray:
+    """K_ij = alpha^2 exp((x_i-x_j)^2 (-0.5/rho^2)) + jitter [i==j] (oracle.c)."""
+    x = _c(x)
+    n = x.shape[0]
+    K = np.empty((n, n), dtype=np.float64)
+    _load().oracle_se_cov(n, _ptr(x), float(alpha), float(rho), float(jitter), _ptr(K))
+    return K
+
+
+def cholesky_info(A) -> tuple[np.ndarray, int]:
+    """(L, info): Cholesky-Banachiewicz; info = 0 or failing row + 1."""
+    A = _c(A)
+    n = A.shape[0]
+    assert A.shape == (n, n)
+    L = np.empty_like(A)
+    info = _load().oracle_cholesky(n, _ptr(A), _ptr(L))
+    return L, int(info)
+
+
+def cholesky(A) -> np.ndarray:
+    L, info = cholesky_info(A)
+    if info != 0:
+        raise NotPositiveDefinite(info)
+    return L
+
+
+def cholesky_ld(A) -> np.ndarray:
+    """Long-double twin of ``cholesky`` (truth proxy for floor studies)."""
+    A = _c(A)
+    n = A.shape[0]
+    L = np.empty_like(A)
+    info = _load().oracle_cholesky_ld(n, _ptr(A), _ptr(L))
+    if info != 0:
+        raise NotPositiveDefinite(info)
+    return L
+
+
+def cholesky_adjoint_info(L, Lbar) -> tuple[np.ndarray, int]:
+    L = _c(L)
+    Lbar = _c(Lbar)
+    n = L.shape[0]
+    assert L.shape == (n, n) and Lbar.shape == (n, n)
+    Abar = np.empty_like(L)
+    info = _load().oracle_cholesky_adjoint(n, _ptr(L), _ptr(Lbar), _ptr(Abar))
+    return Abar, int(info)
+
+
+def cholesky_adjoint(L, Lbar) -> np.ndarray:
+    """A_bar given L and L_bar, Stan's Phi(G + G^T) convention (oracle.c)."""
+    Abar, info = cholesky_adjoint_info(L, Lbar)
+    if info != 0:
+        raise ValueError(f"L[{info - 1}][{info - 1}] is not finite and > 0")
+    return Abar
