@@ -1,0 +1,127 @@
+/*
+ * stan_cl.h -- C ABI of libstancl: FP64 Cholesky factorisation and its
+ * reverse-mode adjoint on NVIDIA B200 (sm_100a), the computation Stan's GPU
+ * backend accelerates for Gaussian-process models
+ * ("GPU-based parallel computation support for Stan", arXiv:1907.01063,
+ * /root/reference/PAPER.md; citations are PAPER.md line numbers).
+ *
+ * Conventions for every matrix argument unless stated otherwise
+ *   - n x n, row-major, leading dimension n, IEEE binary64;
+ *   - CUDA device pointers on the current device (the *_host entry points take
+ *     host pointers instead);
+ *   - only the lower triangle (i >= j) of A, L and L_bar is read
+ *     (reading R1); the strict upper triangle of every output
+ *     matrix is written as +0.0 ("filled with zeros", PAPER.md:321
+ *     set_zeros_in_upper_tri);
+ *   - work is enqueued on the library stream (stan_cl_set_stream; default:
+ *     the legacy default stream).  The plain entry points return after the
+ *     stream has drained (they read back the status word); the *_async entry
+ *     points return immediately and leave the status in device memory.
+ *
+ * Ownership: the caller owns every buffer passed in.  The library owns only
+ * its internal workspace (allocated lazily, released by stan_cl_finalize);
+ * no pointer is retained after a call returns.  Calls are not thread-safe
+ * with respect to each other (one library stream and workspace per process).
+ *
+ * Return values: 0 = success; k > 0 = numerical failure (see each call);
+ * negative = STAN_CL_E* error codes below.
+ */
+#ifndef STAN_CL_H
+#define STAN_CL_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STAN_CL_OK 0
+#define STAN_CL_EINVAL (-1) /* bad argument: n < 0, NULL with n > 0, forbidden overlap, bad nb */
+#define STAN_CL_ENOMEM (-2) /* device workspace allocation failed */
+#define STAN_CL_ECUDA (-3)  /* a CUDA runtime error (launch, copy, sync) */
+#define STAN_CL_ENCCL (-4)  /* reserved for the multi-GPU layer */
+
+/*
+ * L = chol(A): lower-triangular L with positive diagonal and L L^T = A.
+ * Method: PAPER.md:244-291 (§3.3.1) -- blocked right-looking factorisation
+ * (L11 = chol(A11); L21 = A21 L11^-T; A22 -= L21 L21^T), diagonal tiles by the
+ * "classic sequential algorithm", L21 by substitution (R11).
+ *   n   order (n == 0: returns 0, touches nothing)
+ *   A   device, n x n, lower triangle read
+ *   L   device, n x n, written in full; L == A (in place) allowed, any other
+ *       overlap of the two n x n ranges -> STAN_CL_EINVAL
+ * Returns k > 0 (LAPACK-style info) when A is not positive definite: the
+ * first failing pivot (s <= 0 or NaN) is row k-1 (R4); L is then
+ * unspecified.
+ */
+int stan_cl_cholesky(int64_t n, const double* A, double* L);
+
+/*
+ * A_bar = reverse-mode adjoint of L = chol(A) given L and L_bar = df/dL:
+ *   A_bar = Phi(G + G^T),  G = L^-T Phi(L^T tril(L_bar)) L^-1,
+ * Phi(X) = tril(X) with the diagonal halved (Stan's convention: strictly-lower
+ * A_bar[i][j] is df/da_ij of the symmetric pair, the diagonal is df/da_ii;
+ * DESIGN.md R5).  Method: the blocked gradient of PAPER.md:297-323 (§3.3.2),
+ * reverse block order, with reading R6 of the garbled line PAPER.md:320.
+ *   L      device, n x n, lower triangle read (diagonal must be finite and > 0)
+ *   L_bar  device, n x n, lower triangle read
+ *   A_bar  device, n x n, written in full (strict upper +0.0).  A_bar == L_bar
+ *          allowed (in place); A_bar overlapping L, or partially overlapping
+ *          L_bar -> STAN_CL_EINVAL.
+ * Overwrites A_bar (Stan's A.adj += accumulation is the caller's job).
+ * Returns k > 0 when L[k-1][k-1] is not finite and > 0.
+ */
+int stan_cl_cholesky_adjoint(int64_t n, const double* L, const double* L_bar, double* A_bar);
+
+/*
+ * Squared-exponential GP covariance of the paper's GP example (inputs
+ * PAPER.md:475; kernel form DESIGN.md R14):
+ *   K[i][j] = alpha^2 * exp((x_i - x_j)^2 * (-0.5 / rho^2)) + jitter * [i == j]
+ *   x  device, n doubles;  K  device, n x n, written in full (symmetric).
+ * rho must be finite and nonzero, else STAN_CL_EINVAL.
+ */
+int stan_cl_gp_exp_quad_cov(int64_t n, const double* x, double alpha, double rho, double jitter,
+                            double* K);
+
+/*
+ * Asynchronous variants: same arguments and semantics, but the call returns
+ * once the work is enqueued.  d_info (device int, caller-owned, may be NULL
+ * when the caller does not need it) receives the status word the synchronous
+ * call would return for a numerical failure (0 or k > 0) when the stream
+ * reaches it.  Argument errors are still returned directly.
+ */
+int stan_cl_cholesky_async(int64_t n, const double* A, double* L, int* d_info);
+int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_bar, double* A_bar,
+                                   int* d_info);
+
+/*
+ * Host-buffer variants (end-to-end, the quantity PAPER.md:295, 332 measures):
+ * all matrix pointers are HOST pointers (pinned memory is fastest); the call
+ * copies the lower triangles to the device, runs the device path, copies the
+ * result back and returns after the copy-back.  Same return values.
+ */
+int stan_cl_cholesky_host(int64_t n, const double* A, double* L);
+int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar);
+
+/* ---- control ---- */
+int stan_cl_set_stream(void* cuda_stream); /* cudaStream_t; NULL = legacy default stream */
+void* stan_cl_get_stream(void);
+/* block size of the blocked algorithms; 0 = auto (128).  Only 0 and 128 are
+ * supported in this version; others -> STAN_CL_EINVAL. */
+int stan_cl_set_block_size(int nb);
+int stan_cl_get_block_size(void);
+/* device workspace the next call of order n would use (bytes) */
+size_t stan_cl_workspace_bytes(int64_t n);
+const char* stan_cl_status_string(int status);
+/* number of CUDA kernel launches the library has issued so far (process-wide) */
+long long stan_cl_kernel_launches(void);
+/* release library-owned device workspace; the library stays usable */
+int stan_cl_finalize(void);
+int stan_cl_version(void); /* major*10000 + minor*100 + patch */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STAN_CL_H */

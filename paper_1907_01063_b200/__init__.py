@@ -1,0 +1,208 @@
+"""paper_1907_01063_b200 -- B200-native FP64 Cholesky + adjoint (arXiv:1907.01063 hot path).
+
+Thin ctypes binding over the C ABI in ``include/stan_cl.h`` (``libstancl.so``,
+built in-tree for sm_100a).  This module only marshals arguments: every step of
+the path runs in the library's CUDA kernels.  There is no CPU fallback: if the
+library is missing or no CUDA device is present, calls raise.
+
+PyTorch is used for device memory and streams only.
+
+    import torch, paper_1907_01063_b200 as sc
+    K = sc.gp_exp_quad_cov(x, alpha=1.0, rho=1.0, jitter=1e-6)   # x: cuda float64 [n]
+    L = sc.cholesky(K)
+    Abar = sc.cholesky_adjoint(L, Lbar)
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+__all__ = [
+    "cholesky", "cholesky_adjoint", "gp_exp_quad_cov", "cholesky_async", "cholesky_adjoint_async",
+    "cholesky_host", "cholesky_adjoint_host", "kernel_launches", "library_path", "load",
+    "StanClError", "NotPositiveDefinite", "STATUS", "workspace_bytes", "finalize",
+]
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_PKG, "libstancl.so")
+_lib = None
+
+STATUS = {0: "STAN_CL_OK", -1: "STAN_CL_EINVAL", -2: "STAN_CL_ENOMEM", -3: "STAN_CL_ECUDA",
+          -4: "STAN_CL_ENCCL"}
+
+# every entry point declared in include/stan_cl.h: (name, restype, argtypes)
+_P, _I64, _D, _I = ctypes.c_void_p, ctypes.c_int64, ctypes.c_double, ctypes.c_int
+SIGNATURES = {
+    "stan_cl_cholesky": (_I, [_I64, _P, _P]),
+    "stan_cl_cholesky_adjoint": (_I, [_I64, _P, _P, _P]),
+    "stan_cl_gp_exp_quad_cov": (_I, [_I64, _P, _D, _D, _D, _P]),
+    "stan_cl_cholesky_async": (_I, [_I64, _P, _P, _P]),
+    "stan_cl_cholesky_adjoint_async": (_I, [_I64, _P, _P, _P, _P]),
+    "stan_cl_cholesky_host": (_I, [_I64, _P, _P]),
+    "stan_cl_cholesky_adjoint_host": (_I, [_I64, _P, _P, _P]),
+    "stan_cl_set_stream": (_I, [_P]),
+    "stan_cl_get_stream": (_P, []),
+    "stan_cl_set_block_size": (_I, [_I]),
+    "stan_cl_get_block_size": (_I, []),
+    "stan_cl_workspace_bytes": (ctypes.c_size_t, [_I64]),
+    "stan_cl_status_string": (ctypes.c_char_p, [_I]),
+    "stan_cl_kernel_launches": (ctypes.c_longlong, []),
+    "stan_cl_finalize": (_I, []),
+    "stan_cl_version": (_I, []),
+}
+
+
+class StanClError(RuntimeError):
+    def __init__(self, fn: str, status: int, msg: str):
+        super().__init__(f"{fn}: {STATUS.get(status, status)} ({msg})")
+        self.status = status
+
+
+class NotPositiveDefinite(ValueError):
+    def __init__(self, info: int):
+        super().__init__(f"matrix is not positive definite: first failing pivot at row {info - 1}")
+        self.info = info
+
+
+def library_path() -> str:
+    return _LIB_PATH
+
+
+def load():
+    """Load libstancl.so (raises if it has not been built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH):
+            raise ImportError(f"{_LIB_PATH} not built; run `python -m paper_1907_01063_b200._build`")
+        lib = ctypes.CDLL(_LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            f = getattr(lib, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = lib
+    return _lib
+
+
+def _check(fn: str, rc: int):
+    if rc < 0:
+        raise StanClError(fn, rc, load().stan_cl_status_string(rc).decode())
+    return rc
+
+
+def _bind_stream(device: torch.device):
+    s = torch.cuda.current_stream(device)
+    load().stan_cl_set_stream(ctypes.c_void_p(s.cuda_stream))
+
+
+def _dev_matrix(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != torch.float64:
+        raise ValueError(f"{name} must be float64")
+    if t.dim() != 2 or t.shape[0] != t.shape[1]:
+        raise ValueError(f"{name} must be square")
+    return t.contiguous()
+
+
+def cholesky(A: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """L = chol(A) (stan_cl_cholesky).  ``out`` may be ``A`` (in place)."""
+    A = _dev_matrix(A, "A")
+    n = A.shape[0]
+    L = torch.empty_like(A) if out is None else out
+    with torch.cuda.device(A.device):
+        _bind_stream(A.device)
+        rc = _check("stan_cl_cholesky", load().stan_cl_cholesky(n, A.data_ptr(), L.data_ptr()))
+    if rc > 0:
+        raise NotPositiveDefinite(rc)
+    return L
+
+
+def cholesky_adjoint(L: torch.Tensor, Lbar: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """A_bar = Phi(G + G^T) (stan_cl_cholesky_adjoint).  ``out`` may be ``Lbar``."""
+    L = _dev_matrix(L, "L")
+    Lbar = _dev_matrix(Lbar, "Lbar")
+    n = L.shape[0]
+    if Lbar.shape[0] != n:
+        raise ValueError("L and Lbar differ in shape")
+    Abar = torch.empty_like(L) if out is None else out
+    with torch.cuda.device(L.device):
+        _bind_stream(L.device)
+        rc = _check("stan_cl_cholesky_adjoint",
+                    load().stan_cl_cholesky_adjoint(n, L.data_ptr(), Lbar.data_ptr(), Abar.data_ptr()))
+    if rc > 0:
+        raise ValueError(f"L[{rc - 1}][{rc - 1}] is not finite and > 0")
+    return Abar
+
+
+def gp_exp_quad_cov(x: torch.Tensor, alpha: float = 1.0, rho: float = 1.0, jitter: float = 0.0,
+                    out: torch.Tensor | None = None) -> torch.Tensor:
+    """K_ij = alpha^2 exp((x_i-x_j)^2 (-0.5/rho^2)) + jitter [i==j] (stan_cl_gp_exp_quad_cov)."""
+    if not x.is_cuda or x.dtype != torch.float64 or x.dim() != 1:
+        raise ValueError("x must be a 1-D float64 CUDA tensor")
+    x = x.contiguous()
+    n = x.shape[0]
+    K = torch.empty((n, n), dtype=torch.float64, device=x.device) if out is None else out
+    with torch.cuda.device(x.device):
+        _bind_stream(x.device)
+        _check("stan_cl_gp_exp_quad_cov",
+               load().stan_cl_gp_exp_quad_cov(n, x.data_ptr(), float(alpha), float(rho), float(jitter),
+                                              K.data_ptr()))
+    return K
+
+
+def cholesky_async(A: torch.Tensor, L: torch.Tensor, info: torch.Tensor | None = None) -> None:
+    """Enqueue L = chol(A) without synchronising; ``info`` (cuda int32[1]) gets the status."""
+    n = A.shape[0]
+    with torch.cuda.device(A.device):
+        _bind_stream(A.device)
+        _check("stan_cl_cholesky_async", load().stan_cl_cholesky_async(
+            n, A.data_ptr(), L.data_ptr(), None if info is None else info.data_ptr()))
+
+
+def cholesky_adjoint_async(L: torch.Tensor, Lbar: torch.Tensor, Abar: torch.Tensor,
+                           info: torch.Tensor | None = None) -> None:
+    n = L.shape[0]
+    with torch.cuda.device(L.device):
+        _bind_stream(L.device)
+        _check("stan_cl_cholesky_adjoint_async", load().stan_cl_cholesky_adjoint_async(
+            n, L.data_ptr(), Lbar.data_ptr(), Abar.data_ptr(), None if info is None else info.data_ptr()))
+
+
+def _host_matrix(t: torch.Tensor, name: str) -> torch.Tensor:
+    if t.is_cuda or t.dtype != torch.float64 or t.dim() != 2 or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous float64 CPU tensor")
+    return t
+
+
+def cholesky_host(A: torch.Tensor, L: torch.Tensor, device: int = 0) -> int:
+    """Host buffers in, host buffer out (stan_cl_cholesky_host); returns info."""
+    _host_matrix(A, "A")
+    _host_matrix(L, "L")
+    dev = torch.device("cuda", device)
+    with torch.cuda.device(dev):
+        _bind_stream(dev)
+        return _check("stan_cl_cholesky_host", load().stan_cl_cholesky_host(A.shape[0], A.data_ptr(), L.data_ptr()))
+
+
+def cholesky_adjoint_host(L: torch.Tensor, Lbar: torch.Tensor, Abar: torch.Tensor, device: int = 0) -> int:
+    for t, nm in ((L, "L"), (Lbar, "Lbar"), (Abar, "Abar")):
+        _host_matrix(t, nm)
+    dev = torch.device("cuda", device)
+    with torch.cuda.device(dev):
+        _bind_stream(dev)
+        return _check("stan_cl_cholesky_adjoint_host", load().stan_cl_cholesky_adjoint_host(
+            L.shape[0], L.data_ptr(), Lbar.data_ptr(), Abar.data_ptr()))
+
+
+def kernel_launches() -> int:
+    return int(load().stan_cl_kernel_launches())
+
+
+def workspace_bytes(n: int) -> int:
+    return int(load().stan_cl_workspace_bytes(n))
+
+
+def finalize() -> None:
+    load().stan_cl_finalize()

@@ -1,0 +1,419 @@
+// api.cu -- the C ABI of libstancl (include/stan_cl.h) and the host-side
+// schedulers of the blocked forward and adjoint
+// algorithms.
+//
+// Layout: every call works on an N x N row-major working matrix, N = n rounded
+// up to NB = 128.  When n is already a multiple of NB and the buffers are
+// 16-byte aligned, the output buffer itself is the working matrix (no extra
+// HBM traffic).  Otherwise the inputs are copied into a padded workspace:
+//   forward  A_pad = [[A, 0], [0, I]]      -> L_pad = [[L, 0], [0, I]]
+//   adjoint  L_pad = [[L, 0], [0, I]], L_bar_pad = [[L_bar, 0], [0, 0]]
+//                                          -> A_bar_pad = [[A_bar, 0], [0, 0]]
+// (the padded problems decouple), so no kernel needs ragged-edge
+// code.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+
+#include "../../include/stan_cl.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace stancl;
+
+namespace {
+
+struct State {
+  cudaStream_t stream = nullptr;  // nullptr = legacy default stream
+  int nb = NB;
+  void* ws = nullptr;  // library-owned persistent workspace
+  size_t ws_cap = 0;
+  int* h_status = nullptr;  // pinned host word for the synchronous calls
+  char last_err[256] = {0};
+};
+State g;
+
+int cuda_fail(cudaError_t e, const char* where) {
+  snprintf(g.last_err, sizeof(g.last_err), "%s: %s", where, cudaGetErrorString(e));
+  return STAN_CL_ECUDA;
+}
+
+#define CK(x)                                              \
+  do {                                                     \
+    cudaError_t e_ = (x);                                  \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #x);       \
+  } while (0)
+
+inline int64_t round_up(int64_t n, int64_t b) { return (n + b - 1) / b * b; }
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+bool ranges_overlap(const void* a, const void* b, size_t bytes) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + bytes && y < x + bytes;
+}
+
+// ---------------------------------------------------------------- workspace
+constexpr size_t kAlign = 256;
+inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
+
+struct AdjPlan {
+  int64_t N;
+  size_t dinv, part, tmp, total;
+};
+
+// split-K factor for W = C_bar^T L[k:N, 0:k]: minimise waves * (m / splits)
+void splitk_choice(int64_t m, int64_t k, int* splits_out, int* kps_out) {
+  const int ntiles = (int)(k / NB);
+  const int kmax = (int)(m / 16);
+  double best = 1e300;
+  int bs = 1;
+  for (int s = 1; s <= 64 && s <= kmax; ++s) {
+    const int64_t kps = round_up((m + s - 1) / s, 16);
+    const int eff_s = (int)((m + kps - 1) / kps);
+    const int64_t ctas = (int64_t)ntiles * eff_s;
+    const int64_t waves = (ctas + 147) / 148;
+    // per-CTA time ~ kps (+ fixed cost ~ 64 k-rows), plus reduce cost ~ splits
+    const double t = (double)waves * (double)(kps + 64) + 2.0 * eff_s * 16;
+    if (t < best - 1e-9) {
+      best = t;
+      bs = s;
+    }
+  }
+  int64_t kps = round_up((m + bs - 1) / bs, 16);
+  *kps_out = (int)kps;
+  *splits_out = (int)((m + kps - 1) / kps);
+}
+
+AdjPlan adj_plan(int64_t n) {
+  AdjPlan p{};
+  p.N = round_up(n, NB);
+  const int64_t nblk = p.N / NB;
+  p.dinv = al((size_t)nblk * NB * NB * sizeof(double));
+  size_t part = 0;
+  for (int64_t k = p.N; k > 0; k -= NB) {
+    const int64_t m = p.N - k;
+    if (m == 0) continue;
+    int s, kps;
+    splitk_choice(m, k, &s, &kps);
+    const size_t b = (size_t)s * NB * (size_t)k * sizeof(double);
+    if (b > part) part = b;
+  }
+  p.part = al(part);
+  p.tmp = al(4 * NB * NB * sizeof(double));
+  p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp;
+  return p;
+}
+
+int ensure_ws(size_t bytes) {
+  if (g.ws_cap >= bytes && g.ws) return STAN_CL_OK;
+  if (g.ws) {
+    CK(cudaStreamSynchronize(g.stream));
+    CK(cudaFree(g.ws));
+    g.ws = nullptr;
+    g.ws_cap = 0;
+  }
+  cudaError_t e = cudaMalloc(&g.ws, bytes);
+  if (e != cudaSuccess) {
+    g.ws = nullptr;
+    snprintf(g.last_err, sizeof(g.last_err), "workspace cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+    cudaGetLastError();
+    return STAN_CL_ENOMEM;
+  }
+  g.ws_cap = bytes;
+  return STAN_CL_OK;
+}
+
+int ensure_host_status() {
+  if (!g.h_status) CK(cudaMallocHost(&g.h_status, sizeof(int)));
+  return STAN_CL_OK;
+}
+
+int alloc_async(double** p, size_t bytes) {
+  cudaError_t e = cudaMallocAsync((void**)p, bytes, g.stream);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    snprintf(g.last_err, sizeof(g.last_err), "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
+    return STAN_CL_ENOMEM;
+  }
+  return STAN_CL_OK;
+}
+
+// ------------------------------------------------------------------ forward
+// Right-looking blocked Cholesky on the N x N working matrix W (lower part).
+int factor_inplace(double* W, int64_t N, int64_t ld, int* status) {
+  cudaStream_t st = g.stream;
+  for (int64_t k0 = 0; k0 < N; k0 += NB) {
+    CK(potrf_tile(W, ld, k0, status, st));                       // L11 = chol(A11)
+    const int64_t r0 = k0 + NB;
+    if (r0 >= N) break;
+    CK(trsm_panel(W, ld, k0, r0, N, status, st));                // L21 = A21 L11^-T
+    const double* L21 = W + r0 * ld + k0;
+    CK(gemm_lower_nt((int)(N - r0), NB, L21, ld, L21, ld, W + r0 * ld + r0, ld, status, st));  // A22 -= L21 L21^T
+  }
+  return STAN_CL_OK;
+}
+
+int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) {
+    if (d_info) CK(cudaMemsetAsync(d_info, 0, sizeof(int), g.stream));
+    return STAN_CL_OK;
+  }
+  if (!A || !L) return STAN_CL_EINVAL;
+  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  if (A != L && ranges_overlap(A, L, bytes)) return STAN_CL_EINVAL;
+  int rc = ensure_ws(al(sizeof(int) * 64));
+  if (rc) return rc;
+  int* status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  const int64_t N = round_up(n, NB);
+  const bool fast = (N == n) && aligned16(A) && aligned16(L);
+  if (fast) {
+    if (A != L) CK(copy_lower_pad(A, n, n, L, n, n, 1.0, st));
+    rc = factor_inplace(L, n, n, status);
+    if (rc) return rc;
+    if (A == L) CK(zero_upper(L, n, n, st));
+  } else {
+    double* W = nullptr;
+    rc = alloc_async(&W, (size_t)N * N * sizeof(double));
+    if (rc) return rc;
+    CK(copy_lower_pad(A, n, n, W, N, N, 1.0, st));
+    rc = factor_inplace(W, N, N, status);
+    if (rc) return rc;
+    CK(copy_lower_out(W, N, L, n, n, st));
+    CK(cudaFreeAsync(W, st));
+  }
+  if (d_info) CK(cudaMemcpyAsync(d_info, status, sizeof(int), cudaMemcpyDeviceToDevice, st));
+  return STAN_CL_OK;
+}
+
+// ------------------------------------------------------------------ adjoint
+// Blocked reverse sweep on the working matrix Wm (initially
+// tril(L_bar)) with factor Lw, both N x N with leading dimension ld.
+int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* status,
+                    const AdjPlan& plan) {
+  cudaStream_t st = g.stream;
+  char* base = (char*)g.ws + al(sizeof(int) * 64);
+  double* Dinv = (double*)base;
+  double* Pbuf = (double*)(base + plan.dinv);
+  double* T1 = (double*)(base + plan.dinv + plan.part);
+  double* T2 = T1 + NB * NB;
+  double* T3 = T2 + NB * NB;
+  double* T4 = T3 + NB * NB;
+  const int nblk = (int)(N / NB);
+  // D^-1 of every diagonal block depends only on L: one batched launch, off the
+  // critical path (lower_triangular_inverse(D))
+  CK(tri_inverse_batched(Lw, ld, nblk, Dinv, status, st));
+  for (int64_t k = N; k > 0; k -= NB) {
+    const int64_t j = k - NB, m = N - k;
+    const double* D = Lw + j * ld + j;
+    const double* Db = Dinv + (j / NB) * NB * NB;
+    const double* R = Lw + j * ld;       // L(j:k, 0:j)
+    double* Cb = Wm + k * ld + j;        // C_adj = L_adj(k:N, j:k)
+    double* Dbar = Wm + j * ld + j;      // D_adj
+    if (m > 0) {
+      // C_adj = C_adj * lower_triangular_inverse(D)
+      CK(gemm_full(true, false, (int)m, NB, NB, 1.0, 0, Cb, ld, Db, NB, Cb, ld, status, st));
+      // B_adj = B_adj - C_adj * R
+      if (j > 0)
+        CK(gemm_full(true, false, (int)m, (int)j, NB, -1.0, 1, Cb, ld, R, ld, Wm + k * ld, ld, status, st));
+      // [R_adj D_adj] -= C_adj^T [B C]   (PAPER.md:311 and the C_adj^T B term of 319),
+      // split-K over the m rows with a fixed-order reduction
+      int splits, kps;
+      splitk_choice(m, k, &splits, &kps);
+      CK(gemm_splitk_tn(NB, (int)k, (int)m, splits, kps, Cb, ld, Lw + k * ld, ld, Pbuf, status, st));
+      CK(splitk_reduce_sub(Pbuf, splits, NB, (int)k, Wm + j * ld, ld, status, st));
+    }
+    // D_adj = transpose(D) * D_adj; copy_lower_tri_to_upper_tri
+    CK(gemm128(true, true, false, false, D, ld, Dbar, ld, T1, NB, status, st));
+    // D = transpose(lower_triangular_inverse(D)); D_adj = D * transpose(D * D_adj)
+    // computed as S = D^-T sym(P) D^-1
+    CK(gemm128(true, false, false, true, Db, NB, T1, NB, T2, NB, status, st));
+    CK(gemm128(false, false, false, false, T2, NB, Db, NB, T3, NB, status, st));
+    // copy_lower_tri_to_upper_tri; diagonal * 0.5; set_zeros_in_upper_tri
+    CK(phi_sym(T3, T4, Dbar, ld, status, st));
+    // R_adj = R_adj - D_adj * R
+    if (j > 0) CK(gemm_full(true, false, NB, (int)j, NB, -1.0, 1, T4, NB, R, ld, Wm + j * ld, ld, status, st));
+  }
+  return STAN_CL_OK;
+}
+
+int adjoint_enqueue(int64_t n, const double* L, const double* Lbar, double* Abar, int* d_info) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) {
+    if (d_info) CK(cudaMemsetAsync(d_info, 0, sizeof(int), g.stream));
+    return STAN_CL_OK;
+  }
+  if (!L || !Lbar || !Abar) return STAN_CL_EINVAL;
+  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  if (ranges_overlap(L, Abar, bytes)) return STAN_CL_EINVAL;
+  if (Lbar != Abar && ranges_overlap(Lbar, Abar, bytes)) return STAN_CL_EINVAL;
+  const AdjPlan plan = adj_plan(n);
+  int rc = ensure_ws(plan.total);
+  if (rc) return rc;
+  int* status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  CK(check_diag(L, n, n, status, st));
+  const int64_t N = plan.N;
+  const bool fast = (N == n) && aligned16(L) && aligned16(Lbar) && aligned16(Abar);
+  if (fast) {
+    if (Lbar != Abar) CK(copy_lower_pad(Lbar, n, n, Abar, n, n, 0.0, st));
+    else CK(zero_upper(Abar, n, n, st));
+    rc = adjoint_inplace(L, Abar, n, n, status, plan);
+    if (rc) return rc;
+  } else {
+    double *Lw = nullptr, *Wm = nullptr;
+    rc = alloc_async(&Lw, (size_t)N * N * sizeof(double));
+    if (rc) return rc;
+    rc = alloc_async(&Wm, (size_t)N * N * sizeof(double));
+    if (rc) return rc;
+    CK(copy_lower_pad(L, n, n, Lw, N, N, 1.0, st));
+    CK(copy_lower_pad(Lbar, n, n, Wm, N, N, 0.0, st));
+    rc = adjoint_inplace(Lw, Wm, N, N, status, plan);
+    if (rc) return rc;
+    CK(copy_lower_out(Wm, N, Abar, n, n, st));
+    CK(cudaFreeAsync(Lw, st));
+    CK(cudaFreeAsync(Wm, st));
+  }
+  if (d_info) CK(cudaMemcpyAsync(d_info, status, sizeof(int), cudaMemcpyDeviceToDevice, st));
+  return STAN_CL_OK;
+}
+
+int read_status() {
+  int rc = ensure_host_status();
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(g.h_status, g.ws, sizeof(int), cudaMemcpyDeviceToHost, g.stream));
+  CK(cudaStreamSynchronize(g.stream));
+  return *g.h_status;
+}
+
+}  // namespace
+
+// ===================================================================== C ABI
+extern "C" {
+
+int stan_cl_cholesky_async(int64_t n, const double* A, double* L, int* d_info) {
+  return cholesky_enqueue(n, A, L, d_info);
+}
+
+int stan_cl_cholesky(int64_t n, const double* A, double* L) {
+  int rc = cholesky_enqueue(n, A, L, nullptr);
+  if (rc || n == 0) return rc;
+  return read_status();
+}
+
+int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_bar, double* A_bar,
+                                   int* d_info) {
+  return adjoint_enqueue(n, L, L_bar, A_bar, d_info);
+}
+
+int stan_cl_cholesky_adjoint(int64_t n, const double* L, const double* L_bar, double* A_bar) {
+  int rc = adjoint_enqueue(n, L, L_bar, A_bar, nullptr);
+  if (rc || n == 0) return rc;
+  return read_status();
+}
+
+int stan_cl_gp_exp_quad_cov(int64_t n, const double* x, double alpha, double rho, double jitter,
+                            double* K) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!x || !K) return STAN_CL_EINVAL;
+  if (!(rho != 0.0) || !(rho - rho == 0.0)) return STAN_CL_EINVAL;
+  CK(se_cov(n, x, alpha, rho, jitter, K, g.stream));
+  return STAN_CL_OK;
+}
+
+int stan_cl_cholesky_host(int64_t n, const double* A, double* L) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!A || !L) return STAN_CL_EINVAL;
+  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  double* dA = nullptr;
+  int rc = alloc_async(&dA, bytes);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(dA, A, bytes, cudaMemcpyHostToDevice, g.stream));
+  rc = cholesky_enqueue(n, dA, dA, nullptr);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(L, dA, bytes, cudaMemcpyDeviceToHost, g.stream));
+  CK(cudaFreeAsync(dA, g.stream));
+  return read_status();
+}
+
+int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
+  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  double *dL = nullptr, *dB = nullptr;
+  int rc = alloc_async(&dL, bytes);
+  if (rc) return rc;
+  rc = alloc_async(&dB, bytes);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(dL, L, bytes, cudaMemcpyHostToDevice, g.stream));
+  CK(cudaMemcpyAsync(dB, L_bar, bytes, cudaMemcpyHostToDevice, g.stream));
+  rc = adjoint_enqueue(n, dL, dB, dB, nullptr);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(A_bar, dB, bytes, cudaMemcpyDeviceToHost, g.stream));
+  CK(cudaFreeAsync(dL, g.stream));
+  CK(cudaFreeAsync(dB, g.stream));
+  return read_status();
+}
+
+int stan_cl_set_stream(void* s) {
+  g.stream = (cudaStream_t)s;
+  return STAN_CL_OK;
+}
+
+void* stan_cl_get_stream(void) { return (void*)g.stream; }
+
+int stan_cl_set_block_size(int nb) {
+  if (nb == 0 || nb == NB) {
+    g.nb = NB;
+    return STAN_CL_OK;
+  }
+  return STAN_CL_EINVAL;
+}
+
+int stan_cl_get_block_size(void) { return g.nb; }
+
+size_t stan_cl_workspace_bytes(int64_t n) {
+  if (n <= 0) return 0;
+  const AdjPlan p = adj_plan(n);
+  size_t pad = (p.N == n) ? 0 : 2 * (size_t)p.N * p.N * sizeof(double);
+  return p.total + pad;
+}
+
+const char* stan_cl_status_string(int status) {
+  switch (status) {
+    case STAN_CL_OK: return "ok";
+    case STAN_CL_EINVAL: return "invalid argument";
+    case STAN_CL_ENOMEM: return "device workspace allocation failed";
+    case STAN_CL_ECUDA: return g.last_err[0] ? g.last_err : "CUDA error";
+    case STAN_CL_ENCCL: return "NCCL error";
+    default: return status > 0 ? "numerical failure (not positive definite / bad diagonal)" : "unknown status";
+  }
+}
+
+long long stan_cl_kernel_launches(void) { return launches(); }
+
+int stan_cl_finalize(void) {
+  if (g.ws) {
+    cudaStreamSynchronize(g.stream);
+    cudaFree(g.ws);
+    g.ws = nullptr;
+    g.ws_cap = 0;
+  }
+  if (g.h_status) {
+    cudaFreeHost(g.h_status);
+    g.h_status = nullptr;
+  }
+  return STAN_CL_OK;
+}
+
+int stan_cl_version(void) { return 100; }
+
+}  // extern "C"

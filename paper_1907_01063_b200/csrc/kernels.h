@@ -1,0 +1,69 @@
+// kernels.h -- host-side launchers for the libstancl CUDA kernels (internal).
+// Every launcher enqueues on `st` and returns the launch error (no sync).
+// All matrices are row-major with an explicit leading dimension (doubles).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace stancl {
+
+// ---- launch accounting (gpu_launches in bench.py) ----
+void count_launch(int k = 1);
+long long launches();
+
+// ---- F0: SE covariance (K1) ----
+cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
+                   cudaStream_t st);
+
+// ---- layout helpers (K11) ----
+// dst[N x N] (ldd) <- lower(src[n x n], lds) with +0.0 strict upper; rows/cols >= n
+// become diag_pad * I (diag_pad = 1 for L/A, 0 for adjoints).  N >= n.
+cudaError_t copy_lower_pad(const double* src, int64_t n, int64_t lds, double* dst, int64_t N,
+                           int64_t ldd, double diag_pad, cudaStream_t st);
+// dst[n x n] (ldd) <- lower(src) (lds), strict upper written +0.0
+cudaError_t copy_lower_out(const double* src, int64_t lds, double* dst, int64_t n, int64_t ldd,
+                           cudaStream_t st);
+// zero the strict upper triangle in place
+cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st);
+
+// ---- F1/F2: diagonal tile POTRF (K2) and panel TRSM (K3), NB = 128 ----
+// factor W[k0:k0+128, k0:k0+128] in place (lower); on failure status = k0 + j + 1
+cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStream_t st);
+// rows [r0, r1) of columns [k0, k0+128): X <- X L11^-T (L11 = W[k0.., k0..]), substitution
+cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
+                       cudaStream_t st);
+
+// ---- DMMA GEMM family (F3, R1, R2, R3, R5) ----
+// C[M x N] = beta*C + sign * op(A) op(B)   (see gemm_dmma.cuh)
+//   a_kmaj: A is M x K row-major (else K x M);  b_kmaj: B is N x K (else K x N)
+cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
+                      const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                      int64_t ldc, const int* status, cudaStream_t st);
+// lower tiles of square C[M x M] -= A A'^T style: C -= A B^T, A, B both k-major (SYRK)
+cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                          double* C, int64_t ldc, const int* status, cudaStream_t st);
+// split-K: P[z][M][N] = op(A) op(B) over K range z*kps..; a_kmaj=false, b_kmaj=false only
+cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const double* A, int64_t lda,
+                           const double* B, int64_t ldb, double* P, const int* status,
+                           cudaStream_t st);
+// dst[r][c] -= sum_{z=0}^{splits-1} P[z][r][c]  (fixed order), r < M, c < N
+cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double* dst, int64_t ldd,
+                              const int* status, cudaStream_t st);
+
+// ---- adjoint diagonal-block helpers (R4, R5) ----
+// Dinv[b] = (W[b*128.., b*128..])^-1 for b in [0, nblk), lower, by substitution
+cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* Dinv,
+                                const int* status, cudaStream_t st);
+// C[128x128] (ldc) = op(A) op(B) over K = 128; a_t: A given as K x M; a_tril: only the
+// lower triangle of A's storage is read (upper taken as 0); b_t: B given as N x K;
+// b_sym: B read as sym(tril(B)) i.e. B[max][min]
+cudaError_t gemm128(bool a_t, bool a_tril, bool b_t, bool b_sym, const double* A, int64_t lda,
+                    const double* B, int64_t ldb, double* C, int64_t ldc, const int* status,
+                    cudaStream_t st);
+// S (128x128, ld 128): Ssym = mirror(tril(S)) -> ws; Dbar = Phi(S) = tril(S) with halved diagonal
+cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, const int* status,
+                    cudaStream_t st);
+// status = first k+1 with !(L[k][k] > 0 && finite), k < n
+cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st);
+
+}  // namespace stancl

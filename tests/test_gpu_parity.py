@@ -1,0 +1,229 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): relative Frobenius error <= 1e-11 for L and
+<= 1e-9 for A_bar, with the SAME input bits on both sides (the oracle's K for
+the forward, the oracle's L for the adjoint).  Integer work
+(the integer-exact families, status codes) is compared bit-exactly.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1907_01063_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+
+L_BAR_TOL = 1e-11
+A_BAR_TOL = 1e-9
+
+
+@pytest.fixture(scope="module")
+def sc():
+    import paper_1907_01063_b200 as m
+    m.load()
+    return m
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.cpu().numpy()
+
+
+def relf(a, b):
+    nb = np.linalg.norm(b)
+    return float(np.linalg.norm(a - b) / (nb if nb > 0 else 1.0))
+
+
+def se(n, seed=inputs.X_SEED, jitter=1e-6):
+    return oracle.se_cov(inputs.gp_x(n, seed), 1.0, 1.0, jitter)
+
+
+SIZES = [1, 2, 3, 31, 64, 100, 127, 128, 129, 255, 256, 300, 511, 512, 1000, 1024]
+
+
+# ------------------------------------------------------------------ SE builder
+@pytest.mark.parametrize("n", [1, 7, 64, 300, 1024])
+def test_se_cov_matches_oracle(sc, n):
+    x = inputs.gp_x(n)
+    for alpha, rho, jit in [(1.0, 1.0, 1e-6), (2.5, 0.3, 0.0), (0.7, 5.5, 1e-3)]:
+        want = oracle.se_cov(x, alpha, rho, jit)
+        got = host(sc.gp_exp_quad_cov(dev(x), alpha, rho, jit))
+        # CUDA exp vs libm exp differ by <= 2 ulp; everything else is exact
+        assert np.all(np.abs(got - want) <= 4 * np.finfo(float).eps * np.abs(want) + 1e-300)
+        assert np.array_equal(got, got.T)
+        assert np.all(np.diag(got) == alpha * alpha + jit)
+
+
+# --------------------------------------------------------------------- forward
+@pytest.mark.parametrize("n", SIZES)
+def test_cholesky_parity_se(sc, n):
+    K = se(n)
+    want = oracle.cholesky(K)
+    got = host(sc.cholesky(dev(K)))
+    assert relf(got, want) <= L_BAR_TOL
+    up = got[np.triu_indices(n, 1)]
+    assert np.all(up == 0) and not np.any(np.signbit(up))
+
+
+@pytest.mark.parametrize("n", [3, 130, 700])
+def test_cholesky_parity_toeplitz(sc, n):
+    A = inputs.toeplitz(n)                       # the paper's benchmark matrix
+    assert relf(host(sc.cholesky(dev(A))), oracle.cholesky(A)) <= 1e-14
+
+
+@pytest.mark.parametrize("n", [64, 200, 1000, 1024, 2048])
+def test_cholesky_integer_exact(sc, n):
+    L0 = inputs.unit_lower_pm1(n, seed=n)
+    A = inputs.gram_exact(L0)
+    assert np.array_equal(host(sc.cholesky(dev(A))), L0)
+
+
+def test_cholesky_in_place_and_upper_garbage(sc):
+    n = 384
+    K = se(n)
+    want = oracle.cholesky(K)
+    G = K.copy()
+    G[np.triu_indices(n, 1)] = np.nan
+    t = dev(G)
+    sc.cholesky(t, out=t)                         # A == L
+    assert relf(host(t), want) <= L_BAR_TOL
+    assert np.all(host(t)[np.triu_indices(n, 1)] == 0)
+    t2 = dev(G[:300, :300].copy())                # ragged (padded) path, in place
+    sc.cholesky(t2, out=t2)
+    assert relf(host(t2), oracle.cholesky(K[:300, :300])) <= L_BAR_TOL
+
+
+def test_cholesky_not_pd(sc):
+    for A, info in [(np.array([[1.0, 2.0], [2.0, 1.0]]), 2), (np.array([[-1.0]]), 1)]:
+        with pytest.raises(sc.NotPositiveDefinite) as e:
+            sc.cholesky(dev(A))
+        assert e.value.info == info
+    for n, r in [(64, 10), (300, 200), (1024, 1000), (1024, 128), (512, 0)]:
+        A = inputs.toeplitz(n)
+        A[r, r] = -1e12
+        with pytest.raises(sc.NotPositiveDefinite) as e:
+            sc.cholesky(dev(A))
+        assert e.value.info == r + 1 == oracle.cholesky_info(A)[1]
+        A = inputs.toeplitz(n)
+        A[r, r] = np.nan
+        with pytest.raises(sc.NotPositiveDefinite) as e:
+            sc.cholesky(dev(A))
+        assert e.value.info == r + 1
+
+
+def test_cholesky_empty_and_errors(sc):
+    lib = sc.load()
+    assert lib.stan_cl_cholesky(0, None, None) == 0
+    assert lib.stan_cl_cholesky(-1, None, None) == -1
+    assert lib.stan_cl_cholesky(4, None, None) == -1
+    t = torch.zeros(8, 8, dtype=torch.float64, device="cuda")
+    # partial overlap of A and L is rejected
+    assert lib.stan_cl_cholesky(4, t.data_ptr(), t.data_ptr() + 8) == -1
+    assert lib.stan_cl_gp_exp_quad_cov(4, t.data_ptr(), 1.0, 0.0, 0.0, t.data_ptr()) == -1
+
+
+def test_cholesky_non_default_stream(sc):
+    n = 512
+    K = se(n)
+    want = oracle.cholesky(K)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        A = dev(K)
+        L = sc.cholesky(A)
+    s.synchronize()
+    assert relf(host(L), want) <= L_BAR_TOL
+
+
+def test_cholesky_deterministic(sc):
+    K = dev(se(1024))
+    a = sc.cholesky(K)
+    b = sc.cholesky(K)
+    assert torch.equal(a, b)
+
+
+# --------------------------------------------------------------------- adjoint
+@pytest.mark.parametrize("n", SIZES)
+def test_adjoint_parity_se(sc, n):
+    L = oracle.cholesky(se(n))                    # same L bits on both sides
+    W = inputs.lbar(n)
+    want = oracle.cholesky_adjoint(L, W)
+    got = host(sc.cholesky_adjoint(dev(L), dev(W)))
+    assert relf(got, want) <= A_BAR_TOL
+    up = got[np.triu_indices(n, 1)]
+    assert np.all(up == 0) and not np.any(np.signbit(up))
+
+
+@pytest.mark.parametrize("n", [130, 512])
+def test_adjoint_parity_toeplitz(sc, n):
+    L = oracle.cholesky(inputs.toeplitz(n))
+    W = inputs.lbar(n, seed=5)
+    assert relf(host(sc.cholesky_adjoint(dev(L), dev(W))), oracle.cholesky_adjoint(L, W)) <= 1e-12
+
+
+@pytest.mark.parametrize("n,band", [(256, 1), (256, 2), (1024, 2), (1000, 1)])
+def test_adjoint_integer_exact(sc, n, band):
+    L = inputs.unit_lower_pm1(n, seed=3, band=band)
+    W = inputs.int_lbar(n, seed=4)
+    want = oracle.cholesky_adjoint(L, W)
+    assert np.array_equal(host(sc.cholesky_adjoint(dev(L), dev(W))), want)
+
+
+def test_adjoint_in_place_and_upper_garbage(sc):
+    n = 384
+    L = oracle.cholesky(se(n))
+    W = inputs.lbar(n)
+    want = oracle.cholesky_adjoint(L, W)
+    Lg, Wg = L.copy(), W.copy()
+    Lg[np.triu_indices(n, 1)] = np.nan
+    Wg[np.triu_indices(n, 1)] = np.nan
+    t = dev(Wg)
+    sc.cholesky_adjoint(dev(Lg), t, out=t)
+    assert relf(host(t), want) <= A_BAR_TOL
+    assert np.all(host(t)[np.triu_indices(n, 1)] == 0)
+
+
+def test_adjoint_bad_diagonal_and_errors(sc):
+    lib = sc.load()
+    L = np.eye(300)
+    L[150, 150] = 0.0
+    with pytest.raises(ValueError):
+        sc.cholesky_adjoint(dev(L), dev(np.eye(300)))
+    Ld = dev(L)
+    out = torch.empty_like(Ld)
+    assert lib.stan_cl_cholesky_adjoint(300, Ld.data_ptr(), Ld.data_ptr(), out.data_ptr()) == 151
+    assert lib.stan_cl_cholesky_adjoint(300, Ld.data_ptr(), out.data_ptr(), Ld.data_ptr()) == -1  # A_bar == L
+    assert lib.stan_cl_cholesky_adjoint(0, None, None, None) == 0
+
+
+def test_adjoint_zero_seed(sc):
+    n = 256
+    L = oracle.cholesky(se(n))
+    got = host(sc.cholesky_adjoint(dev(L), dev(np.zeros((n, n)))))
+    assert np.array_equal(got, np.zeros((n, n)))
+
+
+# ----------------------------------------------------------- host-buffer API
+def test_host_entry_points(sc):
+    n = 640
+    K = se(n)
+    A = torch.from_numpy(K.copy()).pin_memory()
+    L = torch.empty_like(A).pin_memory()
+    assert sc.cholesky_host(A, L) == 0
+    assert relf(L.numpy(), oracle.cholesky(K)) <= L_BAR_TOL
+    Lo = oracle.cholesky(K)
+    W = inputs.lbar(n)
+    Ab = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    assert sc.cholesky_adjoint_host(torch.from_numpy(Lo), torch.from_numpy(W), Ab) == 0
+    assert relf(Ab.numpy(), oracle.cholesky_adjoint(Lo, W)) <= A_BAR_TOL
+
+
+def test_kernel_launch_counter(sc):
+    before = sc.kernel_launches()
+    sc.cholesky(dev(se(256)))
+    assert sc.kernel_launches() > before
