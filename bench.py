@@ -1,0 +1,320 @@
+#!/usr/bin/env python
+"""bench.py -- FP64 Cholesky + adjoint on B200 (arXiv:1907.01063 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--n 16384] [--impl ours|reference]
+
+One step = one pass of the whole hot path over one synthetic GP problem at
+n = 16384 (BASELINE.json configs[3], the configuration the metric is quoted on):
+SE covariance build from x (F0), Cholesky (F1-F4), adjoint (R0-R5), all through
+the C ABI with device-resident inputs.  Flops counted: n^3/3 + 2n^3/3 (SURVEY.md
+§8 convention; the O(n^2) SE build is timed but not counted).
+
+Prints ONE JSON line on rank 0.  Multi-GPU (torchrun): replicas -- every rank
+factors its own matrix, value = sum over ranks, time = max over
+ranks.  ``--impl reference`` times the CPU oracle (oracle/, single thread) on a
+bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "FP64 Cholesky+adjoint GFLOP/s and ms at n=16384; fraction of B200 FP64 peak"
+UNIT = "GFLOP/s"
+ALPHA, RHO, JITTER = 1.0, 1.0, 1e-6
+# FP64 peak: DMMA (mma.sync .f64) register-resident microbenchmark on this pool's
+# B200s, 37.15 TFLOP/s at 1965 MHz (profiles/fp64_peak_r01.jsonl; tools/fp64_peak.cu).
+# MEASURED_PEAKS.json carries no FP64 figure; its bf16 numbers do not apply.
+FP64_PEAK_TFLOPS = 37.1
+PEAK_SOURCE = "measured: tools/fp64_peak.cu DMMA.8x8x4 loop, 148 SMs, profiles/fp64_peak_r01.jsonl"
+ORACLE_SAMPLE_N = 2048
+
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+
+def config(n: int, world: int) -> dict:
+    return {
+        "workload": f"SE-kernel GP covariance n={n} (1-D x~U(-10,10), alpha=rho=1, jitter 1e-6): "
+                    "SE build + Cholesky + adjoint (BASELINE.json configs[3])",
+        "n": n, "nb": 128, "flops_per_step": n ** 3,
+        "flop_convention": "n^3/3 (Cholesky) + 2n^3/3 (adjoint)",
+        "l2": "inputs exceed L2 (one n x n FP64 matrix = %.1f GiB vs 126 MB L2); no flush needed" % (8 * n * n / 2 ** 30),
+        "parallelism": "replicas" if world > 1 else "single",
+    }
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle sampling during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                bits = int(parts[3], 16)
+            except ValueError:
+                continue
+            for b, name in REASON_BITS.items():
+                if bits & b and name != "gpu_idle":
+                    reasons.add(name)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def traffic_from_profiles(kind: str):
+    """dram bytes per launch of `kind` from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d.get(kind)
+    except Exception:
+        return None
+
+
+def run_oracle_sample(n: int) -> tuple[float, float]:
+    """Oracle Cholesky + adjoint at order n on one core: (seconds, flops)."""
+    import oracle
+    from paper_1907_01063_b200 import inputs
+    K = oracle.se_cov(inputs.gp_x(n), ALPHA, RHO, JITTER)
+    W = inputs.lbar(n)
+    t0 = time.perf_counter()
+    L = oracle.cholesky(K)
+    oracle.cholesky_adjoint(L, W)
+    return time.perf_counter() - t0, float(n) ** 3
+
+
+def cpu_baseline_entry(n_sample: int) -> dict:
+    secs, fl = run_oracle_sample(n_sample)
+    return {"value": fl / secs / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle (oracle/oracle.c, 1 thread, -O2 -ffp-contract=off) Cholesky + adjoint of the "
+                      f"same SE-GP workload at n={n_sample} instead of 16384, one run, {secs:.2f} s; "
+                      f"host {os.cpu_count()} logical cores"}
+
+
+def bench_reference(args, rank: int, world: int):
+    if rank != 0:
+        return
+    n_s = args.oracle_n
+    for _ in range(args.warmup):
+        run_oracle_sample(n_s)
+    times = []
+    for _ in range(args.steps):
+        s, fl = run_oracle_sample(n_s)
+        times.append(s)
+    ms = 1e3 * statistics.mean(times)
+    val = float(n_s) ** 3 / (ms / 1e3) / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config(args.n, world),
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
+                         "sample": f"each step = oracle Cholesky + adjoint at n={n_s} (bounded sample of the "
+                                   f"n={args.n} workload), 1 thread"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def bench_ours(args, rank: int, world: int, local_rank: int):
+    import numpy as np
+    import torch
+    import paper_1907_01063_b200 as sc
+    from paper_1907_01063_b200 import inputs
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n = args.n
+    sc.load()
+    x = torch.from_numpy(inputs.gp_x(n, seed=inputs.X_SEED + rank)).to(dev)
+    Lbar = torch.from_numpy(inputs.lbar(n, seed=inputs.LBAR_SEED + rank)).to(dev)
+    K = torch.empty((n, n), dtype=torch.float64, device=dev)
+    Abar = torch.empty_like(K)
+
+    def step():
+        sc.gp_exp_quad_cov(x, ALPHA, RHO, JITTER, out=K)      # F0
+        sc.cholesky(K, out=K)                                 # F1-F4 (in place)
+        sc.cholesky_adjoint(K, Lbar, out=Abar)                # R0-R5
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier(device_ids=[local_rank])
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with sampler:
+        time.sleep(0.3)
+        launches0 = sc.kernel_launches()
+        sc.profile_reset()
+        sc.profile_enable(True)
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        sc.profile_enable(False)
+        launches = sc.kernel_launches() - launches0
+        prof = sc.profile_read()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    ms_max = float(t.item())
+    flops = float(n) ** 3
+    value = world * flops / (ms_max / 1e3) / 1e9
+    clocks = sampler.summary()
+
+    # roofline of the dominant kernel class (by summed event time)
+    dmma = {k: prof[k] for k in ("syrk", "adj_gemm", "splitk")}
+    dom = max(dmma, key=lambda k: dmma[k]["ms"])
+    d = prof[dom]
+    achieved = d["flops"] / (d["ms"] / 1e3) / 1e12 if d["ms"] > 0 else 0.0
+    tr = traffic_from_profiles(dom)
+    roofline = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS,
+                "traffic": tr, "peak_source": PEAK_SOURCE,
+                "per_launch_ms": d["ms"] / max(d["launches"], 1), "launches": d["launches"] // args.steps}
+    classes = {k: {"ms_per_step": v["ms"] / args.steps,
+                   "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] > 0 and v["flops"] > 0 else None,
+                   "launches_per_step": v["launches"] // args.steps} for k, v in prof.items()}
+
+    # end-to-end through the public host-buffer API (pinned host in/out)
+    e2e = None
+    if args.e2e_steps > 0:
+        Kh = torch.empty((n, n), dtype=torch.float64).pin_memory()
+        sc.gp_exp_quad_cov(x, ALPHA, RHO, JITTER, out=K)
+        Kh.copy_(K)
+        Lh = torch.empty_like(Kh).pin_memory()
+        Lbh = torch.empty_like(Kh).pin_memory()
+        Lbh.copy_(Lbar)
+        Abh = torch.empty_like(Kh).pin_memory()
+        torch.cuda.synchronize()
+
+        def e2e_step():
+            sc.cholesky_host(Kh, Lh, device=local_rank)
+            sc.cholesky_adjoint_host(Lh, Lbh, Abh, device=local_rank)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        f1.record()
+        torch.cuda.synchronize()
+        ems = f0.elapsed_time(f1) / args.e2e_steps
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if world > 1:
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+        ems = float(te.item())
+        e2e = {"value": world * flops / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": 3 * 8 * n * n, "d2h_bytes_per_step": 2 * 8 * n * n,
+               "path": "stan_cl_cholesky_host(K) + stan_cl_cholesky_adjoint_host(L, L_bar), pinned host buffers"}
+        del Kh, Lh, Lbh, Abh
+
+    if rank != 0:
+        return
+    cpu = None if args.no_cpu_baseline else cpu_baseline_entry(args.oracle_n)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config(n, world),
+        "fp64_peak_frac": (flops / (ms_max / 1e3) / 1e12) / FP64_PEAK_TFLOPS,
+        "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": clocks, "kernel_classes": classes,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--oracle-n", type=int, default=ORACLE_SAMPLE_N)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        ap.error("--warmup must be >= 3")
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        bench_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        bench_ours(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch
+            torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -23,6 +23,7 @@ __all__ = [
     "cholesky", "cholesky_adjoint", "gp_exp_quad_cov", "cholesky_async", "cholesky_adjoint_async",
     "cholesky_host", "cholesky_adjoint_host", "kernel_launches", "library_path", "load",
     "StanClError", "NotPositiveDefinite", "STATUS", "workspace_bytes", "finalize",
+    "profile_enable", "profile_reset", "profile_read", "PROFILE_KINDS",
 ]
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
@@ -49,6 +50,10 @@ SIGNATURES = {
     "stan_cl_workspace_bytes": (ctypes.c_size_t, [_I64]),
     "stan_cl_status_string": (ctypes.c_char_p, [_I]),
     "stan_cl_kernel_launches": (ctypes.c_longlong, []),
+    "stan_cl_profile_enable": (_I, [_I]),
+    "stan_cl_profile_reset": (_I, []),
+    "stan_cl_profile_read": (_I, [_I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                                  ctypes.POINTER(ctypes.c_longlong)]),
     "stan_cl_finalize": (_I, []),
     "stan_cl_version": (_I, []),
 }
@@ -198,6 +203,27 @@ def cholesky_adjoint_host(L: torch.Tensor, Lbar: torch.Tensor, Abar: torch.Tenso
 
 def kernel_launches() -> int:
     return int(load().stan_cl_kernel_launches())
+
+
+PROFILE_KINDS = ["syrk", "adj_gemm", "splitk", "potrf", "trsm", "tri_inverse", "gemm128", "se_cov", "other"]
+
+
+def profile_enable(on: bool = True) -> None:
+    load().stan_cl_profile_enable(1 if on else 0)
+
+
+def profile_reset() -> None:
+    load().stan_cl_profile_reset()
+
+
+def profile_read() -> dict:
+    """{class: {"ms": summed event ms, "flops": algorithmic flops, "launches": n}}"""
+    out = {}
+    for k, name in enumerate(PROFILE_KINDS):
+        ms, fl, cnt = ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
+        load().stan_cl_profile_read(k, ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(cnt))
+        out[name] = {"ms": ms.value, "flops": fl.value, "launches": cnt.value}
+    return out
 
 
 def workspace_bytes(n: int) -> int:

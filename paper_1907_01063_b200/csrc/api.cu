@@ -400,6 +400,22 @@ const char* stan_cl_status_string(int status) {
 
 long long stan_cl_kernel_launches(void) { return launches(); }
 
+int stan_cl_profile_enable(int on) {
+  prof_enable(on != 0);
+  return STAN_CL_OK;
+}
+
+int stan_cl_profile_reset(void) {
+  prof_reset();
+  return STAN_CL_OK;
+}
+
+int stan_cl_profile_read(int kind, double* ms, double* flops, long long* n) {
+  if (kind < 0 || kind >= PROF_KINDS || !ms || !flops || !n) return STAN_CL_EINVAL;
+  prof_read(kind, ms, flops, n);
+  return STAN_CL_OK;
+}
+
 int stan_cl_finalize(void) {
   if (g.ws) {
     cudaStreamSynchronize(g.stream);

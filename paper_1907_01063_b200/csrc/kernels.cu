@@ -14,6 +14,7 @@
 //       splitk_reduce_sub (the paper's large-k reduction)
 #include <atomic>
 #include <climits>
+#include <vector>
 
 #include "common.cuh"
 #include "gemm_dmma.cuh"
@@ -24,6 +25,73 @@ namespace stancl {
 static std::atomic<long long> g_launches{0};
 void count_launch(int k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 long long launches() { return g_launches.load(std::memory_order_relaxed); }
+
+// ---- per-kernel-class CUDA-event timing (stan_cl_profile_*) ----
+namespace {
+struct ProfRec {
+  int kind;
+  double flops;
+  cudaEvent_t e0, e1;
+};
+struct ProfState {
+  bool on = false;
+  std::vector<ProfRec> recs;
+  std::vector<cudaEvent_t> pool;
+  double ms[PROF_KINDS] = {0};
+  double flops[PROF_KINDS] = {0};
+  long long count[PROF_KINDS] = {0};
+};
+ProfState g_prof;
+cudaEvent_t prof_event() {
+  if (!g_prof.pool.empty()) {
+    cudaEvent_t e = g_prof.pool.back();
+    g_prof.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+}  // namespace
+
+Prof::Prof(int kind, double flops, cudaStream_t st) : kind_(kind), flops_(flops), st_(st) {
+  count_launch();
+  if (g_prof.on) {
+    e0_ = prof_event();
+    e1_ = prof_event();
+    cudaEventRecord(e0_, st_);
+  }
+}
+Prof::~Prof() {
+  if (g_prof.on && e0_) {
+    cudaEventRecord(e1_, st_);
+    g_prof.recs.push_back({kind_, flops_, e0_, e1_});
+  }
+}
+void prof_enable(bool on) { g_prof.on = on; }
+void prof_collect() {
+  for (auto& r : g_prof.recs) {
+    cudaEventSynchronize(r.e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, r.e0, r.e1);
+    g_prof.ms[r.kind] += ms;
+    g_prof.flops[r.kind] += r.flops;
+    g_prof.count[r.kind] += 1;
+    g_prof.pool.push_back(r.e0);
+    g_prof.pool.push_back(r.e1);
+  }
+  g_prof.recs.clear();
+}
+void prof_reset() {
+  prof_collect();
+  for (int k = 0; k < PROF_KINDS; ++k) g_prof.ms[k] = g_prof.flops[k] = 0, g_prof.count[k] = 0;
+}
+void prof_read(int kind, double* ms, double* flops, long long* count) {
+  prof_collect();
+  *ms = g_prof.ms[kind];
+  *flops = g_prof.flops[kind];
+  *count = g_prof.count[kind];
+}
 
 static inline int grid_for(long long work, int threads, int cap = 148 * 16) {
   long long b = (work + threads - 1) / threads;
@@ -50,11 +118,11 @@ __global__ void se_cov_kernel(int64_t n, const double* __restrict__ x, double sq
 
 cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
                    cudaStream_t st) {
+  Prof prof_(PROF_SE, 0.0, st);
   if (n == 0) return cudaSuccess;
   const double sq_alpha = alpha * alpha;
   const double c = -0.5 / (rho * rho);
   se_cov_kernel<<<grid_for((long long)n * n, 256), 256, 0, st>>>(n, x, sq_alpha, c, jitter, K);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -75,10 +143,10 @@ __global__ void copy_lower_pad_kernel(const double* __restrict__ src, int64_t n,
 
 cudaError_t copy_lower_pad(const double* src, int64_t n, int64_t lds, double* dst, int64_t N,
                            int64_t ldd, double diag_pad, cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st);
   if (N == 0) return cudaSuccess;
   copy_lower_pad_kernel<<<grid_for((long long)N * N, 256), 256, 0, st>>>(src, n, lds, dst, N, ldd,
                                                                           diag_pad);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -94,9 +162,9 @@ __global__ void copy_lower_out_kernel(const double* __restrict__ src, int64_t ld
 
 cudaError_t copy_lower_out(const double* src, int64_t lds, double* dst, int64_t n, int64_t ldd,
                            cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st);
   if (n == 0) return cudaSuccess;
   copy_lower_out_kernel<<<grid_for((long long)n * n, 256), 256, 0, st>>>(src, lds, dst, n, ldd);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -110,9 +178,9 @@ __global__ void zero_upper_kernel(double* A, int64_t n, int64_t ld) {
 }
 
 cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st);
   if (n == 0) return cudaSuccess;
   zero_upper_kernel<<<grid_for((long long)n * n, 256), 256, 0, st>>>(A, n, ld);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -168,6 +236,7 @@ __global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t l
 }
 
 cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStream_t st) {
+  Prof prof_(PROF_POTRF, (double)NB * NB * NB / 3.0, st);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(potrf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -176,7 +245,6 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
     attr = true;
   }
   potrf_tile_kernel<<<1, 256, POTRF_SMEM, st>>>(W, ld, k0, status);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -229,6 +297,7 @@ __global__ void __launch_bounds__(256, 1) trsm_panel_kernel(double* W, int64_t l
 
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st) {
+  Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st);
   if (r1 <= r0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -239,7 +308,6 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
   }
   const int blocks = (int)((r1 - r0) / TRSM_ROWS);
   trsm_panel_kernel<<<blocks, 256, TRSM_SMEM, st>>>(W, ld, k0, r0, status);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -247,9 +315,9 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st) {
+  Prof prof_(PROF_GEMM, 2.0 * M * N * K, st);
   if (M == 0 || N == 0) return cudaSuccess;
   GemmArgs p{A, lda, B, ldb, C, ldc, M, N, K, K, sign, beta, status};
-  count_launch();
   if (a_kmaj && b_kmaj) return launch_gemm<true, true, MODE_FULL>(p, 1, st);
   if (a_kmaj && !b_kmaj) return launch_gemm<true, false, MODE_FULL>(p, 1, st);
   if (!a_kmaj && b_kmaj) return launch_gemm<false, true, MODE_FULL>(p, 1, st);
@@ -258,18 +326,18 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
 
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                           double* C, int64_t ldc, const int* status, cudaStream_t st) {
+  Prof prof_(PROF_SYRK, (double)K * M * (M + 1.0), st);
   if (M == 0) return cudaSuccess;
   GemmArgs p{A, lda, B, ldb, C, ldc, M, M, K, K, -1.0, 1, status};
-  count_launch();
   return launch_gemm<true, true, MODE_LOWER>(p, 1, st);
 }
 
 cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const double* A, int64_t lda,
                            const double* B, int64_t ldb, double* P, const int* status,
                            cudaStream_t st) {
+  Prof prof_(PROF_SPLITK, 2.0 * M * N * K, st);
   if (M == 0 || N == 0) return cudaSuccess;
   GemmArgs p{A, lda, B, ldb, P, N, M, N, K, kps, 1.0, 0, status};
-  count_launch();
   return launch_gemm<false, false, MODE_SPLITK>(p, splits, st);
 }
 
@@ -298,10 +366,10 @@ __global__ void splitk_reduce_sub_kernel(const double* __restrict__ P, int split
 
 cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double* dst, int64_t ldd,
                               const int* status, cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st);
   if (M == 0 || N == 0) return cudaSuccess;
   splitk_reduce_sub_kernel<<<grid_for((long long)M * N / 2, 256), 256, 0, st>>>(P, splits, M, N, dst,
                                                                                 ldd, status);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -344,6 +412,7 @@ __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, in
 
 cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* Dinv,
                                 const int* status, cudaStream_t st) {
+  Prof prof_(PROF_TRINV, (double)nblk * NB * NB * NB / 3.0, st);
   if (nblk == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -353,7 +422,6 @@ cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* D
     attr = true;
   }
   tri_inverse_kernel<<<nblk, NB, TINV_SMEM, st>>>(L, ld, Dinv, status);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -434,6 +502,7 @@ __global__ void __launch_bounds__(128) gemm128_kernel(bool a_t, bool a_tril, boo
 cudaError_t gemm128(bool a_t, bool a_tril, bool b_t, bool b_sym, const double* A, int64_t lda,
                     const double* B, int64_t ldb, double* C, int64_t ldc, const int* status,
                     cudaStream_t st) {
+  Prof prof_(PROF_SMALL, 2.0 * NB * NB * NB, st);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -442,7 +511,6 @@ cudaError_t gemm128(bool a_t, bool a_tril, bool b_t, bool b_sym, const double* A
     attr = true;
   }
   gemm128_kernel<<<dim3(4, 4), 128, G128_SMEM, st>>>(a_t, a_tril, b_t, b_sym, A, lda, B, ldb, C, ldc, status);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -460,8 +528,8 @@ __global__ void phi_sym_kernel(const double* __restrict__ S, double* __restrict_
 
 cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, const int* status,
                     cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st);
   phi_sym_kernel<<<64, 256, 0, st>>>(S, Ssym, Dbar, ldd, status);
-  count_launch();
   return cudaGetLastError();
 }
 
@@ -482,9 +550,9 @@ __global__ void check_diag_kernel(const double* L, int64_t n, int64_t ld, int* s
 }
 
 cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st);
   if (n == 0) return cudaSuccess;
   check_diag_kernel<<<grid_for(n, 256, 148), 256, 0, st>>>(L, n, ld, status);
-  count_launch();
   return cudaGetLastError();
 }
 
