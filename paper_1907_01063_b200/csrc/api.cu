@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "../../include/stan_cl.h"
 #include "common.cuh"
@@ -26,6 +27,8 @@ namespace {
 
 struct State {
   cudaStream_t stream = nullptr;  // nullptr = legacy default stream
+  cudaStream_t side = nullptr;    // library-owned high-priority stream (panel lookahead)
+  std::vector<cudaEvent_t> events;
   int nb = NB;
   void* ws = nullptr;  // library-owned persistent workspace
   size_t ws_cap = 0;
@@ -141,16 +144,56 @@ int alloc_async(double** p, size_t bytes) {
 }
 
 // ------------------------------------------------------------------ forward
-// Right-looking blocked Cholesky on the N x N working matrix W (lower part).
+int ensure_side(size_t nevents) {
+  if (!g.side) {
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&g.side, cudaStreamNonBlocking, hi));
+  }
+  while (g.events.size() < nevents) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g.events.push_back(e);
+  }
+  return STAN_CL_OK;
+}
+
+// Right-looking blocked Cholesky on the N x N working matrix W (lower part),
+// PAPER.md:264-285 with a fixed block of NB, and one step of lookahead: the
+// panel of step k+1 (POTRF + TRSM, the latency-bound critical path) runs on the
+// high-priority side stream while the main stream applies the rest of step k's
+// trailing update.  Per step k (blocks of NB):
+//   main: wait panel k; A[k+1 col] -= L21 L21(k+1)^T        (lookahead column)
+//   side: POTRF(k+1); TRSM(k+1)                            (L11 = chol(A11); L21 = A21 L11^-T)
+//   main: A22[k+2.., k+2..] -= L21 L21^T (lower tiles)      (multiply_transpose)
 int factor_inplace(double* W, int64_t N, int64_t ld, int* status) {
-  cudaStream_t st = g.stream;
-  for (int64_t k0 = 0; k0 < N; k0 += NB) {
-    CK(potrf_tile(W, ld, k0, status, st));                       // L11 = chol(A11)
-    const int64_t r0 = k0 + NB;
-    if (r0 >= N) break;
-    CK(trsm_panel(W, ld, k0, r0, N, status, st));                // L21 = A21 L11^-T
-    const double* L21 = W + r0 * ld + k0;
-    CK(gemm_lower_nt((int)(N - r0), NB, L21, ld, L21, ld, W + r0 * ld + r0, ld, status, st));  // A22 -= L21 L21^T
+  cudaStream_t main = g.stream;
+  const int64_t T = N / NB;
+  int rc = ensure_side(2 * T + 2);
+  if (rc) return rc;
+  cudaStream_t side = g.side;
+  cudaEvent_t* ev = g.events.data();  // ev[0]: start; ev[1 + 2k]: panel k done; ev[2 + 2k]: column k+1 ready
+  CK(cudaEventRecord(ev[0], main));
+  CK(cudaStreamWaitEvent(side, ev[0], 0));
+  CK(potrf_tile(W, ld, 0, status, side));
+  if (T > 1) CK(trsm_panel(W, ld, 0, NB, N, status, side));
+  CK(cudaEventRecord(ev[1], side));
+  for (int64_t k = 0; k < T; ++k) {
+    CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
+    if (k == T - 1) break;
+    const int64_t c0 = k * NB, r1 = (k + 1) * NB, r2 = r1 + NB;
+    const double* L21 = W + r1 * ld + c0;
+    CK(gemm_full(true, true, (int)(N - r1), NB, NB, -1.0, 1, L21, ld, L21, ld, W + r1 * ld + r1, ld, status,
+                 main, /*lower_only=*/1, PROF_SYRK));
+    CK(cudaEventRecord(ev[2 + 2 * k], main));
+    CK(cudaStreamWaitEvent(side, ev[2 + 2 * k], 0));
+    CK(potrf_tile(W, ld, r1, status, side));
+    if (r2 < N) CK(trsm_panel(W, ld, r1, r2, N, status, side));
+    CK(cudaEventRecord(ev[1 + 2 * (k + 1)], side));
+    if (r2 < N) {
+      const double* L31 = W + r2 * ld + c0;
+      CK(gemm_lower_nt((int)(N - r2), NB, L31, ld, L31, ld, W + r2 * ld + r2, ld, status, main));
+    }
   }
   return STAN_CL_OK;
 }
@@ -426,6 +469,12 @@ int stan_cl_finalize(void) {
   if (g.h_status) {
     cudaFreeHost(g.h_status);
     g.h_status = nullptr;
+  }
+  for (cudaEvent_t e : g.events) cudaEventDestroy(e);
+  g.events.clear();
+  if (g.side) {
+    cudaStreamDestroy(g.side);
+    g.side = nullptr;
   }
   return STAN_CL_OK;
 }

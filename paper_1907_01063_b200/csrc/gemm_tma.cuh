@@ -1,0 +1,363 @@
+// gemm_tma.cuh -- the production FP64 tensor-core GEMM: persistent,
+// warp-specialised, TMA-fed DMMA tiles.
+//
+// Used by every O(n^3) step of the path:
+//   F3  SYRK trailing update   A22 -= L21 L21^T
+//   R3  rank-nb update         B_bar -= C_bar R
+//   R2  long-K contraction     W = C_bar^T [B C]        (split-K as the
+//                                                        paper's large-k GEMM)
+//   R5  R_bar -= S R
+// Semantics: C[M x N] = beta*C + sign * op(A) op(B), row-major storage with the
+// layout flags and modes of gemm_dmma.cuh (A_KMAJ: A is M x K, else K x M;
+// B_KMAJ: B is N x K, else K x N; MODE_FULL / MODE_LOWER / MODE_SPLITK).
+//
+// Why this shape (measurements in profiles/r01_gemm_notes.md):
+//  * FP64 MMA on sm_100a is warp-level mma.sync (DMMA.8x8x4, 16 cycles per
+//    instruction per SM sub-partition); there is no tcgen05 .kind::f64.  Fed
+//    from shared memory the DMMA loop reaches 35-37 TFLOP/s, but every
+//    thread-issued staging scheme (cp.async + __syncthreads, 1 or 2 CTAs/SM,
+//    persistent or not) stalled at 26-31 TFLOP/s.
+//  * So one PRODUCER warp moves all operand slabs with the TMA engine:
+//    k-contiguous operands as one 2-D tensor copy per slab (box 16 x rows,
+//    SWIZZLE_128B), m/n-contiguous operands as one 1-D bulk copy per k-row
+//    (cp.async.bulk, rows of 512 B-1 KB).  Completion is byte-counted on a
+//    per-slot "full" mbarrier; the 8 CONSUMER warps wait on it, run LDS + DMMA
+//    and release the slot on an "empty" mbarrier.  No CTA-wide barrier in the
+//    main loop; one CTA per SM walks a list of work items (persistent).
+//  * Bank conflicts: within a k4 step lane (g, t) uses k = kappa(s, t) =
+//    4 * ((((s & 1) ^ (t >> 1)) << 1) | (s >> 1)) + t, a permutation of the 16
+//    k of a slab that is conflict-free for BOTH the 128B-swizzled k-major
+//    tiles and the padded (pitch = 4 mod 16) m/n-major tiles.  A and B use the
+//    same permutation, so the contraction is unchanged.
+//  * C (beta = 1) is prefetched per lane into private shared slots one item
+//    ahead; sign = -1 is applied by negating the accumulator on the way in and
+//    out (exact), so the DMMA operands come straight from shared memory.
+#pragma once
+#include <cuda.h>
+
+#include "gemm_dmma.cuh"
+
+namespace stancl {
+
+// ------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, P1;\n"
+        "}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+// 1-D bulk copy global -> shared (SASS UBLKCP)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// 2-D tensor copy global -> shared (SASS UTMALDG)
+__device__ __forceinline__ void tma_g2s_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+namespace tg {
+constexpr int BK = 16;
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_>
+struct Cfg {
+  static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_;
+  static constexpr int NCONS = 32 * WARPS_M * WARPS_N;  // consumer threads
+  static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
+  static constexpr int MI = WTM / 8, NI = WTN / 8;
+};
+using CfgT = Cfg<128, 64, 4, 2, 4>;  // 8 consumer warps of 32 x 32 + 1 producer warp
+
+constexpr int align1k(int b) { return (b + 1023) / 1024 * 1024; }
+// shared slab of ROWS rows/cols: k-major = dense 128-B rows (TMA, 128B swizzle);
+// m/n-major = BK rows of ROWS + 4 doubles (bulk row copies, padded)
+template <int ROWS, bool KMAJ>
+struct Slab {
+  static constexpr int PITCH = KMAJ ? BK : ROWS + 4;
+  static constexpr int BYTES = align1k((KMAJ ? ROWS * BK : BK * (ROWS + 4)) * 8);
+  static constexpr unsigned TX = ROWS * BK * 8;  // bytes landed per slab
+};
+template <class CF, bool AK, bool BKM>
+struct Smem {
+  static constexpr int A = 0;
+  static constexpr int B = CF::STAGES * Slab<CF::BM, AK>::BYTES;
+  static constexpr int C = B + CF::STAGES * Slab<CF::BN, BKM>::BYTES;
+  static constexpr int BAR = C + CF::BM * CF::BN * 8;
+  static constexpr int TOTAL = BAR + 2 * CF::STAGES * 8 + 1024;  // + alignment slack
+};
+
+__device__ __forceinline__ int kappa(int s, int t) {
+  return 4 * (((((s & 1) ^ (t >> 1)) << 1)) | (s >> 1)) + t;
+}
+template <int ROWS, bool KMAJ>
+__device__ __forceinline__ double frag(const double* s, int rc, int k) {
+  if constexpr (KMAJ) {
+    return s[rc * BK + ((((k >> 1) ^ (rc & 7)) << 1) | (k & 1))];
+  } else {
+    return s[k * Slab<ROWS, KMAJ>::PITCH + rc];
+  }
+}
+}  // namespace tg
+
+template <class CF, int MODE>
+struct TItemMap {
+  int ntn, ntiles, ktiles_full;
+  __device__ __forceinline__ void get(const GemmArgs& p, int item, int& m0, int& n0, int& kbeg, int& ns,
+                                      int& z) const {
+    int tm, tn, tile = item;
+    z = 0;
+    if constexpr (MODE == MODE_SPLITK) {
+      z = item / ntiles;
+      tile = item - z * ntiles;
+    }
+    if constexpr (MODE == MODE_LOWER) {
+      tri_index<CF::BM / CF::BN>(tile, tm, tn);
+    } else {
+      tm = tile / ntn;
+      tn = tile - tm * ntn;
+    }
+    m0 = tm * CF::BM;
+    n0 = tn * CF::BN;
+    if constexpr (MODE == MODE_SPLITK) {
+      kbeg = z * p.kps;
+      ns = (min(p.K, kbeg + p.kps) - kbeg) / tg::BK;
+    } else {
+      kbeg = 0;
+      ns = ktiles_full;
+    }
+  }
+};
+
+template <int ROWS, bool KMAJ>
+__device__ __forceinline__ void produce_slab(double* dst, const CUtensorMap* map, const double* g, long long ld,
+                                             int row0, int k0, int lane, uint64_t* bar) {
+  if constexpr (KMAJ) {
+    if (lane == 0) tma_g2s_2d(dst, map, k0, row0, bar);
+  } else {
+    constexpr int P = tg::Slab<ROWS, false>::PITCH;
+    if (lane < tg::BK) bulk_g2s(dst + lane * P, g + (long long)(k0 + lane) * ld + row0, ROWS * 8, bar);
+  }
+}
+
+template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
+__global__ void __launch_bounds__(CF::NCONS + 32, 1)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    GemmArgs p, int nitems, TItemMap<CF, MODE> map) {
+  using namespace tg;
+  constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, NCONS = CF::NCONS;
+  constexpr int MI = CF::MI, NI = CF::NI;
+  using SA = Slab<BM, A_KMAJ>;
+  using SB = Slab<BN, B_KMAJ>;
+  using SM = Smem<CF, A_KMAJ, B_KMAJ>;
+  if (p.status && *p.status != 0) return;
+  if ((int)blockIdx.x >= nitems) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  double* sA = reinterpret_cast<double*>(base + SM::A);
+  double* sB = reinterpret_cast<double*>(base + SM::B);
+  double* sC = reinterpret_cast<double*>(base + SM::C);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + SM::BAR);
+  uint64_t* empty = full + STAGES;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);            // the producer's arrive.expect_tx
+      mbar_init(&empty[s], NCONS / 32);  // one arrive per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  __syncthreads();
+
+  if (warp == NCONS / 32) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      if (A_KMAJ) prefetch_tmap(&tmA);
+      if (B_KMAJ) prefetch_tmap(&tmB);
+    }
+    int it = 0;
+    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+      int m0, n0, kbeg, ns, z;
+      map.get(p, item, m0, n0, kbeg, ns, z);
+      for (int s = 0; s < ns; ++s, ++it) {
+        const int slot = it % STAGES, round = it / STAGES;
+        if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+        if (lane == 0) mbar_arrive_expect_tx(&full[slot], SA::TX + SB::TX);
+        __syncwarp();
+        const int k0 = kbeg + s * BK;
+        produce_slab<BM, A_KMAJ>(sA + slot * (SA::BYTES / 8), &tmA, p.A, p.lda, m0, k0, lane, &full[slot]);
+        produce_slab<BN, B_KMAJ>(sB + slot * (SB::BYTES / 8), &tmB, p.B, p.ldb, n0, k0, lane, &full[slot]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int wm = warp / CF::WARPS_N, wn = warp % CF::WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+  const bool need_c = (MODE != MODE_SPLITK) && p.beta != 0;
+  const unsigned long long smask = (p.sign < 0) ? 0x8000000000000000ull : 0ull;
+  double2* myC = reinterpret_cast<double2*>(sC) + (size_t)warp * MI * NI * 32 + lane;
+  auto load_c = [&](int m0, int n0) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
+        cp_async16(myC + (i * NI + j) * 32, p.C + (long long)r * p.ldc + c);
+      }
+    cp_async_commit();
+  };
+  int m0, n0, kbeg, ns, z;
+  map.get(p, blockIdx.x, m0, n0, kbeg, ns, z);
+  if (need_c) load_c(m0, n0);
+  int kap[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) kap[s] = kappa(s, t);
+  int it = 0;
+  double acc[MI][NI][2];
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    if (need_c) {
+      cp_async_wait<0>();
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const double2 v = myC[(i * NI + j) * 32];
+          acc[i][j][0] = xor_sign(v.x, smask);
+          acc[i][j][1] = xor_sign(v.y, smask);
+        }
+      const int nxt = item + gridDim.x;
+      if (nxt < nitems) {
+        int m1, n1, kb1, ns1, z1;
+        map.get(p, nxt, m1, n1, kb1, ns1, z1);
+        load_c(m1, n1);
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    for (int s = 0; s < ns; ++s, ++it) {
+      const int slot = it % STAGES, round = it / STAGES;
+      mbar_wait(&full[slot], round & 1);
+      const double* a_s = sA + slot * (SA::BYTES / 8);
+      const double* b_s = sB + slot * (SB::BYTES / 8);
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        const int k = kap[kk];
+        double af[MI], bf[NI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) af[i] = tg::frag<BM, A_KMAJ>(a_s, wm * CF::WTM + i * 8 + g, k);
+#pragma unroll
+        for (int j = 0; j < NI; ++j) bf[j] = tg::frag<BN, B_KMAJ>(b_s, wn * CF::WTN + j * 8 + g, k);
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+    // epilogue: registers -> global
+    double* Cout;
+    long long ldo;
+    if constexpr (MODE == MODE_SPLITK) {
+      Cout = p.C + (long long)z * p.M * p.N;
+      ldo = p.N;
+    } else {
+      Cout = p.C;
+      ldo = p.ldc;
+    }
+    const bool mask = (MODE == MODE_LOWER) || (MODE == MODE_FULL && p.lower_only);
+    const bool crosses = mask && (n0 + BN - 1 > m0);
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
+        double* dst = Cout + (long long)r * ldo + c;
+        const double v0 = xor_sign(acc[i][j][0], smask), v1 = xor_sign(acc[i][j][1], smask);
+        if (crosses) {
+          if (r >= c) dst[0] = v0;
+          if (r >= c + 1) dst[1] = v1;
+        } else {
+          *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+        }
+      }
+    const int nxt = item + gridDim.x;
+    if (nxt < nitems) map.get(p, nxt, m0, n0, kbeg, ns, z);
+  }
+}
+
+// ------------------------------------------------------------------ host side
+int tma_num_sms();
+// k-contiguous operand X[rows][K] (ld doubles): 2-D map, box {16, box_rows}, 128B swizzle
+bool make_kmajor_map(CUtensorMap* map, const double* X, long long rows, long long K, long long ld,
+                     int box_rows);
+
+template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
+cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st) {
+  using SM = tg::Smem<CF, A_KMAJ, B_KMAJ>;
+  auto kern = gemm_tma_kernel<CF, A_KMAJ, B_KMAJ, MODE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  memset(&ma, 0, sizeof(ma));
+  memset(&mb, 0, sizeof(mb));
+  if (A_KMAJ && !make_kmajor_map(&ma, p.A, p.M, p.K, p.lda, CF::BM)) return cudaErrorInvalidValue;
+  if (B_KMAJ && !make_kmajor_map(&mb, p.B, p.N, p.K, p.ldb, CF::BN)) return cudaErrorInvalidValue;
+  TItemMap<CF, MODE> map;
+  map.ntn = p.N / CF::BN;
+  map.ktiles_full = p.K / tg::BK;
+  int ntiles;
+  if (MODE == MODE_LOWER) {
+    constexpr int R = CF::BM / CF::BN;
+    const int T = p.M / CF::BM;
+    ntiles = R * T * (T + 1) / 2;
+  } else {
+    ntiles = (p.M / CF::BM) * map.ntn;
+  }
+  map.ntiles = ntiles;
+  const int nitems = ntiles * (MODE == MODE_SPLITK ? splits : 1);
+  if (nitems == 0) return cudaSuccess;
+  const int nsm = tma_num_sms();
+  const int grid = nitems < nsm ? nitems : nsm;
+  kern<<<grid, CF::NCONS + 32, SM::TOTAL, st>>>(ma, mb, p, nitems, map);
+  return cudaGetLastError();
+}
+
+}  // namespace stancl

@@ -14,10 +14,14 @@
 //       splitk_reduce_sub (the paper's large-k reduction)
 #include <atomic>
 #include <climits>
+#include <cstdlib>
+#include <cstring>
 #include <vector>
 
 #include "common.cuh"
 #include "gemm_dmma.cuh"
+#include "gemm_tma.cuh"
+#include <cudaTypedefs.h>
 #include "kernels.h"
 
 namespace stancl {
@@ -185,120 +189,148 @@ cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st) {
 }
 
 // ----------------------------------------------------------------------- F1
-// One CTA factors the 128 x 128 diagonal tile in shared memory, right-looking
-// column by column: pivot sqrt (IEEE), column scale by IEEE division, rank-1
-// update of the trailing lower part (one FMA per element, ascending j).
-constexpr int TP = NB + 1;  // tile pitch (doubles): conflict-free column access
-constexpr int POTRF_SMEM = (NB * TP + NB) * (int)sizeof(double);
+// One CTA factors the 128 x 128 diagonal tile, right-looking column by column
+// (the "classic sequential algorithm", inner loop parallel).
+// The tile lives in REGISTERS: 256 threads as a 16 x 16 grid, thread (ti, tj)
+// owns rows ti + 16a and columns tj + 16b (a, b = 0..7; cyclic, so the active
+// trailing part stays balanced).  Per column j: the diagonal owner publishes
+// T[j][j]; the owners of column j take d = sqrt(T[j][j]) (IEEE), scale by an
+// IEEE division and publish the column; every thread then applies the rank-1
+// update to its elements with one FMA each (ascending j, R12).
+constexpr int TP = NB + 1;  // pitch of shared 128 x 128 staging tiles (doubles)
 
 __global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t ld, int64_t k0,
                                                             int* status) {
   if (*status != 0) return;
-  extern __shared__ double sm[];
-  double* T = sm;
-  double* col = sm + NB * TP;
+  __shared__ double colbuf[NB];
+  __shared__ double diag_s;
   __shared__ int fail_j;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x;
+  const int ti = tid >> 4, tj = tid & 15;
   double* base = W + k0 * ld + k0;
-  for (int idx = tid; idx < NB * NB; idx += 256) {
-    const int i = idx >> 7, l = idx & (NB - 1);
-    if (l <= i) T[i * TP + l] = base[(long long)i * ld + l];
-  }
+  double T[8][8];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int r = ti + 16 * a, c = tj + 16 * b;
+      T[a][b] = (c <= r) ? base[(long long)r * ld + c] : 0.0;
+    }
   if (tid == 0) fail_j = -1;
-  __syncthreads();
-  for (int j = 0; j < NB; ++j) {
-    if (tid == 0) {
-      const double d = T[j * TP + j];
-      if (!(d > 0.0)) fail_j = j;
-      else T[j * TP + j] = sqrt(d);
+  bool failed = false;  // uniform across the CTA (every thread tests the same pivot)
+#pragma unroll
+  for (int jb = 0; jb < 8; ++jb) {
+    for (int jt = 0; jt < 16; ++jt) {
+      const int j = 16 * jb + jt;
+      // diagonal owner (ti == jt, tj == jt) publishes the updated pivot
+      if (ti == jt && tj == jt) diag_s = T[jb][jb];
+      __syncthreads();
+      const double s = diag_s;
+      if (!(s > 0.0)) {
+        if (tid == 0) fail_j = j;
+        failed = true;
+        break;
+      }
+      if (tj == jt) {  // owners of column j (register column jb)
+        const double d = sqrt(s);
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+          const int r = ti + 16 * a;
+          if (r > j) {
+            const double l = T[a][jb] / d;
+            T[a][jb] = l;
+            colbuf[r] = l;
+          } else if (r == j) {
+            T[a][jb] = d;
+          }
+        }
+      }
+      __syncthreads();
+      double cr[8], cc[8];
+#pragma unroll
+      for (int a = 0; a < 8; ++a) cr[a] = colbuf[ti + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) cc[b] = colbuf[tj + 16 * b];
+      // trailing update of columns c > j (rows r <= j of those columns are the
+      // strict upper triangle: never read or stored, so left unpredicated)
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        if (tj + 16 * b > j) {
+#pragma unroll
+          for (int a = 0; a < 8; ++a) T[a][b] = fma(-cr[a], cc[b], T[a][b]);
+        }
+      }
     }
-    __syncthreads();
-    if (fail_j >= 0) break;
-    const double djj = T[j * TP + j];
-    for (int i = j + 1 + tid; i < NB; i += 256) {
-      const double v = T[i * TP + j] / djj;
-      T[i * TP + j] = v;
-      col[i] = v;
-    }
-    __syncthreads();
-    for (int i = j + 1 + warp; i < NB; i += 8) {
-      const double ci = col[i];
-      for (int l = j + 1 + lane; l <= i; l += 32) T[i * TP + l] = fma(-ci, col[l], T[i * TP + l]);
-    }
-    __syncthreads();
+    if (failed) break;
   }
   __syncthreads();
-  for (int idx = tid; idx < NB * NB; idx += 256) {
-    const int i = idx >> 7, l = idx & (NB - 1);
-    if (l <= i) base[(long long)i * ld + l] = T[i * TP + l];
-  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int r = ti + 16 * a, c = tj + 16 * b;
+      if (c <= r) base[(long long)r * ld + c] = T[a][b];
+    }
   if (tid == 0 && fail_j >= 0) atomicCAS(status, 0, (int)(k0 + fail_j + 1));
 }
 
 cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStream_t st) {
   Prof prof_(PROF_POTRF, (double)NB * NB * NB / 3.0, st);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(potrf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         POTRF_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  potrf_tile_kernel<<<1, 256, POTRF_SMEM, st>>>(W, ld, k0, status);
+  potrf_tile_kernel<<<1, 256, 0, st>>>(W, ld, k0, status);
   return cudaGetLastError();
 }
 
 // ----------------------------------------------------------------------- F2
-// X L11^T = A21 for a 64-row slab per CTA.  L11^T is staged in shared memory
-// (LT[j][l] = L11[l][j]); four threads own a row (columns p, p+4, ...), and
-// column j is finished by its owner with an IEEE division, then broadcast to
-// the other three through shared memory (same warp: __syncwarp suffices).
+// X L11^T = A21 by substitution (no explicit inverse, R11), 64 rows
+// per CTA.  Four threads own a row, thread p holding columns p + 4q (q = 0..31)
+// in registers; column j is finished by its owner with an IEEE division and
+// broadcast with a warp shuffle; L11^T is staged in shared memory
+// (LT[j][l] = L11[l][j], broadcast reads).
 constexpr int TRSM_ROWS = 64;
-constexpr int RP = NB + 4;  // row pitch: 4 rows x 4 threads per half-warp hit distinct banks
-constexpr int TRSM_SMEM = (NB * TP + TRSM_ROWS * RP + NB) * (int)sizeof(double);
+constexpr int TRSM_SMEM = (NB * TP + NB) * (int)sizeof(double);
 
 __global__ void __launch_bounds__(256, 1) trsm_panel_kernel(double* W, int64_t ld, int64_t k0,
                                                             int64_t r0, const int* status) {
   if (*status != 0) return;
   extern __shared__ double sm[];
   double* LT = sm;
-  double* R = sm + NB * TP;
-  double* dg = R + TRSM_ROWS * RP;
-  const int tid = threadIdx.x;
+  double* dg = sm + NB * TP;
+  const int tid = threadIdx.x, lane = tid & 31;
   const double* L11 = W + k0 * ld + k0;
   for (int idx = tid; idx < NB * NB; idx += 256) {
     const int l = idx >> 7, j = idx & (NB - 1);
-    if (j <= l) LT[j * TP + l] = L11[(long long)l * ld + j];
-    if (j == l) dg[j] = L11[(long long)l * ld + j];
+    if (j <= l) {
+      const double v = L11[(long long)l * ld + j];
+      LT[j * TP + l] = v;
+      if (j == l) dg[j] = v;
+    }
   }
-  const long long row0 = r0 + (long long)blockIdx.x * TRSM_ROWS;
-  double* P = W + row0 * ld + k0;
-  for (int idx = tid; idx < TRSM_ROWS * NB; idx += 256) {
-    const int r = idx >> 7, c = idx & (NB - 1);
-    R[r * RP + c] = P[(long long)r * ld + c];
-  }
-  __syncthreads();
   const int r = tid >> 2, p = tid & 3;
-  double* row = R + r * RP;
-  for (int j = 0; j < NB; ++j) {
-    if ((j & 3) == p) row[j] = row[j] / dg[j];
-    __syncwarp();
-    const double x = row[j];
-    const double* lt = LT + j * TP;
-    for (int c = j + 1 + ((p - (j + 1)) & 3); c < NB; c += 4) row[c] = fma(-x, lt[c], row[c]);
-    __syncwarp();
-  }
+  const long long row = r0 + (long long)blockIdx.x * TRSM_ROWS + r;
+  double* P = W + row * ld + k0;
+  double x[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) x[q] = P[p + 4 * q];
   __syncthreads();
-  for (int idx = tid; idx < TRSM_ROWS * NB; idx += 256) {
-    const int rr = idx >> 7, c = idx & (NB - 1);
-    P[(long long)rr * ld + c] = R[rr * RP + c];
+  const int owner_base = lane & ~3;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    if (p == (j & 3)) x[j >> 2] = x[j >> 2] / dg[j];
+    const double v = __shfl_sync(0xffffffffu, x[j >> 2], owner_base | (j & 3));
+    const double* lt = LT + j * TP;
+#pragma unroll
+    for (int q = (j >> 2); q < 32; ++q) {
+      if (p + 4 * q > j) x[q] = fma(-v, lt[p + 4 * q], x[q]);
+    }
   }
+#pragma unroll
+  for (int q = 0; q < 32; ++q) P[p + 4 * q] = x[q];
 }
 
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st) {
-  Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st);
   if (r1 <= r0) return cudaSuccess;
+  Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -312,33 +344,107 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
 }
 
 // ------------------------------------------------------------ DMMA GEMM family
+// Tile configuration per call class, tunable with STAN_CL_GEMM_CFG="syrk,gemm,splitk",
+// each one of big (128x128, 8 warps of 64x32, 1 CTA/SM), mid (128x64, 4 warps of
+// 64x32, 2 CTAs/SM), w8 (128x64, 8 warps of 32x32, 2 CTAs/SM), w16 (128x128, 16
+// warps of 32x32, 1 CTA/SM).
+namespace {
+enum { CFG_BIG = 0, CFG_MID = 1, CFG_W8 = 2, CFG_W16 = 3 };
+struct CfgSel {
+  int syrk = CFG_MID, gemm = CFG_MID, splitk = CFG_BIG;
+  int pingpong = 0;
+  int persist = 1;  // persistent TMA-fed warp-specialised kernels (gemm_tma.cuh)
+  CfgSel() {
+    const char* pp = getenv("STAN_CL_PINGPONG");
+    if (pp) pingpong = atoi(pp);
+    const char* ps = getenv("STAN_CL_TMA");
+    if (ps) persist = atoi(ps);
+    const char* e = getenv("STAN_CL_GEMM_CFG");
+    if (!e) return;
+    char buf[64];
+    strncpy(buf, e, sizeof(buf) - 1);
+    buf[sizeof(buf) - 1] = 0;
+    int* dst[3] = {&syrk, &gemm, &splitk};
+    int i = 0;
+    for (char* tok = strtok(buf, ","); tok && i < 3; tok = strtok(nullptr, ","), ++i) {
+      if (!strcmp(tok, "big")) *dst[i] = CFG_BIG;
+      else if (!strcmp(tok, "mid")) *dst[i] = CFG_MID;
+      else if (!strcmp(tok, "w8")) *dst[i] = CFG_W8;
+      else if (!strcmp(tok, "w16")) *dst[i] = CFG_W16;
+    }
+  }
+};
+const CfgSel& cfgsel() {
+  static CfgSel s;
+  return s;
+}
+
+cudaError_t gemm_full_persist(bool a_kmaj, bool b_kmaj, const GemmArgs& p, cudaStream_t st) {
+  using CF = tg::CfgT;
+  if (a_kmaj && b_kmaj) return launch_tma<CF, true, true, MODE_FULL>(p, 1, st);
+  if (a_kmaj && !b_kmaj) return launch_tma<CF, true, false, MODE_FULL>(p, 1, st);
+  if (!a_kmaj && b_kmaj) return launch_tma<CF, false, true, MODE_FULL>(p, 1, st);
+  return launch_tma<CF, false, false, MODE_FULL>(p, 1, st);
+}
+
+template <class CF>
+cudaError_t gemm_full_cfg(bool a_kmaj, bool b_kmaj, const GemmArgs& p, cudaStream_t st) {
+  if (a_kmaj && b_kmaj) return launch_gemm<CF, true, true, MODE_FULL>(p, 1, st);
+  if (a_kmaj && !b_kmaj) return launch_gemm<CF, true, false, MODE_FULL>(p, 1, st);
+  if (!a_kmaj && b_kmaj) return launch_gemm<CF, false, true, MODE_FULL>(p, 1, st);
+  return launch_gemm<CF, false, false, MODE_FULL>(p, 1, st);
+}
+}  // namespace
+
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-                      int64_t ldc, const int* status, cudaStream_t st) {
-  Prof prof_(PROF_GEMM, 2.0 * M * N * K, st);
+                      int64_t ldc, const int* status, cudaStream_t st, int lower_only, int prof_kind) {
   if (M == 0 || N == 0) return cudaSuccess;
-  GemmArgs p{A, lda, B, ldb, C, ldc, M, N, K, K, sign, beta, status};
-  if (a_kmaj && b_kmaj) return launch_gemm<true, true, MODE_FULL>(p, 1, st);
-  if (a_kmaj && !b_kmaj) return launch_gemm<true, false, MODE_FULL>(p, 1, st);
-  if (!a_kmaj && b_kmaj) return launch_gemm<false, true, MODE_FULL>(p, 1, st);
-  return launch_gemm<false, false, MODE_FULL>(p, 1, st);
+  Prof prof_(prof_kind, 2.0 * M * N * K, st);
+  GemmArgs p{A, lda, B, ldb, C, ldc, M, N, K, K, sign, beta, lower_only, status, cfgsel().pingpong};
+  // A aliasing C (in-place C <- A B): one CTA must own whole rows of C, i.e. a
+  // single 128-wide tile column with the one-tile-per-CTA kernel
+  const bool alias = (const void*)A == (const void*)C;
+  if (alias) {
+    if (N != gemm::CfgBig::BN) return cudaErrorInvalidValue;
+    return gemm_full_cfg<gemm::CfgBig>(a_kmaj, b_kmaj, p, st);
+  }
+  if (cfgsel().persist) return gemm_full_persist(a_kmaj, b_kmaj, p, st);
+  switch (cfgsel().gemm) {
+    case CFG_BIG: return gemm_full_cfg<gemm::CfgBig>(a_kmaj, b_kmaj, p, st);
+    case CFG_W8: return gemm_full_cfg<gemm::CfgW8>(a_kmaj, b_kmaj, p, st);
+    case CFG_W16: return gemm_full_cfg<gemm::CfgW16>(a_kmaj, b_kmaj, p, st);
+    default: return gemm_full_cfg<gemm::CfgMid>(a_kmaj, b_kmaj, p, st);
+  }
 }
 
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                           double* C, int64_t ldc, const int* status, cudaStream_t st) {
-  Prof prof_(PROF_SYRK, (double)K * M * (M + 1.0), st);
   if (M == 0) return cudaSuccess;
-  GemmArgs p{A, lda, B, ldb, C, ldc, M, M, K, K, -1.0, 1, status};
-  return launch_gemm<true, true, MODE_LOWER>(p, 1, st);
+  Prof prof_(PROF_SYRK, (double)K * M * (M + 1.0), st);
+  GemmArgs p{A, lda, B, ldb, C, ldc, M, M, K, K, -1.0, 1, 1, status, cfgsel().pingpong};
+  if (cfgsel().persist) return launch_tma<tg::CfgT, true, true, MODE_LOWER>(p, 1, st);
+  switch (cfgsel().syrk) {
+    case CFG_BIG: return launch_gemm<gemm::CfgBig, true, true, MODE_LOWER>(p, 1, st);
+    case CFG_W8: return launch_gemm<gemm::CfgW8, true, true, MODE_LOWER>(p, 1, st);
+    case CFG_W16: return launch_gemm<gemm::CfgW16, true, true, MODE_LOWER>(p, 1, st);
+    default: return launch_gemm<gemm::CfgMid, true, true, MODE_LOWER>(p, 1, st);
+  }
 }
 
 cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const double* A, int64_t lda,
                            const double* B, int64_t ldb, double* P, const int* status,
                            cudaStream_t st) {
-  Prof prof_(PROF_SPLITK, 2.0 * M * N * K, st);
   if (M == 0 || N == 0) return cudaSuccess;
-  GemmArgs p{A, lda, B, ldb, P, N, M, N, K, kps, 1.0, 0, status};
-  return launch_gemm<false, false, MODE_SPLITK>(p, splits, st);
+  Prof prof_(PROF_SPLITK, 2.0 * M * N * K, st);
+  GemmArgs p{A, lda, B, ldb, P, N, M, N, K, kps, 1.0, 0, 0, status, cfgsel().pingpong};
+  if (cfgsel().persist) return launch_tma<tg::CfgT, false, false, MODE_SPLITK>(p, splits, st);
+  switch (cfgsel().splitk) {
+    case CFG_MID: return launch_gemm<gemm::CfgMid, false, false, MODE_SPLITK>(p, splits, st);
+    case CFG_W8: return launch_gemm<gemm::CfgW8, false, false, MODE_SPLITK>(p, splits, st);
+    case CFG_W16: return launch_gemm<gemm::CfgW16, false, false, MODE_SPLITK>(p, splits, st);
+    default: return launch_gemm<gemm::CfgBig, false, false, MODE_SPLITK>(p, splits, st);
+  }
 }
 
 __global__ void splitk_reduce_sub_kernel(const double* __restrict__ P, int splits, int M, int N,
@@ -556,4 +662,38 @@ cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cuda
   return cudaGetLastError();
 }
 
+}  // namespace stancl
+
+// ---------------------------------------------------------- TMA host helpers
+namespace stancl {
+int tma_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+bool make_kmajor_map(CUtensorMap* map, const double* X, long long rows, long long K, long long ld,
+                     int box_rows) {
+  static PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return false;
+    encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * sizeof(double)};
+  cuuint32_t box[2] = {(cuuint32_t)tg::BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)X, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
 }  // namespace stancl

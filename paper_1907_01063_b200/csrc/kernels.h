@@ -61,9 +61,11 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
 // ---- DMMA GEMM family (F3, R1, R2, R3, R5) ----
 // C[M x N] = beta*C + sign * op(A) op(B)   (see gemm_dmma.cuh)
 //   a_kmaj: A is M x K row-major (else K x M);  b_kmaj: B is N x K (else K x N)
+// lower_only: store only r >= c (relative to C); prof_kind: profiling class
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-                      int64_t ldc, const int* status, cudaStream_t st);
+                      int64_t ldc, const int* status, cudaStream_t st, int lower_only = 0,
+                      int prof_kind = 1);
 // lower tiles of square C[M x M] -= A A'^T style: C -= A B^T, A, B both k-major (SYRK)
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                           double* C, int64_t ldc, const int* status, cudaStream_t st);
