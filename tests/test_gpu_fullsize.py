@@ -1,0 +1,151 @@
+"""Full-size GPU checks (n up to 16384, the bench configuration).
+
+At these sizes the oracle cannot run inside a test (20 min for the forward at
+n=16384, ~35 min for the adjoint), so parity is checked
+  * on SAMPLED oracle outputs: tests/golden/oracle_chol_se_n{4096,8192,16384}.npz
+    were written by tools/make_golden_large.py, which calls only oracle/;
+  * via properties that hold at any size: the integer-exact family (bit-exact),
+    sampled reconstruction, the leading-block reduction of the adjoint (an
+    L_bar supported on the leading m x m block gives exactly the oracle's
+    adjoint of that block, zeros elsewhere), and a closed-form evaluation of
+    A_bar = Phi(G + G^T), G = L^-T Phi(L^T L_bar) L^-1 at sampled entries for an
+    L_bar supported on the last rows (rank-r M = L^T L_bar, O(r n) per entry).
+Inputs to the adjoint come from LAPACK (numpy.linalg.cholesky), never from the
+CUDA path.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg as sla
+import torch
+
+import oracle
+from paper_1907_01063_b200 import inputs
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+@pytest.fixture(scope="module")
+def sc():
+    import paper_1907_01063_b200 as m
+    m.load()
+    return m
+
+
+_K_CACHE: dict = {}
+
+
+def oracle_K(n):
+    if n not in _K_CACHE:
+        _K_CACHE.clear()
+        _K_CACHE[n] = oracle.se_cov(inputs.gp_x(n), 1.0, 1.0, 1e-6)
+    return _K_CACHE[n]
+
+
+@pytest.mark.parametrize("n", [4096, 8192, 16384])
+def test_cholesky_matches_sampled_oracle(sc, n):
+    g = np.load(os.path.join(GOLD, f"oracle_chol_se_n{n}.npz"))
+    assert int(g["n"]) == n and int(g["x_seed"]) == inputs.X_SEED
+    K = oracle_K(n)
+    L = sc.cholesky(torch.from_numpy(K).cuda())
+    rows = torch.from_numpy(g["rows"]).cuda()
+    got_rows = L[rows].cpu().numpy()
+    ii = torch.from_numpy(g["ii"]).cuda()
+    jj = torch.from_numpy(g["jj"]).cuda()
+    got_vals = L[ii, jj].cpu().numpy()
+    got_diag = torch.diagonal(L).cpu().numpy()
+    want = np.concatenate([g["row_vals"].ravel(), g["vals"], g["diag"]])
+    got = np.concatenate([got_rows.ravel(), got_vals, got_diag])
+    err = np.linalg.norm(got - want) / np.linalg.norm(want)
+    assert err <= 1e-11, err
+    # log det from the diagonal (2 sum log L_ii), oracle vs GPU
+    ld_w, ld_g = 2 * np.sum(np.log(g["diag"])), 2 * np.sum(np.log(got_diag))
+    assert abs(ld_g - ld_w) <= 1e-11 * abs(ld_w)
+    del L
+    torch.cuda.empty_cache()
+
+
+def test_cholesky_reconstruction_sampled_16384(sc):
+    n = 16384
+    K = oracle_K(n)
+    L = sc.cholesky(torch.from_numpy(K).cuda()).cpu().numpy()
+    assert np.all(L[np.triu_indices(8, 1)] == 0)
+    g = np.random.default_rng(3)
+    i = g.integers(0, n, 4000)
+    j = g.integers(0, n, 4000)
+    rec = np.einsum("ij,ij->i", L[i], L[j])
+    # Frobenius-norm estimate of ||L L^T - A|| / ||A|| from the sample
+    err = np.sqrt(np.mean((rec - K[i, j]) ** 2) * n * n) / np.linalg.norm(K)
+    assert err <= 1e-13, err
+
+
+def test_cholesky_integer_exact_16384(sc):
+    n = 16384
+    L0 = inputs.unit_lower_pm1(n, seed=n)
+    Lt = torch.from_numpy(L0).cuda()
+    A = Lt @ Lt.T          # integer Gram matrix: exact in any summation order
+    del Lt
+    L = sc.cholesky(A, out=A)
+    assert torch.equal(L.cpu(), torch.from_numpy(L0))
+
+
+@pytest.fixture(scope="module")
+def lapack_L():
+    n = 16384
+    return np.linalg.cholesky(oracle_K(n))
+
+
+def test_adjoint_leading_block_16384(sc, lapack_L):
+    n, m = 16384, 1024
+    L = lapack_L
+    W = np.zeros((n, n))
+    W[:m, :m] = inputs.lbar(m, seed=21)
+    want = oracle.cholesky_adjoint(L[:m, :m].copy(), W[:m, :m].copy())
+    got = sc.cholesky_adjoint(torch.from_numpy(L).cuda(), torch.from_numpy(W).cuda()).cpu().numpy()
+    assert np.linalg.norm(got[:m, :m] - want) / np.linalg.norm(want) <= 1e-9
+    got[:m, :m] = 0.0
+    assert not np.any(got)                     # exactly zero outside the block
+
+
+def _adjoint_entry(L, rows, Wr, i, j):
+    """A_bar[i][j] (i >= j) = G_ij + G_ji (i > j) or G_ii, with
+    G = L^-T Phi(L^T W) L^-1 and W = L_bar supported on `rows` (Wr = W[rows])."""
+    n = L.shape[0]
+
+    def g(a, b):
+        u = sla.solve_triangular(L, np.eye(1, n, a).ravel(), lower=True)
+        v = sla.solve_triangular(L, np.eye(1, n, b).ravel(), lower=True)
+        # u^T Phi(M) v, M = sum_k L[k,:]^T W[k,:]; Phi keeps a > b, halves a == b
+        tot = 0.0
+        for k, row in enumerate(rows):
+            p = u * L[row]                     # p_a = u_a L_ka
+            q = Wr[k] * v                      # q_b = W_kb v_b
+            cq = np.concatenate(([0.0], np.cumsum(q)[:-1]))   # sum_{b<a} q_b
+            tot += np.dot(p, cq) + 0.5 * np.dot(p, q)
+        return tot
+
+    return g(i, j) + g(j, i) if i != j else g(i, i)
+
+
+def test_adjoint_trailing_rows_closed_form_16384(sc, lapack_L):
+    n, r = 16384, 128
+    L = lapack_L
+    rows = np.arange(n - r, n)
+    W = np.zeros((n, n))
+    Wr = inputs.lbar(n, seed=5)[n - r:]        # last r rows of a random lower L_bar
+    W[n - r:] = Wr
+    got = sc.cholesky_adjoint(torch.from_numpy(L).cuda(), torch.from_numpy(W).cuda()).cpu().numpy()
+    scale = np.linalg.norm(got) / n            # RMS entry size
+    g = np.random.default_rng(9)
+    picks = [(n - 1, n - 1), (n - 5, 17), (8000, 123), (n - r, n - r - 1)]
+    for _ in range(3):
+        a, b = sorted(g.integers(0, n, 2))[::-1]
+        picks.append((int(a), int(b)))
+    for a, b in picks:
+        want = _adjoint_entry(L, rows, Wr, a, b)
+        assert abs(got[a, b] - want) <= 1e-9 * max(abs(want), scale), (a, b, got[a, b], want)
