@@ -13,6 +13,7 @@
 //       diagonal step), phi_sym,
 //       splitk_reduce_sub (the paper's large-k reduction)
 #include <atomic>
+#include <cstdio>
 #include <climits>
 #include <cstdlib>
 #include <cstring>
@@ -351,14 +352,25 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
 namespace {
 enum { CFG_BIG = 0, CFG_MID = 1, CFG_W8 = 2, CFG_W16 = 3 };
 struct CfgSel {
-  int syrk = CFG_MID, gemm = CFG_MID, splitk = CFG_BIG;
+  int syrk = CFG_W8, gemm = CFG_W8, splitk = CFG_W8;
   int pingpong = 0;
-  int persist = 1;  // persistent TMA-fed warp-specialised kernels (gemm_tma.cuh)
+  // persistent TMA-fed warp-specialised kernels (gemm_tma.cuh) per class:
+  // STAN_CL_TMA="syrk,gemm,splitk" with 1 = TMA kernel, 0 = one-tile-per-CTA cp.async kernel
+  // default: the forward SYRK stays one-tile-per-CTA so the lookahead panel
+  // kernels on the side stream find SMs at CTA boundaries
+  int tma_syrk = 0, tma_gemm = 1, tma_splitk = 1;
   CfgSel() {
     const char* pp = getenv("STAN_CL_PINGPONG");
     if (pp) pingpong = atoi(pp);
     const char* ps = getenv("STAN_CL_TMA");
-    if (ps) persist = atoi(ps);
+    if (ps) {
+      int v[3] = {1, 1, 1};
+      int n = sscanf(ps, "%d,%d,%d", &v[0], &v[1], &v[2]);
+      if (n == 1) v[1] = v[2] = v[0];
+      tma_syrk = v[0];
+      tma_gemm = v[1];
+      tma_splitk = v[2];
+    }
     const char* e = getenv("STAN_CL_GEMM_CFG");
     if (!e) return;
     char buf[64];
@@ -409,7 +421,7 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
     if (N != gemm::CfgBig::BN) return cudaErrorInvalidValue;
     return gemm_full_cfg<gemm::CfgBig>(a_kmaj, b_kmaj, p, st);
   }
-  if (cfgsel().persist) return gemm_full_persist(a_kmaj, b_kmaj, p, st);
+  if (cfgsel().tma_gemm) return gemm_full_persist(a_kmaj, b_kmaj, p, st);
   switch (cfgsel().gemm) {
     case CFG_BIG: return gemm_full_cfg<gemm::CfgBig>(a_kmaj, b_kmaj, p, st);
     case CFG_W8: return gemm_full_cfg<gemm::CfgW8>(a_kmaj, b_kmaj, p, st);
@@ -423,7 +435,7 @@ cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const doub
   if (M == 0) return cudaSuccess;
   Prof prof_(PROF_SYRK, (double)K * M * (M + 1.0), st);
   GemmArgs p{A, lda, B, ldb, C, ldc, M, M, K, K, -1.0, 1, 1, status, cfgsel().pingpong};
-  if (cfgsel().persist) return launch_tma<tg::CfgT, true, true, MODE_LOWER>(p, 1, st);
+  if (cfgsel().tma_syrk) return launch_tma<tg::CfgT, true, true, MODE_LOWER>(p, 1, st);
   switch (cfgsel().syrk) {
     case CFG_BIG: return launch_gemm<gemm::CfgBig, true, true, MODE_LOWER>(p, 1, st);
     case CFG_W8: return launch_gemm<gemm::CfgW8, true, true, MODE_LOWER>(p, 1, st);
@@ -438,7 +450,7 @@ cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const doubl
   if (M == 0 || N == 0) return cudaSuccess;
   Prof prof_(PROF_SPLITK, 2.0 * M * N * K, st);
   GemmArgs p{A, lda, B, ldb, P, N, M, N, K, kps, 1.0, 0, 0, status, cfgsel().pingpong};
-  if (cfgsel().persist) return launch_tma<tg::CfgT, false, false, MODE_SPLITK>(p, splits, st);
+  if (cfgsel().tma_splitk) return launch_tma<tg::CfgT, false, false, MODE_SPLITK>(p, splits, st);
   switch (cfgsel().splitk) {
     case CFG_MID: return launch_gemm<gemm::CfgMid, false, false, MODE_SPLITK>(p, splits, st);
     case CFG_W8: return launch_gemm<gemm::CfgW8, false, false, MODE_SPLITK>(p, splits, st);
