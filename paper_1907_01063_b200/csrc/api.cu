@@ -66,25 +66,26 @@ struct AdjPlan {
   size_t dinv, part, tmp, total;
 };
 
-// split-K factor for W = C_bar^T L[k:N, 0:k]: minimise waves * (m / splits)
+// split-K factor for W = C_bar^T L[k:N, 0:k] (persistent TMA GEMM, 128 x 64
+// output tiles, 32-deep slabs): minimise rounds-of-148 x per-item K (+ a fixed
+// per-item cost) plus the reduction's extra reads
 void splitk_choice(int64_t m, int64_t k, int* splits_out, int* kps_out) {
-  const int ntiles = (int)(k / NB);
-  const int kmax = (int)(m / 16);
+  const int ntiles = (int)(k / 64);
+  const int kmax = (int)(m / 32);
   double best = 1e300;
   int bs = 1;
   for (int s = 1; s <= 64 && s <= kmax; ++s) {
-    const int64_t kps = round_up((m + s - 1) / s, 16);
+    const int64_t kps = round_up((m + s - 1) / s, 32);
     const int eff_s = (int)((m + kps - 1) / kps);
-    const int64_t ctas = (int64_t)ntiles * eff_s;
-    const int64_t waves = (ctas + 147) / 148;
-    // per-CTA time ~ kps (+ fixed cost ~ 64 k-rows), plus reduce cost ~ splits
-    const double t = (double)waves * (double)(kps + 64) + 2.0 * eff_s * 16;
+    const int64_t items = (int64_t)ntiles * eff_s;
+    const int64_t rounds = (items + 147) / 148;
+    const double t = (double)rounds * (double)(kps + 96) + 3.0 * eff_s * 64 * (double)k / (148.0 * 64);
     if (t < best - 1e-9) {
       best = t;
       bs = s;
     }
   }
-  int64_t kps = round_up((m + bs - 1) / bs, 16);
+  const int64_t kps = round_up((m + bs - 1) / bs, 32);
   *kps_out = (int)kps;
   *splits_out = (int)((m + kps - 1) / kps);
 }

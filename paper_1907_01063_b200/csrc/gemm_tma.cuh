@@ -87,42 +87,52 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
 
 namespace tg {
 constexpr int BK = 16;
-template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_>
+template <int BM_, int BN_, int WARPS_M_, int WARPS_N_, int STAGES_, int MINB_ = 1, bool CPREF_ = true,
+          int BKS_ = 16>
 struct Cfg {
   static constexpr int BM = BM_, BN = BN_, WARPS_M = WARPS_M_, WARPS_N = WARPS_N_, STAGES = STAGES_;
+  static constexpr int BKS = BKS_;       // slab depth (k per pipeline stage): 16 or 32
+  static constexpr int MINB = MINB_;     // CTAs per SM (launch bound)
+  static constexpr bool CPREF = CPREF_;  // prefetch C through shared memory
   static constexpr int NCONS = 32 * WARPS_M * WARPS_N;  // consumer threads
   static constexpr int WTM = BM / WARPS_M, WTN = BN / WARPS_N;
   static constexpr int MI = WTM / 8, NI = WTN / 8;
 };
 using CfgT = Cfg<128, 64, 4, 2, 4>;  // 8 consumer warps of 32 x 32 + 1 producer warp
+using CfgT2 = Cfg<128, 64, 4, 2, 3, 2, false>;  // same, 2 CTAs/SM, C straight from global
+using CfgT2P = Cfg<128, 64, 4, 2, 2, 2, true>;  // 2 CTAs/SM, double-buffered ring, C prefetch
+using CfgT32 = Cfg<128, 64, 4, 2, 3, 1, true, 32>;  // 32-deep slabs (two TMA boxes per operand)
 
 constexpr int align1k(int b) { return (b + 1023) / 1024 * 1024; }
-// shared slab of ROWS rows/cols: k-major = dense 128-B rows (TMA, 128B swizzle);
-// m/n-major = BK rows of ROWS + 4 doubles (bulk row copies, padded)
-template <int ROWS, bool KMAJ>
+// shared slab of ROWS rows/cols and depth BKS: k-major = BKS/16 dense sub-tiles of
+// ROWS x 128-B rows (one TMA box each, 128B swizzle); m/n-major = BKS rows of
+// ROWS + 4 doubles (bulk row copies, padded)
+template <int ROWS, bool KMAJ, int BKS = 16>
 struct Slab {
   static constexpr int PITCH = KMAJ ? BK : ROWS + 4;
-  static constexpr int BYTES = align1k((KMAJ ? ROWS * BK : BK * (ROWS + 4)) * 8);
-  static constexpr unsigned TX = ROWS * BK * 8;  // bytes landed per slab
+  static constexpr int BYTES = align1k((KMAJ ? ROWS * BKS : BKS * (ROWS + 4)) * 8);
+  static constexpr unsigned TX = ROWS * BKS * 8;  // bytes landed per slab
 };
 template <class CF, bool AK, bool BKM>
 struct Smem {
   static constexpr int A = 0;
-  static constexpr int B = CF::STAGES * Slab<CF::BM, AK>::BYTES;
-  static constexpr int C = B + CF::STAGES * Slab<CF::BN, BKM>::BYTES;
-  static constexpr int BAR = C + CF::BM * CF::BN * 8;
+  static constexpr int B = CF::STAGES * Slab<CF::BM, AK, CF::BKS>::BYTES;
+  static constexpr int C = B + CF::STAGES * Slab<CF::BN, BKM, CF::BKS>::BYTES;
+  static constexpr int BAR = C + (CF::CPREF ? CF::BM * CF::BN * 8 : 0);
   static constexpr int TOTAL = BAR + 2 * CF::STAGES * 8 + 1024;  // + alignment slack
 };
 
 __device__ __forceinline__ int kappa(int s, int t) {
   return 4 * (((((s & 1) ^ (t >> 1)) << 1)) | (s >> 1)) + t;
 }
+// element (row/col rc, k) of a slab; k in [0, BKS)
 template <int ROWS, bool KMAJ>
 __device__ __forceinline__ double frag(const double* s, int rc, int k) {
   if constexpr (KMAJ) {
-    return s[rc * BK + ((((k >> 1) ^ (rc & 7)) << 1) | (k & 1))];
+    const int kk = k & 15;
+    return s[(k >> 4) * ROWS * BK + rc * BK + ((((kk >> 1) ^ (rc & 7)) << 1) | (kk & 1))];
   } else {
-    return s[k * Slab<ROWS, KMAJ>::PITCH + rc];
+    return s[k * (ROWS + 4) + rc];
   }
 }
 }  // namespace tg
@@ -148,7 +158,7 @@ struct TItemMap {
     n0 = tn * CF::BN;
     if constexpr (MODE == MODE_SPLITK) {
       kbeg = z * p.kps;
-      ns = (min(p.K, kbeg + p.kps) - kbeg) / tg::BK;
+      ns = (min(p.K, kbeg + p.kps) - kbeg) / CF::BKS;
     } else {
       kbeg = 0;
       ns = ktiles_full;
@@ -156,26 +166,29 @@ struct TItemMap {
   }
 };
 
-template <int ROWS, bool KMAJ>
+template <int ROWS, bool KMAJ, int BKS>
 __device__ __forceinline__ void produce_slab(double* dst, const CUtensorMap* map, const double* g, long long ld,
                                              int row0, int k0, int lane, uint64_t* bar) {
   if constexpr (KMAJ) {
-    if (lane == 0) tma_g2s_2d(dst, map, k0, row0, bar);
+#pragma unroll
+    for (int h = 0; h < BKS / 16; ++h)
+      if (lane == h) tma_g2s_2d(dst + h * ROWS * tg::BK, map, k0 + 16 * h, row0, bar);
   } else {
-    constexpr int P = tg::Slab<ROWS, false>::PITCH;
-    if (lane < tg::BK) bulk_g2s(dst + lane * P, g + (long long)(k0 + lane) * ld + row0, ROWS * 8, bar);
+    constexpr int P = ROWS + 4;
+    if (lane < BKS) bulk_g2s(dst + lane * P, g + (long long)(k0 + lane) * ld + row0, ROWS * 8, bar);
   }
 }
 
 template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
-__global__ void __launch_bounds__(CF::NCONS + 32, 1)
+__global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     GemmArgs p, int nitems, TItemMap<CF, MODE> map) {
   using namespace tg;
   constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, NCONS = CF::NCONS;
   constexpr int MI = CF::MI, NI = CF::NI;
-  using SA = Slab<BM, A_KMAJ>;
-  using SB = Slab<BN, B_KMAJ>;
+  constexpr int BKS = CF::BKS;
+  using SA = Slab<BM, A_KMAJ, BKS>;
+  using SB = Slab<BN, B_KMAJ, BKS>;
   using SM = Smem<CF, A_KMAJ, B_KMAJ>;
   if (p.status && *p.status != 0) return;
   if ((int)blockIdx.x >= nitems) return;
@@ -212,9 +225,9 @@ __global__ void __launch_bounds__(CF::NCONS + 32, 1)
         if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
         if (lane == 0) mbar_arrive_expect_tx(&full[slot], SA::TX + SB::TX);
         __syncwarp();
-        const int k0 = kbeg + s * BK;
-        produce_slab<BM, A_KMAJ>(sA + slot * (SA::BYTES / 8), &tmA, p.A, p.lda, m0, k0, lane, &full[slot]);
-        produce_slab<BN, B_KMAJ>(sB + slot * (SB::BYTES / 8), &tmB, p.B, p.ldb, n0, k0, lane, &full[slot]);
+        const int k0 = kbeg + s * BKS;
+        produce_slab<BM, A_KMAJ, BKS>(sA + slot * (SA::BYTES / 8), &tmA, p.A, p.lda, m0, k0, lane, &full[slot]);
+        produce_slab<BN, B_KMAJ, BKS>(sB + slot * (SB::BYTES / 8), &tmB, p.B, p.ldb, n0, k0, lane, &full[slot]);
       }
     }
     return;
@@ -238,14 +251,14 @@ __global__ void __launch_bounds__(CF::NCONS + 32, 1)
   };
   int m0, n0, kbeg, ns, z;
   map.get(p, blockIdx.x, m0, n0, kbeg, ns, z);
-  if (need_c) load_c(m0, n0);
+  if (CF::CPREF && need_c) load_c(m0, n0);
   int kap[4];
 #pragma unroll
   for (int s = 0; s < 4; ++s) kap[s] = kappa(s, t);
   int it = 0;
   double acc[MI][NI][2];
   for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
-    if (need_c) {
+    if (need_c && CF::CPREF) {
       cp_async_wait<0>();
 #pragma unroll
       for (int i = 0; i < MI; ++i)
@@ -261,6 +274,16 @@ __global__ void __launch_bounds__(CF::NCONS + 32, 1)
         map.get(p, nxt, m1, n1, kb1, ns1, z1);
         load_c(m1, n1);
       }
+    } else if (need_c) {
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
+          const double2 v = *reinterpret_cast<const double2*>(p.C + (long long)r * p.ldc + c);
+          acc[i][j][0] = xor_sign(v.x, smask);
+          acc[i][j][1] = xor_sign(v.y, smask);
+        }
     } else {
 #pragma unroll
       for (int i = 0; i < MI; ++i)
@@ -273,8 +296,8 @@ __global__ void __launch_bounds__(CF::NCONS + 32, 1)
       const double* a_s = sA + slot * (SA::BYTES / 8);
       const double* b_s = sB + slot * (SB::BYTES / 8);
 #pragma unroll
-      for (int kk = 0; kk < BK / 4; ++kk) {
-        const int k = kap[kk];
+      for (int kk = 0; kk < BKS / 4; ++kk) {
+        const int k = ((kk >> 2) << 4) + kap[kk & 3];
         double af[MI], bf[NI];
 #pragma unroll
         for (int i = 0; i < MI; ++i) af[i] = tg::frag<BM, A_KMAJ>(a_s, wm * CF::WTM + i * 8 + g, k);
@@ -342,7 +365,7 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st) {
   if (B_KMAJ && !make_kmajor_map(&mb, p.B, p.N, p.K, p.ldb, CF::BN)) return cudaErrorInvalidValue;
   TItemMap<CF, MODE> map;
   map.ntn = p.N / CF::BN;
-  map.ktiles_full = p.K / tg::BK;
+  map.ktiles_full = p.K / CF::BKS;
   int ntiles;
   if (MODE == MODE_LOWER) {
     constexpr int R = CF::BM / CF::BN;
@@ -354,7 +377,7 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st) {
   map.ntiles = ntiles;
   const int nitems = ntiles * (MODE == MODE_SPLITK ? splits : 1);
   if (nitems == 0) return cudaSuccess;
-  const int nsm = tma_num_sms();
+  const int nsm = tma_num_sms() * CF::MINB;
   const int grid = nitems < nsm ? nitems : nsm;
   kern<<<grid, CF::NCONS + 32, SM::TOTAL, st>>>(ma, mb, p, nitems, map);
   return cudaGetLastError();

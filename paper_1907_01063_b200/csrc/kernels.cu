@@ -392,7 +392,7 @@ const CfgSel& cfgsel() {
 }
 
 cudaError_t gemm_full_persist(bool a_kmaj, bool b_kmaj, const GemmArgs& p, cudaStream_t st) {
-  using CF = tg::CfgT;
+  using CF = tg::CfgT32;
   if (a_kmaj && b_kmaj) return launch_tma<CF, true, true, MODE_FULL>(p, 1, st);
   if (a_kmaj && !b_kmaj) return launch_tma<CF, true, false, MODE_FULL>(p, 1, st);
   if (!a_kmaj && b_kmaj) return launch_tma<CF, false, true, MODE_FULL>(p, 1, st);
@@ -435,7 +435,7 @@ cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const doub
   if (M == 0) return cudaSuccess;
   Prof prof_(PROF_SYRK, (double)K * M * (M + 1.0), st);
   GemmArgs p{A, lda, B, ldb, C, ldc, M, M, K, K, -1.0, 1, 1, status, cfgsel().pingpong};
-  if (cfgsel().tma_syrk) return launch_tma<tg::CfgT, true, true, MODE_LOWER>(p, 1, st);
+  if (cfgsel().tma_syrk) return launch_tma<tg::CfgT32, true, true, MODE_LOWER>(p, 1, st);
   switch (cfgsel().syrk) {
     case CFG_BIG: return launch_gemm<gemm::CfgBig, true, true, MODE_LOWER>(p, 1, st);
     case CFG_W8: return launch_gemm<gemm::CfgW8, true, true, MODE_LOWER>(p, 1, st);
@@ -450,7 +450,7 @@ cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const doubl
   if (M == 0 || N == 0) return cudaSuccess;
   Prof prof_(PROF_SPLITK, 2.0 * M * N * K, st);
   GemmArgs p{A, lda, B, ldb, P, N, M, N, K, kps, 1.0, 0, 0, status, cfgsel().pingpong};
-  if (cfgsel().tma_splitk) return launch_tma<tg::CfgT, false, false, MODE_SPLITK>(p, splits, st);
+  if (cfgsel().tma_splitk) return launch_tma<tg::CfgT32, false, false, MODE_SPLITK>(p, splits, st);
   switch (cfgsel().splitk) {
     case CFG_MID: return launch_gemm<gemm::CfgMid, false, false, MODE_SPLITK>(p, splits, st);
     case CFG_W8: return launch_gemm<gemm::CfgW8, false, false, MODE_SPLITK>(p, splits, st);

@@ -21,10 +21,13 @@ __global__ void maxdiff(const double* a, const double* b, size_t n, double* out)
   atomicMax((unsigned long long*)&out[1], __double_as_longlong(s));
 }
 
-int g_impl = 0;  // 0 = w8 (one tile per CTA), 1 = tma
+int g_impl = 0;  // 0 = w8 (one tile per CTA), 1 = tma, 2 = tma 2 CTAs/SM, 3 = tma 2 CTAs + C prefetch
 template <bool AK, bool BK, int MODE>
 cudaError_t launch(GemmArgs p, int splits) {
   if (g_impl == 1) return launch_tma<tg::CfgT, AK, BK, MODE>(p, splits, 0);
+  if (g_impl == 2) return launch_tma<tg::CfgT2, AK, BK, MODE>(p, splits, 0);
+  if (g_impl == 3) return launch_tma<tg::CfgT2P, AK, BK, MODE>(p, splits, 0);
+  if (g_impl == 4) return launch_tma<tg::CfgT32, AK, BK, MODE>(p, splits, 0);
   return launch_gemm<gemm::CfgW8, AK, BK, MODE>(p, splits, 0);
 }
 template <bool AK, bool BK, int MODE>
@@ -43,7 +46,7 @@ double timeit(GemmArgs p, int splits, int reps = 5) {
   if (e != cudaSuccess) printf("ERR %s\n", cudaGetErrorString(e));
   return best;
 }
-const char* NAMES[] = {"w8", "tma"};
+const char* NAMES[] = {"w8", "tma", "tma2", "tma2p", "tma32"};
 
 // run once with impl 0 and impl 1 from the same C0 and compare
 template <bool AK, bool BK, int MODE>
@@ -52,7 +55,7 @@ void check(GemmArgs p, int splits, double* C0, double* C1, double* C2, size_t nC
   cudaMemcpy(C1, C0, nC * 8, cudaMemcpyDeviceToDevice);
   cudaMemcpy(C2, C0, nC * 8, cudaMemcpyDeviceToDevice);
   GemmArgs q = p; q.C = C1; g_impl = 0; launch<AK, BK, MODE>(q, splits);
-  q.C = C2; g_impl = 1; launch<AK, BK, MODE>(q, splits);
+  q.C = C2; g_impl = 4; launch<AK, BK, MODE>(q, splits);
   cudaMemset(d, 0, 16);
   maxdiff<<<256, 256>>>(C2, C1, nC, d);
   cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
@@ -85,7 +88,7 @@ int main() {
     GemmArgs sk{B, 128, B, 2048, nullptr, 2048, 128, 2048, 4096, 1024, 1.0, 0, 0, nullptr, 0};
     check<false, false, MODE_SPLITK>(sk, 4, C, C1, C2, (size_t)4 * 128 * 2048, d, "splitk_n2048_k4096");
   }
-  for (int impl : {0, 1}) {
+  for (int impl : {1, 4}) {
     g_impl = impl;
     for (int K : {128, 256}) {
       GemmArgs s{A, K, A, K, C, M, M, M, K, K, -1.0, 1, 1, nullptr, 0};
