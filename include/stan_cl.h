@@ -107,8 +107,9 @@ int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_ba
 /* ---- control ---- */
 int stan_cl_set_stream(void* cuda_stream); /* cudaStream_t; NULL = legacy default stream */
 void* stan_cl_get_stream(void);
-/* block size of the blocked algorithms; 0 = auto (128).  Only 0 and 128 are
- * supported in this version; others -> STAN_CL_EINVAL. */
+/* outer block size of the blocked Cholesky: 0 = auto (256 = two-level blocking
+ * with 128-wide diagonal tiles when it pays, else 128), 128 or 256; others ->
+ * STAN_CL_EINVAL.  The adjoint always uses 128-wide diagonal blocks. */
 int stan_cl_set_block_size(int nb);
 int stan_cl_get_block_size(void);
 /* device workspace the next call of order n would use (bytes) */

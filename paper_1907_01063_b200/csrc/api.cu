@@ -29,7 +29,7 @@ struct State {
   cudaStream_t stream = nullptr;  // nullptr = legacy default stream
   cudaStream_t side = nullptr;    // library-owned high-priority stream (panel lookahead)
   std::vector<cudaEvent_t> events;
-  int nb = NB;
+  int nb = 0;  // forward outer block: 0 = auto, 128 or 256
   void* ws = nullptr;  // library-owned persistent workspace
   size_t ws_cap = 0;
   int* h_status = nullptr;  // pinned host word for the synchronous calls
@@ -159,41 +159,61 @@ int ensure_side(size_t nevents) {
   return STAN_CL_OK;
 }
 
+// The factored panel of outer block [c0, c0+OB): L11 = chol(A11) and
+// L21 = A21 L11^-T.  OB = 128: one POTRF tile + one TRSM.
+// OB = 256 (two-level blocking): two 128 sub-steps with the second half of the
+// panel updated in between (GEMM, K = 128), so the trailing update outside
+// the panel runs with K = 256.
+int panel(double* W, int64_t ld, int64_t c0, int64_t N, int64_t OB, int* status, cudaStream_t st) {
+  CK(potrf_tile(W, ld, c0, status, st));
+  if (c0 + NB < N) CK(trsm_panel(W, ld, c0, c0 + NB, N, status, st));
+  if (OB == 2 * NB) {
+    const int64_t h = c0 + NB;
+    const double* L21 = W + h * ld + c0;
+    CK(gemm_full(true, true, (int)(N - h), NB, NB, -1.0, 1, L21, ld, L21, ld, W + h * ld + h, ld, status, st,
+                 /*lower_only=*/1, PROF_SYRK));
+    CK(potrf_tile(W, ld, h, status, st));
+    if (h + NB < N) CK(trsm_panel(W, ld, h, h + NB, N, status, st));
+  }
+  return STAN_CL_OK;
+}
+
 // Right-looking blocked Cholesky on the N x N working matrix W (lower part),
-// PAPER.md:264-285 with a fixed block of NB, and one step of lookahead: the
-// panel of step k+1 (POTRF + TRSM, the latency-bound critical path) runs on the
-// high-priority side stream while the main stream applies the rest of step k's
-// trailing update.  Per step k (blocks of NB):
-//   main: wait panel k; A[k+1 col] -= L21 L21(k+1)^T        (lookahead column)
-//   side: POTRF(k+1); TRSM(k+1)                            (L11 = chol(A11); L21 = A21 L11^-T)
-//   main: A22[k+2.., k+2..] -= L21 L21^T (lower tiles)      (multiply_transpose)
-int factor_inplace(double* W, int64_t N, int64_t ld, int* status) {
+// PAPER.md:264-285 with a fixed outer block OB (N % OB == 0), and one step of
+// lookahead: the panel of step k+1 (the latency-bound critical path) runs on
+// the high-priority side stream while the main stream applies the rest of step
+// k's trailing update.  Per step k:
+//   main: wait panel k; A[col block k+1] -= L21 L21(k+1)^T     (lookahead column)
+//   side: panel(k+1)                                          (L11 = chol(A11); L21 = A21 L11^-T)
+//   main: A22[k+2.., k+2..] -= L21 L21^T (lower tiles)         (multiply_transpose)
+int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status) {
   cudaStream_t main = g.stream;
-  const int64_t T = N / NB;
+  const int64_t T = N / OB;
   int rc = ensure_side(2 * T + 2);
   if (rc) return rc;
-  cudaStream_t side = g.side;
+  static const bool no_lookahead = getenv("STAN_CL_NO_LOOKAHEAD") != nullptr;  // debugging aid
+  cudaStream_t side = no_lookahead ? main : g.side;
   cudaEvent_t* ev = g.events.data();  // ev[0]: start; ev[1 + 2k]: panel k done; ev[2 + 2k]: column k+1 ready
   CK(cudaEventRecord(ev[0], main));
   CK(cudaStreamWaitEvent(side, ev[0], 0));
-  CK(potrf_tile(W, ld, 0, status, side));
-  if (T > 1) CK(trsm_panel(W, ld, 0, NB, N, status, side));
+  rc = panel(W, ld, 0, N, OB, status, side);
+  if (rc) return rc;
   CK(cudaEventRecord(ev[1], side));
   for (int64_t k = 0; k < T; ++k) {
     CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
     if (k == T - 1) break;
-    const int64_t c0 = k * NB, r1 = (k + 1) * NB, r2 = r1 + NB;
+    const int64_t c0 = k * OB, r1 = (k + 1) * OB, r2 = r1 + OB;
     const double* L21 = W + r1 * ld + c0;
-    CK(gemm_full(true, true, (int)(N - r1), NB, NB, -1.0, 1, L21, ld, L21, ld, W + r1 * ld + r1, ld, status,
-                 main, /*lower_only=*/1, PROF_SYRK));
+    CK(gemm_full(true, true, (int)(N - r1), (int)OB, (int)OB, -1.0, 1, L21, ld, L21, ld, W + r1 * ld + r1, ld,
+                 status, main, /*lower_only=*/1, PROF_SYRK));
     CK(cudaEventRecord(ev[2 + 2 * k], main));
     CK(cudaStreamWaitEvent(side, ev[2 + 2 * k], 0));
-    CK(potrf_tile(W, ld, r1, status, side));
-    if (r2 < N) CK(trsm_panel(W, ld, r1, r2, N, status, side));
+    rc = panel(W, ld, r1, N, OB, status, side);
+    if (rc) return rc;
     CK(cudaEventRecord(ev[1 + 2 * (k + 1)], side));
     if (r2 < N) {
       const double* L31 = W + r2 * ld + c0;
-      CK(gemm_lower_nt((int)(N - r2), NB, L31, ld, L31, ld, W + r2 * ld + r2, ld, status, main));
+      CK(gemm_lower_nt((int)(N - r2), (int)OB, L31, ld, L31, ld, W + r2 * ld + r2, ld, status, main));
     }
   }
   return STAN_CL_OK;
@@ -213,11 +233,14 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
   int* status = (int*)g.ws;
   cudaStream_t st = g.stream;
   CK(cudaMemsetAsync(status, 0, sizeof(int), st));
-  const int64_t N = round_up(n, NB);
+  // outer block: 256 (two-level) when it divides n, else 128 (set_block_size overrides)
+  int64_t OB = g.nb;
+  if (!OB) OB = (n % (2 * NB) == 0) ? 2 * NB : (n % NB == 0) ? NB : (n > 1024 ? 2 * NB : NB);
+  const int64_t N = round_up(n, OB);
   const bool fast = (N == n) && aligned16(A) && aligned16(L);
   if (fast) {
     if (A != L) CK(copy_lower_pad(A, n, n, L, n, n, 1.0, st));
-    rc = factor_inplace(L, n, n, status);
+    rc = factor_inplace(L, n, n, OB, status);
     if (rc) return rc;
     if (A == L) CK(zero_upper(L, n, n, st));
   } else {
@@ -225,7 +248,7 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
     rc = alloc_async(&W, (size_t)N * N * sizeof(double));
     if (rc) return rc;
     CK(copy_lower_pad(A, n, n, W, N, N, 1.0, st));
-    rc = factor_inplace(W, N, N, status);
+    rc = factor_inplace(W, N, N, OB, status);
     if (rc) return rc;
     CK(copy_lower_out(W, N, L, n, n, st));
     CK(cudaFreeAsync(W, st));
@@ -415,8 +438,8 @@ int stan_cl_set_stream(void* s) {
 void* stan_cl_get_stream(void) { return (void*)g.stream; }
 
 int stan_cl_set_block_size(int nb) {
-  if (nb == 0 || nb == NB) {
-    g.nb = NB;
+  if (nb == 0 || nb == NB || nb == 2 * NB) {
+    g.nb = nb;
     return STAN_CL_OK;
   }
   return STAN_CL_EINVAL;

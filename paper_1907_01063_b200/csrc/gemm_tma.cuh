@@ -268,12 +268,6 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
           acc[i][j][0] = xor_sign(v.x, smask);
           acc[i][j][1] = xor_sign(v.y, smask);
         }
-      const int nxt = item + gridDim.x;
-      if (nxt < nitems) {
-        int m1, n1, kb1, ns1, z1;
-        map.get(p, nxt, m1, n1, kb1, ns1, z1);
-        load_c(m1, n1);
-      }
     } else if (need_c) {
 #pragma unroll
       for (int i = 0; i < MI; ++i)
@@ -310,6 +304,17 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
+      if (CF::CPREF && need_c && s == 0) {
+        // prefetch the next item's C into the private slots only now: the DMMAs
+        // above consumed acc (loaded from these slots), and asm-volatile order
+        // keeps this cp.async behind them, so the refill cannot overtake the read
+        const int nxt = item + gridDim.x;
+        if (nxt < nitems) {
+          int m1, n1, kb1, ns1, z1;
+          map.get(p, nxt, m1, n1, kb1, ns1, z1);
+          load_c(m1, n1);
+        }
+      }
     }
     // epilogue: registers -> global
     double* Cout;

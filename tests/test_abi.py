@@ -47,7 +47,8 @@ def test_binding_signatures_cover_header(lib_path):
     assert lib.stan_cl_version() >= 100
     # pure host-side calls (no device work)
     assert lib.stan_cl_status_string(-1) == b"invalid argument"
-    assert lib.stan_cl_set_block_size(0) == 0 and lib.stan_cl_get_block_size() == 128
+    assert lib.stan_cl_set_block_size(256) == 0 and lib.stan_cl_get_block_size() == 256
+    assert lib.stan_cl_set_block_size(0) == 0 and lib.stan_cl_get_block_size() == 0
     assert lib.stan_cl_set_block_size(96) == -1
     assert lib.stan_cl_workspace_bytes(0) == 0
     assert lib.stan_cl_workspace_bytes(16384) > 16384 * 128 * 8

@@ -84,6 +84,33 @@ def test_cholesky_integer_exact(sc, n):
     assert np.array_equal(host(sc.cholesky(dev(A))), L0)
 
 
+@pytest.mark.parametrize("n", [300, 1000, 1024, 2048])
+def test_cholesky_blocking_invariance(sc, n):
+    # outer block 128 vs 256 (two-level): both within the bar of the oracle and of
+    # each other (SPEC.md:490 blocking invariance)
+    K = se(n)
+    want = oracle.cholesky(K)
+    lib = sc.load()
+    outs = []
+    try:
+        for nb in (128, 256):
+            assert lib.stan_cl_set_block_size(nb) == 0
+            outs.append(host(sc.cholesky(dev(K))))
+    finally:
+        lib.stan_cl_set_block_size(0)
+    for o in outs:
+        assert relf(o, want) <= L_BAR_TOL
+    assert relf(outs[0], outs[1]) <= L_BAR_TOL
+    L0 = inputs.unit_lower_pm1(n, seed=n + 1)
+    A = inputs.gram_exact(L0)
+    for nb in (128, 256):
+        lib.stan_cl_set_block_size(nb)
+        try:
+            assert np.array_equal(host(sc.cholesky(dev(A))), L0)
+        finally:
+            lib.stan_cl_set_block_size(0)
+
+
 def test_cholesky_in_place_and_upper_garbage(sc):
     n = 384
     K = se(n)
@@ -140,11 +167,16 @@ def test_cholesky_non_default_stream(sc):
     assert relf(host(L), want) <= L_BAR_TOL
 
 
-def test_cholesky_deterministic(sc):
-    K = dev(se(1024))
-    a = sc.cholesky(K)
-    b = sc.cholesky(K)
-    assert torch.equal(a, b)
+@pytest.mark.parametrize("n", [1024, 4096])
+def test_deterministic(sc, n):
+    # fixed reduction orders everywhere (no atomics in the arithmetic): repeated
+    # runs are bit-identical; also catches ordering races
+    K = dev(se(n))
+    Ls = [sc.cholesky(K) for _ in range(3)]
+    assert all(torch.equal(Ls[0], x) for x in Ls[1:])
+    W = dev(inputs.lbar(n))
+    As = [sc.cholesky_adjoint(Ls[0], W) for _ in range(3)]
+    assert all(torch.equal(As[0], x) for x in As[1:])
 
 
 # --------------------------------------------------------------------- adjoint

@@ -85,6 +85,12 @@ int main() {
     check<true, false, MODE_FULL>(g, 1, C, C1, C2, (size_t)m * 2048, d, "gemm_kn_m1024_n2048");
     GemmArgs g2{A, 128, A + 128 * 128, 128, nullptr, 128, m, 128, 128, 128, 1.0, 0, 0, nullptr, 0};
     check<true, true, MODE_FULL>(g2, 1, C, C1, C2, (size_t)m * 128, d, "gemm_kk_beta0");
+    GemmArgs s2{A, 256, A, 256, nullptr, m, m, m, 256, 256, -1.0, 1, 1, nullptr, 0};
+    check<true, true, MODE_LOWER>(s2, 1, C, C1, C2, (size_t)m * m, d, "syrk_lower_m1024_k256");
+    GemmArgs g3{A, 256, A + 4096 * 256, 256, nullptr, 256, 4096, 256, 256, 256, -1.0, 1, 1, nullptr, 0};
+    check<true, true, MODE_FULL>(g3, 1, C, C1, C2, (size_t)4096 * 256, d, "lookahead_m4096_n256_k256");
+    GemmArgs g4{A, 256, B, 2048, nullptr, 2048, m, 2048, 256, 256, -1.0, 1, 0, nullptr, 0};
+    check<true, false, MODE_FULL>(g4, 1, C, C1, C2, (size_t)m * 2048, d, "gemm_kn_k256");
     GemmArgs sk{B, 128, B, 2048, nullptr, 2048, 128, 2048, 4096, 1024, 1.0, 0, 0, nullptr, 0};
     check<false, false, MODE_SPLITK>(sk, 4, C, C1, C2, (size_t)4 * 128 * 2048, d, "splitk_n2048_k4096");
   }
