@@ -119,17 +119,22 @@ const char* stan_cl_status_string(int status);
 long long stan_cl_kernel_launches(void);
 /*
  * Per-kernel-class timing with CUDA events recorded on the launch stream around
- * every kernel the library issues (off by default; a few microseconds of host
- * overhead per launch when on).  Classes (kind): 0 SYRK trailing update,
- * 1 adjoint DMMA GEMMs, 2 split-K long-K contraction, 3 POTRF tile, 4 TRSM panel,
- * 5 batched diagonal-block inverse, 6 128^3 products, 7 SE build, 8 other.
+ * the kernels the library issues (off by default; a few microseconds of host
+ * overhead per recorded launch).  Classes (kind): 0 SYRK trailing update,
+ * 1 adjoint DMMA GEMMs (B_bar, R_bar updates), 2 split-K long-K contraction,
+ * 3 POTRF tile, 4 TRSM panel, 5 batched diagonal-block inverse, 6 128^3
+ * products, 7 SE build, 8 other, 9 forward lookahead-column GEMMs,
+ * 10 C_bar D^-1 products.  stan_cl_profile_enable(on): 0 = off, 1 = every
+ * class, otherwise (mask << 1) enables class k when bit k of mask is set.
  * stan_cl_profile_read synchronises on the recorded events and returns the
  * summed milliseconds, the summed algorithmic flops and the launch count of a
  * class since the last reset.
  */
-int stan_cl_profile_enable(int on);
+int stan_cl_profile_enable(int on);  /* see above */
 int stan_cl_profile_reset(void);
 int stan_cl_profile_read(int kind, double* ms, double* flops, long long* launches);
+/* summed algorithmic (minimum) HBM bytes of the recorded launches of a class */
+int stan_cl_profile_read_bytes(int kind, double* bytes);
 /* release library-owned device workspace; the library stays usable */
 int stan_cl_finalize(void);
 int stan_cl_version(void); /* major*10000 + minor*100 + patch */

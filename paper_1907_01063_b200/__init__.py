@@ -54,6 +54,7 @@ SIGNATURES = {
     "stan_cl_profile_reset": (_I, []),
     "stan_cl_profile_read": (_I, [_I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_longlong)]),
+    "stan_cl_profile_read_bytes": (_I, [_I, ctypes.POINTER(ctypes.c_double)]),
     "stan_cl_finalize": (_I, []),
     "stan_cl_version": (_I, []),
 }
@@ -205,11 +206,21 @@ def kernel_launches() -> int:
     return int(load().stan_cl_kernel_launches())
 
 
-PROFILE_KINDS = ["syrk", "adj_gemm", "splitk", "potrf", "trsm", "tri_inverse", "gemm128", "se_cov", "other"]
+PROFILE_KINDS = ["syrk", "adj_gemm", "splitk", "potrf", "trsm", "tri_inverse", "gemm128", "se_cov", "other",
+                 "lookahead", "trmm"]
 
 
-def profile_enable(on: bool = True) -> None:
-    load().stan_cl_profile_enable(1 if on else 0)
+def profile_enable(on: bool = True, kinds=None) -> None:
+    """Record CUDA events around every launch (kinds=None) or only those classes."""
+    if not on:
+        load().stan_cl_profile_enable(0)
+    elif kinds is None:
+        load().stan_cl_profile_enable(1)
+    else:
+        mask = 0
+        for k in kinds:
+            mask |= 1 << PROFILE_KINDS.index(k)
+        load().stan_cl_profile_enable(mask << 1)
 
 
 def profile_reset() -> None:
@@ -217,12 +228,14 @@ def profile_reset() -> None:
 
 
 def profile_read() -> dict:
-    """{class: {"ms": summed event ms, "flops": algorithmic flops, "launches": n}}"""
+    """{class: {"ms": summed event ms, "flops": algorithmic flops, "bytes": algorithmic
+    HBM bytes, "launches": n}}"""
     out = {}
     for k, name in enumerate(PROFILE_KINDS):
-        ms, fl, cnt = ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong()
+        ms, fl, cnt, by = ctypes.c_double(), ctypes.c_double(), ctypes.c_longlong(), ctypes.c_double()
         load().stan_cl_profile_read(k, ctypes.byref(ms), ctypes.byref(fl), ctypes.byref(cnt))
-        out[name] = {"ms": ms.value, "flops": fl.value, "launches": cnt.value}
+        load().stan_cl_profile_read_bytes(k, ctypes.byref(by))
+        out[name] = {"ms": ms.value, "flops": fl.value, "bytes": by.value, "launches": cnt.value}
     return out
 
 

@@ -171,7 +171,7 @@ int panel(double* W, int64_t ld, int64_t c0, int64_t N, int64_t OB, int* status,
     const int64_t h = c0 + NB;
     const double* L21 = W + h * ld + c0;
     CK(gemm_full(true, true, (int)(N - h), NB, NB, -1.0, 1, L21, ld, L21, ld, W + h * ld + h, ld, status, st,
-                 /*lower_only=*/1, PROF_SYRK));
+                 /*lower_only=*/1, PROF_LOOKAHEAD));
     CK(potrf_tile(W, ld, h, status, st));
     if (h + NB < N) CK(trsm_panel(W, ld, h, h + NB, N, status, st));
   }
@@ -205,7 +205,7 @@ int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status) {
     const int64_t c0 = k * OB, r1 = (k + 1) * OB, r2 = r1 + OB;
     const double* L21 = W + r1 * ld + c0;
     CK(gemm_full(true, true, (int)(N - r1), (int)OB, (int)OB, -1.0, 1, L21, ld, L21, ld, W + r1 * ld + r1, ld,
-                 status, main, /*lower_only=*/1, PROF_SYRK));
+                 status, main, /*lower_only=*/1, PROF_LOOKAHEAD));
     CK(cudaEventRecord(ev[2 + 2 * k], main));
     CK(cudaStreamWaitEvent(side, ev[2 + 2 * k], 0));
     rc = panel(W, ld, r1, N, OB, status, side);
@@ -283,7 +283,7 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
     double* Dbar = Wm + j * ld + j;      // D_adj
     if (m > 0) {
       // C_adj = C_adj * lower_triangular_inverse(D)
-      CK(gemm_full(true, false, (int)m, NB, NB, 1.0, 0, Cb, ld, Db, NB, Cb, ld, status, st));
+      CK(gemm_full(true, false, (int)m, NB, NB, 1.0, 0, Cb, ld, Db, NB, Cb, ld, status, st, 0, PROF_TRMM));
       // B_adj = B_adj - C_adj * R
       if (j > 0)
         CK(gemm_full(true, false, (int)m, (int)j, NB, -1.0, 1, Cb, ld, R, ld, Wm + k * ld, ld, status, st));
@@ -467,8 +467,8 @@ const char* stan_cl_status_string(int status) {
 
 long long stan_cl_kernel_launches(void) { return launches(); }
 
-int stan_cl_profile_enable(int on) {
-  prof_enable(on != 0);
+int stan_cl_profile_enable(int mask) {
+  prof_enable(mask == 1 ? ~0u : (unsigned)mask >> 1);
   return STAN_CL_OK;
 }
 
@@ -480,6 +480,14 @@ int stan_cl_profile_reset(void) {
 int stan_cl_profile_read(int kind, double* ms, double* flops, long long* n) {
   if (kind < 0 || kind >= PROF_KINDS || !ms || !flops || !n) return STAN_CL_EINVAL;
   prof_read(kind, ms, flops, n);
+  return STAN_CL_OK;
+}
+
+int stan_cl_profile_read_bytes(int kind, double* bytes) {
+  if (kind < 0 || kind >= PROF_KINDS || !bytes) return STAN_CL_EINVAL;
+  double ms, fl;
+  long long n;
+  prof_read(kind, &ms, &fl, &n, bytes);
   return STAN_CL_OK;
 }
 

@@ -35,15 +35,16 @@ long long launches() { return g_launches.load(std::memory_order_relaxed); }
 namespace {
 struct ProfRec {
   int kind;
-  double flops;
+  double flops, bytes;
   cudaEvent_t e0, e1;
 };
 struct ProfState {
-  bool on = false;
+  unsigned mask = 0;
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
   double ms[PROF_KINDS] = {0};
   double flops[PROF_KINDS] = {0};
+  double bytes[PROF_KINDS] = {0};
   long long count[PROF_KINDS] = {0};
 };
 ProfState g_prof;
@@ -59,21 +60,22 @@ cudaEvent_t prof_event() {
 }
 }  // namespace
 
-Prof::Prof(int kind, double flops, cudaStream_t st) : kind_(kind), flops_(flops), st_(st) {
+Prof::Prof(int kind, double flops, cudaStream_t st, double bytes)
+    : kind_(kind), flops_(flops), bytes_(bytes), st_(st) {
   count_launch();
-  if (g_prof.on) {
+  if ((g_prof.mask >> kind) & 1u) {
     e0_ = prof_event();
     e1_ = prof_event();
     cudaEventRecord(e0_, st_);
   }
 }
 Prof::~Prof() {
-  if (g_prof.on && e0_) {
+  if (e0_) {
     cudaEventRecord(e1_, st_);
-    g_prof.recs.push_back({kind_, flops_, e0_, e1_});
+    g_prof.recs.push_back({kind_, flops_, bytes_, e0_, e1_});
   }
 }
-void prof_enable(bool on) { g_prof.on = on; }
+void prof_enable(unsigned mask) { g_prof.mask = mask; }
 void prof_collect() {
   for (auto& r : g_prof.recs) {
     cudaEventSynchronize(r.e1);
@@ -81,6 +83,7 @@ void prof_collect() {
     cudaEventElapsedTime(&ms, r.e0, r.e1);
     g_prof.ms[r.kind] += ms;
     g_prof.flops[r.kind] += r.flops;
+    g_prof.bytes[r.kind] += r.bytes;
     g_prof.count[r.kind] += 1;
     g_prof.pool.push_back(r.e0);
     g_prof.pool.push_back(r.e1);
@@ -89,13 +92,14 @@ void prof_collect() {
 }
 void prof_reset() {
   prof_collect();
-  for (int k = 0; k < PROF_KINDS; ++k) g_prof.ms[k] = g_prof.flops[k] = 0, g_prof.count[k] = 0;
+  for (int k = 0; k < PROF_KINDS; ++k) g_prof.ms[k] = g_prof.flops[k] = g_prof.bytes[k] = 0, g_prof.count[k] = 0;
 }
-void prof_read(int kind, double* ms, double* flops, long long* count) {
+void prof_read(int kind, double* ms, double* flops, long long* count, double* bytes) {
   prof_collect();
   *ms = g_prof.ms[kind];
   *flops = g_prof.flops[kind];
   *count = g_prof.count[kind];
+  if (bytes) *bytes = g_prof.bytes[kind];
 }
 
 static inline int grid_for(long long work, int threads, int cap = 148 * 16) {
@@ -123,7 +127,7 @@ __global__ void se_cov_kernel(int64_t n, const double* __restrict__ x, double sq
 
 cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
                    cudaStream_t st) {
-  Prof prof_(PROF_SE, 0.0, st);
+  Prof prof_(PROF_SE, 0.0, st, 8.0 * n * n + 8.0 * n);
   if (n == 0) return cudaSuccess;
   const double sq_alpha = alpha * alpha;
   const double c = -0.5 / (rho * rho);
@@ -148,7 +152,7 @@ __global__ void copy_lower_pad_kernel(const double* __restrict__ src, int64_t n,
 
 cudaError_t copy_lower_pad(const double* src, int64_t n, int64_t lds, double* dst, int64_t N,
                            int64_t ldd, double diag_pad, cudaStream_t st) {
-  Prof prof_(PROF_MISC, 0.0, st);
+  Prof prof_(PROF_MISC, 0.0, st, 8.0 * N * N + 4.0 * n * n);
   if (N == 0) return cudaSuccess;
   copy_lower_pad_kernel<<<grid_for((long long)N * N, 256), 256, 0, st>>>(src, n, lds, dst, N, ldd,
                                                                           diag_pad);
@@ -167,7 +171,7 @@ __global__ void copy_lower_out_kernel(const double* __restrict__ src, int64_t ld
 
 cudaError_t copy_lower_out(const double* src, int64_t lds, double* dst, int64_t n, int64_t ldd,
                            cudaStream_t st) {
-  Prof prof_(PROF_MISC, 0.0, st);
+  Prof prof_(PROF_MISC, 0.0, st, 12.0 * n * n);
   if (n == 0) return cudaSuccess;
   copy_lower_out_kernel<<<grid_for((long long)n * n, 256), 256, 0, st>>>(src, lds, dst, n, ldd);
   return cudaGetLastError();
@@ -183,7 +187,7 @@ __global__ void zero_upper_kernel(double* A, int64_t n, int64_t ld) {
 }
 
 cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st) {
-  Prof prof_(PROF_MISC, 0.0, st);
+  Prof prof_(PROF_MISC, 0.0, st, 4.0 * n * n);
   if (n == 0) return cudaSuccess;
   zero_upper_kernel<<<grid_for((long long)n * n, 256), 256, 0, st>>>(A, n, ld);
   return cudaGetLastError();
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t l
 }
 
 cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStream_t st) {
-  Prof prof_(PROF_POTRF, (double)NB * NB * NB / 3.0, st);
+  Prof prof_(PROF_POTRF, (double)NB * NB * NB / 3.0, st, 8.0 * NB * (NB + 1));
   potrf_tile_kernel<<<1, 256, 0, st>>>(W, ld, k0, status);
   return cudaGetLastError();
 }
@@ -331,7 +335,7 @@ __global__ void __launch_bounds__(256, 1) trsm_panel_kernel(double* W, int64_t l
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
-  Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st);
+  Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st, 16.0 * (r1 - r0) * NB + 4.0 * NB * NB);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -412,7 +416,7 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st, int lower_only, int prof_kind) {
   if (M == 0 || N == 0) return cudaSuccess;
-  Prof prof_(prof_kind, 2.0 * M * N * K, st);
+  Prof prof_(prof_kind, 2.0 * M * N * K, st, (beta ? 16.0 : 8.0) * M * N + 8.0 * ((double)M * K + (double)N * K));
   GemmArgs p{A, lda, B, ldb, C, ldc, M, N, K, K, sign, beta, lower_only, status, cfgsel().pingpong};
   // A aliasing C (in-place C <- A B): one CTA must own whole rows of C, i.e. a
   // single 128-wide tile column with the one-tile-per-CTA kernel
@@ -433,7 +437,7 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                           double* C, int64_t ldc, const int* status, cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  Prof prof_(PROF_SYRK, (double)K * M * (M + 1.0), st);
+  Prof prof_(PROF_SYRK, (double)K * M * (M + 1.0), st, 8.0 * M * (M + 1.0) + 8.0 * (double)M * K);
   GemmArgs p{A, lda, B, ldb, C, ldc, M, M, K, K, -1.0, 1, 1, status, cfgsel().pingpong};
   if (cfgsel().tma_syrk) return launch_tma<tg::CfgT32, true, true, MODE_LOWER>(p, 1, st);
   switch (cfgsel().syrk) {
@@ -448,7 +452,7 @@ cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const doubl
                            const double* B, int64_t ldb, double* P, const int* status,
                            cudaStream_t st) {
   if (M == 0 || N == 0) return cudaSuccess;
-  Prof prof_(PROF_SPLITK, 2.0 * M * N * K, st);
+  Prof prof_(PROF_SPLITK, 2.0 * M * N * K, st, 8.0 * ((double)M * K + (double)K * N) + 8.0 * splits * (double)M * N);
   GemmArgs p{A, lda, B, ldb, P, N, M, N, K, kps, 1.0, 0, 0, status, cfgsel().pingpong};
   if (cfgsel().tma_splitk) return launch_tma<tg::CfgT32, false, false, MODE_SPLITK>(p, splits, st);
   switch (cfgsel().splitk) {
@@ -484,7 +488,7 @@ __global__ void splitk_reduce_sub_kernel(const double* __restrict__ P, int split
 
 cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double* dst, int64_t ldd,
                               const int* status, cudaStream_t st) {
-  Prof prof_(PROF_MISC, 0.0, st);
+  Prof prof_(PROF_MISC, 0.0, st, 8.0 * (splits + 2.0) * M * N);
   if (M == 0 || N == 0) return cudaSuccess;
   splitk_reduce_sub_kernel<<<grid_for((long long)M * N / 2, 256), 256, 0, st>>>(P, splits, M, N, dst,
                                                                                 ldd, status);
@@ -530,7 +534,7 @@ __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, in
 
 cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* Dinv,
                                 const int* status, cudaStream_t st) {
-  Prof prof_(PROF_TRINV, (double)nblk * NB * NB * NB / 3.0, st);
+  Prof prof_(PROF_TRINV, (double)nblk * NB * NB * NB / 3.0, st, 12.0 * nblk * NB * NB);
   if (nblk == 0) return cudaSuccess;
   static bool attr = false;
   if (!attr) {
@@ -620,7 +624,7 @@ __global__ void __launch_bounds__(128) gemm128_kernel(bool a_t, bool a_tril, boo
 cudaError_t gemm128(bool a_t, bool a_tril, bool b_t, bool b_sym, const double* A, int64_t lda,
                     const double* B, int64_t ldb, double* C, int64_t ldc, const int* status,
                     cudaStream_t st) {
-  Prof prof_(PROF_SMALL, 2.0 * NB * NB * NB, st);
+  Prof prof_(PROF_SMALL, 2.0 * NB * NB * NB, st, 24.0 * NB * NB);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(gemm128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -646,7 +650,7 @@ __global__ void phi_sym_kernel(const double* __restrict__ S, double* __restrict_
 
 cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, const int* status,
                     cudaStream_t st) {
-  Prof prof_(PROF_MISC, 0.0, st);
+  Prof prof_(PROF_MISC, 0.0, st, 24.0 * NB * NB);
   phi_sym_kernel<<<64, 256, 0, st>>>(S, Ssym, Dbar, ldd, status);
   return cudaGetLastError();
 }
@@ -668,7 +672,7 @@ __global__ void check_diag_kernel(const double* L, int64_t n, int64_t ld, int* s
 }
 
 cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st) {
-  Prof prof_(PROF_MISC, 0.0, st);
+  Prof prof_(PROF_MISC, 0.0, st, 8.0 * n);
   if (n == 0) return cudaSuccess;
   check_diag_kernel<<<grid_for(n, 256, 148), 256, 0, st>>>(L, n, ld, status);
   return cudaGetLastError();

@@ -11,30 +11,32 @@ namespace stancl {
 void count_launch(int k = 1);
 long long launches();
 enum ProfKind {
-  PROF_SYRK = 0,    // F3 trailing update (DMMA, lower tiles)
-  PROF_GEMM = 1,    // R1/R3/R5 DMMA GEMMs (C_bar D^-1, B_bar -= C_bar R, R_bar -= S R)
-  PROF_SPLITK = 2,  // R2 long-K contraction C_bar^T [B C] (DMMA, split-K)
-  PROF_POTRF = 3,   // F1 diagonal tile
-  PROF_TRSM = 4,    // F2 panel solve
-  PROF_TRINV = 5,   // R1 batched diagonal-block inverses
-  PROF_SMALL = 6,   // R4 128^3 products of the symbolic diagonal step
-  PROF_SE = 7,      // F0 covariance build
-  PROF_MISC = 8,    // copies, reductions, Phi, checks
-  PROF_KINDS = 9
+  PROF_SYRK = 0,       // F3 trailing update outside the lookahead column (DMMA, lower tiles)
+  PROF_GEMM = 1,       // R3/R5 DMMA GEMMs (B_bar -= C_bar R, R_bar -= S R)
+  PROF_SPLITK = 2,     // R2 long-K contraction C_bar^T [B C] (DMMA, split-K)
+  PROF_POTRF = 3,      // F1 diagonal tile
+  PROF_TRSM = 4,       // F2 panel solve
+  PROF_TRINV = 5,      // R1 batched diagonal-block inverses
+  PROF_SMALL = 6,      // R4 128^3 products of the symbolic diagonal step
+  PROF_SE = 7,         // F0 covariance build
+  PROF_MISC = 8,       // copies, reductions, Phi, checks
+  PROF_LOOKAHEAD = 9,  // F3 lookahead column + in-panel update (DMMA)
+  PROF_TRMM = 10,      // R1 C_bar <- C_bar D^-1 (DMMA)
+  PROF_KINDS = 11
 };
 // RAII launch scope: counts the launch and, when profiling is on, brackets it
 // with CUDA events on its stream
 struct Prof {
-  Prof(int kind, double flops, cudaStream_t st);
+  Prof(int kind, double flops, cudaStream_t st, double bytes = 0.0);  // bytes: algorithmic HBM bytes
   ~Prof();
   int kind_;
-  double flops_;
+  double flops_, bytes_;
   cudaStream_t st_;
   cudaEvent_t e0_ = nullptr, e1_ = nullptr;
 };
-void prof_enable(bool on);
+void prof_enable(unsigned mask);  // bit k enables class k
 void prof_reset();
-void prof_read(int kind, double* ms, double* flops, long long* count);
+void prof_read(int kind, double* ms, double* flops, long long* count, double* bytes = nullptr);
 
 // ---- F0: SE covariance (K1) ----
 cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
