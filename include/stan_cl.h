@@ -97,9 +97,17 @@ int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_b
 
 /*
  * Host-buffer variants (end-to-end, the quantity PAPER.md:295, 332 measures):
- * all matrix pointers are HOST pointers (pinned memory is fastest); the call
- * copies the lower triangles to the device, runs the device path, copies the
- * result back and returns after the copy-back.  Same return values.
+ * all matrix pointers are HOST pointers (row-major, leading dimension n; pinned
+ * memory is fastest).  Only the lower triangles cross PCIe -- the paper's
+ * packed transfers -- as one rectangle per 128-row block
+ * (rows r0..r1-1, columns 0..r1-1), streamed against the compute: the forward
+ * ships each factored panel while the trailing update continues; the adjoint
+ * uploads row blocks bottom-up (the order its reverse sweep consumes them) and
+ * ships each column block of A_bar as soon as it is final.  The call returns
+ * after the last copy-back.  Output contract: the lower triangle of the host
+ * output is written; inside the 128 x 128 diagonal tiles the strict upper part
+ * is written as +0.0; the rest of the strict upper triangle is NOT written
+ * (LAPACK convention).  Same return values as the device calls.
  */
 int stan_cl_cholesky_host(int64_t n, const double* A, double* L);
 int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar);

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <algorithm>
 #include <mutex>
 #include <vector>
 
@@ -28,7 +29,11 @@ namespace {
 struct State {
   cudaStream_t stream = nullptr;  // nullptr = legacy default stream
   cudaStream_t side = nullptr;    // library-owned high-priority stream (panel lookahead)
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the *_host entry points
   std::vector<cudaEvent_t> events;
+  std::vector<cudaEvent_t> xev;  // per-block events of the streamed host transfers
+  void* mat[2] = {nullptr, nullptr};  // cached N x N working matrices (padded / host paths)
+  size_t mat_cap[2] = {0, 0};
   int nb = 0;  // forward outer block: 0 = auto, 128 or 256
   void* ws = nullptr;  // library-owned persistent workspace
   size_t ws_cap = 0;
@@ -134,15 +139,29 @@ int ensure_host_status() {
   return STAN_CL_OK;
 }
 
-int alloc_async(double** p, size_t bytes) {
-  cudaError_t e = cudaMallocAsync((void**)p, bytes, g.stream);
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    snprintf(g.last_err, sizeof(g.last_err), "cudaMallocAsync(%zu): %s", bytes, cudaGetErrorString(e));
-    return STAN_CL_ENOMEM;
+// cached working matrix `slot` of at least `bytes` (grown with a sync, kept across
+// calls: re-mapping GBs of device memory per call costs 10-1000 ms)
+int ensure_mat(int slot, size_t bytes, double** p) {
+  if (g.mat_cap[slot] < bytes || !g.mat[slot]) {
+    if (g.mat[slot]) {
+      CK(cudaDeviceSynchronize());
+      CK(cudaFree(g.mat[slot]));
+      g.mat[slot] = nullptr;
+      g.mat_cap[slot] = 0;
+    }
+    cudaError_t e = cudaMalloc(&g.mat[slot], bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      g.mat[slot] = nullptr;
+      snprintf(g.last_err, sizeof(g.last_err), "matrix workspace cudaMalloc(%zu): %s", bytes, cudaGetErrorString(e));
+      return STAN_CL_ENOMEM;
+    }
+    g.mat_cap[slot] = bytes;
   }
+  *p = (double*)g.mat[slot];
   return STAN_CL_OK;
 }
+
 
 // ------------------------------------------------------------------ forward
 int ensure_side(size_t nevents) {
@@ -156,6 +175,36 @@ int ensure_side(size_t nevents) {
     CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     g.events.push_back(e);
   }
+  return STAN_CL_OK;
+}
+
+int ensure_copy(size_t nevents) {
+  if (!g.h2d) CK(cudaStreamCreateWithFlags(&g.h2d, cudaStreamNonBlocking));
+  if (!g.d2h) CK(cudaStreamCreateWithFlags(&g.d2h, cudaStreamNonBlocking));
+  while (g.xev.size() < nevents) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g.xev.push_back(e);
+  }
+  return STAN_CL_OK;
+}
+
+// host destination of a streamed result: the leading n x n block (row-major,
+// leading dimension n) receives the lower triangle (+0.0 above the diagonal
+// inside the 128 x 128 diagonal tiles; the rest of the strict upper untouched)
+struct HostOut {
+  double* host;
+  int64_t n;
+};
+
+// rows [r0, r1) x columns [c0, c1) of W (ld) -> host (ld n), on stream st
+int copy_rect_d2h(const HostOut& o, const double* W, int64_t ld, int64_t r0, int64_t r1, int64_t c0, int64_t c1,
+                  cudaStream_t st) {
+  r1 = std::min(r1, o.n);
+  c1 = std::min(c1, o.n);
+  if (r1 <= r0 || c1 <= c0) return STAN_CL_OK;
+  CK(cudaMemcpy2DAsync(o.host + r0 * o.n + c0, o.n * sizeof(double), W + r0 * ld + c0, ld * sizeof(double),
+                       (c1 - c0) * sizeof(double), r1 - r0, cudaMemcpyDeviceToHost, st));
   return STAN_CL_OK;
 }
 
@@ -186,7 +235,7 @@ int panel(double* W, int64_t ld, int64_t c0, int64_t N, int64_t OB, int* status,
 //   main: wait panel k; A[col block k+1] -= L21 L21(k+1)^T     (lookahead column)
 //   side: panel(k+1)                                          (L11 = chol(A11); L21 = A21 L11^-T)
 //   main: A22[k+2.., k+2..] -= L21 L21^T (lower tiles)         (multiply_transpose)
-int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status) {
+int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status, const HostOut* out = nullptr) {
   cudaStream_t main = g.stream;
   const int64_t T = N / OB;
   int rc = ensure_side(2 * T + 2);
@@ -199,6 +248,17 @@ int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status) {
   rc = panel(W, ld, 0, N, OB, status, side);
   if (rc) return rc;
   CK(cudaEventRecord(ev[1], side));
+  // streamed D2H: the rows of panel k are final once panel k is done
+  auto ship = [&](int64_t k) -> int {
+    if (!out) return STAN_CL_OK;
+    CK(cudaStreamWaitEvent(g.d2h, ev[1 + 2 * k], 0));
+    for (int64_t r0 = k * OB; r0 < (k + 1) * OB; r0 += NB) {  // lower rows + their diagonal tile
+      int rc2 = copy_rect_d2h(*out, W, ld, r0, r0 + NB, 0, r0 + NB, g.d2h);
+      if (rc2) return rc2;
+    }
+    return STAN_CL_OK;
+  };
+  if ((rc = ship(0))) return rc;
   for (int64_t k = 0; k < T; ++k) {
     CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
     if (k == T - 1) break;
@@ -211,6 +271,7 @@ int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status) {
     rc = panel(W, ld, r1, N, OB, status, side);
     if (rc) return rc;
     CK(cudaEventRecord(ev[1 + 2 * (k + 1)], side));
+    if ((rc = ship(k + 1))) return rc;
     if (r2 < N) {
       const double* L31 = W + r2 * ld + c0;
       CK(gemm_lower_nt((int)(N - r2), (int)OB, L31, ld, L31, ld, W + r2 * ld + r2, ld, status, main));
@@ -245,13 +306,12 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
     if (A == L) CK(zero_upper(L, n, n, st));
   } else {
     double* W = nullptr;
-    rc = alloc_async(&W, (size_t)N * N * sizeof(double));
+    rc = ensure_mat(0, (size_t)N * N * sizeof(double), &W);
     if (rc) return rc;
     CK(copy_lower_pad(A, n, n, W, N, N, 1.0, st));
     rc = factor_inplace(W, N, N, OB, status);
     if (rc) return rc;
     CK(copy_lower_out(W, N, L, n, n, st));
-    CK(cudaFreeAsync(W, st));
   }
   if (d_info) CK(cudaMemcpyAsync(d_info, status, sizeof(int), cudaMemcpyDeviceToDevice, st));
   return STAN_CL_OK;
@@ -260,8 +320,13 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
 // ------------------------------------------------------------------ adjoint
 // Blocked reverse sweep on the working matrix Wm (initially
 // tril(L_bar)) with factor Lw, both N x N with leading dimension ld.
+// rows_ready (optional): event per 128-row block, recorded when rows of that
+// block of Lw / Wm have arrived and its D^-1 is in the workspace (streamed H2D);
+// out (optional): column block j of the result is shipped to the host as soon as
+// it is final (after the step that Phi-s D_bar(j))
 int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* status,
-                    const AdjPlan& plan) {
+                    const AdjPlan& plan, const cudaEvent_t* rows_ready = nullptr,
+                    const HostOut* out = nullptr, const cudaEvent_t* col_done = nullptr) {
   cudaStream_t st = g.stream;
   char* base = (char*)g.ws + al(sizeof(int) * 64);
   double* Dinv = (double*)base;
@@ -272,10 +337,12 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
   double* T4 = T3 + NB * NB;
   const int nblk = (int)(N / NB);
   // D^-1 of every diagonal block depends only on L: one batched launch, off the
-  // critical path (lower_triangular_inverse(D))
-  CK(tri_inverse_batched(Lw, ld, nblk, Dinv, status, st));
+  // critical path (lower_triangular_inverse(D)); the streamed
+  // host path computes it per block as the rows arrive
+  if (!rows_ready) CK(tri_inverse_batched(Lw, ld, nblk, Dinv, status, st));
   for (int64_t k = N; k > 0; k -= NB) {
     const int64_t j = k - NB, m = N - k;
+    if (rows_ready) CK(cudaStreamWaitEvent(st, rows_ready[j / NB], 0));
     const double* D = Lw + j * ld + j;
     const double* Db = Dinv + (j / NB) * NB * NB;
     const double* R = Lw + j * ld;       // L(j:k, 0:j)
@@ -304,6 +371,12 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
     CK(phi_sym(T3, T4, Dbar, ld, status, st));
     // R_adj = R_adj - D_adj * R
     if (j > 0) CK(gemm_full(true, false, NB, (int)j, NB, -1.0, 1, T4, NB, R, ld, Wm + j * ld, ld, status, st));
+    if (out) {  // column block j is final: ship rows j.. of it
+      CK(cudaEventRecord(col_done[j / NB], st));
+      CK(cudaStreamWaitEvent(g.d2h, col_done[j / NB], 0));
+      int rc = copy_rect_d2h(*out, Wm, ld, j, N, j, k, g.d2h);
+      if (rc) return rc;
+    }
   }
   return STAN_CL_OK;
 }
@@ -334,17 +407,15 @@ int adjoint_enqueue(int64_t n, const double* L, const double* Lbar, double* Abar
     if (rc) return rc;
   } else {
     double *Lw = nullptr, *Wm = nullptr;
-    rc = alloc_async(&Lw, (size_t)N * N * sizeof(double));
+    rc = ensure_mat(0, (size_t)N * N * sizeof(double), &Lw);
     if (rc) return rc;
-    rc = alloc_async(&Wm, (size_t)N * N * sizeof(double));
+    rc = ensure_mat(1, (size_t)N * N * sizeof(double), &Wm);
     if (rc) return rc;
     CK(copy_lower_pad(L, n, n, Lw, N, N, 1.0, st));
     CK(copy_lower_pad(Lbar, n, n, Wm, N, N, 0.0, st));
     rc = adjoint_inplace(Lw, Wm, N, N, status, plan);
     if (rc) return rc;
     CK(copy_lower_out(Wm, N, Abar, n, n, st));
-    CK(cudaFreeAsync(Lw, st));
-    CK(cudaFreeAsync(Wm, st));
   }
   if (d_info) CK(cudaMemcpyAsync(d_info, status, sizeof(int), cudaMemcpyDeviceToDevice, st));
   return STAN_CL_OK;
@@ -394,19 +465,43 @@ int stan_cl_gp_exp_quad_cov(int64_t n, const double* x, double alpha, double rho
   return STAN_CL_OK;
 }
 
+// Host-buffer entry points: only the lower triangles cross PCIe (the paper's
+// packed transfers), as one rectangle per 128-row block
+// (rows r0..r1, columns 0..r1), and the transfers are streamed against the
+// compute: the forward ships each panel's rows as soon as that panel is
+// factored; the adjoint uploads row blocks bottom-up (the order the reverse
+// sweep consumes them) and ships each column block of A_bar as soon as it is
+// final.
 int stan_cl_cholesky_host(int64_t n, const double* A, double* L) {
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!A || !L) return STAN_CL_EINVAL;
-  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
-  double* dA = nullptr;
-  int rc = alloc_async(&dA, bytes);
+  int64_t OB = g.nb;
+  if (!OB) OB = (n % (2 * NB) == 0) ? 2 * NB : (n % NB == 0) ? NB : (n > 1024 ? 2 * NB : NB);
+  const int64_t N = round_up(n, OB);
+  int rc = ensure_ws(al(sizeof(int) * 64));
   if (rc) return rc;
-  CK(cudaMemcpyAsync(dA, A, bytes, cudaMemcpyHostToDevice, g.stream));
-  rc = cholesky_enqueue(n, dA, dA, nullptr);
+  if ((rc = ensure_copy(4))) return rc;
+  int* status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  double* W = nullptr;
+  if ((rc = ensure_mat(0, (size_t)N * N * sizeof(double), &W))) return rc;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  CK(init_pad(W, n, N, 1.0, st));
+  CK(cudaEventRecord(g.xev[0], st));
+  CK(cudaStreamWaitEvent(g.h2d, g.xev[0], 0));
+  for (int64_t r0 = 0; r0 < n; r0 += NB) {
+    const int64_t r1 = std::min(r0 + NB, n);
+    CK(cudaMemcpy2DAsync(W + r0 * N, N * sizeof(double), A + r0 * n, n * sizeof(double), r1 * sizeof(double),
+                         r1 - r0, cudaMemcpyHostToDevice, g.h2d));
+  }
+  CK(cudaEventRecord(g.xev[1], g.h2d));
+  CK(cudaStreamWaitEvent(st, g.xev[1], 0));
+  HostOut out{L, n};
+  rc = factor_inplace(W, N, N, OB, status, &out);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(L, dA, bytes, cudaMemcpyDeviceToHost, g.stream));
-  CK(cudaFreeAsync(dA, g.stream));
+  CK(cudaEventRecord(g.xev[2], g.d2h));
+  CK(cudaStreamWaitEvent(st, g.xev[2], 0));
   return read_status();
 }
 
@@ -414,19 +509,42 @@ int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_ba
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
-  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
-  double *dL = nullptr, *dB = nullptr;
-  int rc = alloc_async(&dL, bytes);
+  const AdjPlan plan = adj_plan(n);
+  const int64_t N = plan.N, nblk = N / NB;
+  int rc = ensure_ws(plan.total);
   if (rc) return rc;
-  rc = alloc_async(&dB, bytes);
+  if ((rc = ensure_copy(2 * nblk + 4))) return rc;
+  int* status = (int*)g.ws;
+  double* Dinv = (double*)((char*)g.ws + al(sizeof(int) * 64));
+  cudaStream_t st = g.stream;
+  double *Lw = nullptr, *Wm = nullptr;
+  if ((rc = ensure_mat(0, (size_t)N * N * sizeof(double), &Lw))) return rc;
+  if ((rc = ensure_mat(1, (size_t)N * N * sizeof(double), &Wm))) return rc;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  CK(init_pad(Lw, n, N, 1.0, st));
+  CK(init_pad(Wm, n, N, 0.0, st));
+  cudaEvent_t* ready = g.xev.data() + 2;
+  cudaEvent_t* col_done = ready + nblk;
+  CK(cudaEventRecord(g.xev[0], st));
+  CK(cudaStreamWaitEvent(g.h2d, g.xev[0], 0));
+  for (int64_t b = nblk - 1; b >= 0; --b) {  // bottom-up: the order the reverse sweep needs
+    const int64_t r0 = b * NB, r1 = std::min(r0 + NB, n);
+    if (r0 < n) {
+      CK(cudaMemcpy2DAsync(Lw + r0 * N, N * sizeof(double), L + r0 * n, n * sizeof(double), r1 * sizeof(double),
+                           r1 - r0, cudaMemcpyHostToDevice, g.h2d));
+      CK(cudaMemcpy2DAsync(Wm + r0 * N, N * sizeof(double), L_bar + r0 * n, n * sizeof(double),
+                           r1 * sizeof(double), r1 - r0, cudaMemcpyHostToDevice, g.h2d));
+      CK(zero_tile_upper(Wm, N, r0, (int)(r1 - r0), g.h2d));  // only the lower triangle of L_bar is read
+      CK(check_diag(Lw + r0 * N + r0, r1 - r0, N, status, g.h2d, r0));
+    }
+    CK(tri_inverse_batched(Lw + r0 * N + r0, N, 1, Dinv + b * NB * NB, status, g.h2d));
+    CK(cudaEventRecord(ready[b], g.h2d));
+  }
+  HostOut out{A_bar, n};
+  rc = adjoint_inplace(Lw, Wm, N, N, status, plan, ready, &out, col_done);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(dL, L, bytes, cudaMemcpyHostToDevice, g.stream));
-  CK(cudaMemcpyAsync(dB, L_bar, bytes, cudaMemcpyHostToDevice, g.stream));
-  rc = adjoint_enqueue(n, dL, dB, dB, nullptr);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(A_bar, dB, bytes, cudaMemcpyDeviceToHost, g.stream));
-  CK(cudaFreeAsync(dL, g.stream));
-  CK(cudaFreeAsync(dB, g.stream));
+  CK(cudaEventRecord(g.xev[1], g.d2h));
+  CK(cudaStreamWaitEvent(st, g.xev[1], 0));
   return read_status();
 }
 
@@ -504,6 +622,21 @@ int stan_cl_finalize(void) {
   }
   for (cudaEvent_t e : g.events) cudaEventDestroy(e);
   g.events.clear();
+  for (cudaEvent_t e : g.xev) cudaEventDestroy(e);
+  g.xev.clear();
+  for (int i = 0; i < 2; ++i) {
+    if (g.mat[i]) cudaFree(g.mat[i]);
+    g.mat[i] = nullptr;
+    g.mat_cap[i] = 0;
+  }
+  if (g.h2d) {
+    cudaStreamDestroy(g.h2d);
+    g.h2d = nullptr;
+  }
+  if (g.d2h) {
+    cudaStreamDestroy(g.d2h);
+    g.d2h = nullptr;
+  }
   if (g.side) {
     cudaStreamDestroy(g.side);
     g.side = nullptr;

@@ -186,6 +186,38 @@ __global__ void zero_upper_kernel(double* A, int64_t n, int64_t ld) {
   }
 }
 
+// +0.0 into the strict upper triangle of the rows x rows diagonal tile at (r0, r0)
+__global__ void zero_tile_upper_kernel(double* A, int64_t ld, int64_t r0, int rows) {
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < rows * rows; idx += gridDim.x * blockDim.x) {
+    const int i = idx / rows, j = idx - i * rows;
+    if (j > i) A[(r0 + i) * ld + r0 + j] = 0.0;
+  }
+}
+
+cudaError_t zero_tile_upper(double* A, int64_t ld, int64_t r0, int rows, cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st, 4.0 * rows * rows);
+  zero_tile_upper_kernel<<<16, 256, 0, st>>>(A, ld, r0, rows);
+  return cudaGetLastError();
+}
+
+// padding of an N x N working matrix around its leading n x n block: rows >= n
+// and columns >= n become diag_pad * I (the leading block is left untouched)
+__global__ void init_pad_kernel(double* W, int64_t n, int64_t N, double diag_pad) {
+  const long long total = (long long)N * N;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx / N, j = idx - i * N;
+    if (i >= n || j >= n) W[idx] = (i == j) ? diag_pad : 0.0;
+  }
+}
+
+cudaError_t init_pad(double* W, int64_t n, int64_t N, double diag_pad, cudaStream_t st) {
+  if (N == n) return cudaSuccess;
+  Prof prof_(PROF_MISC, 0.0, st, 8.0 * ((double)N * N - (double)n * n));
+  init_pad_kernel<<<grid_for((long long)N * N, 256), 256, 0, st>>>(W, n, N, diag_pad);
+  return cudaGetLastError();
+}
+
 cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st) {
   Prof prof_(PROF_MISC, 0.0, st, 4.0 * n * n);
   if (n == 0) return cudaSuccess;
@@ -274,7 +306,7 @@ __global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t l
 #pragma unroll
     for (int b = 0; b < 8; ++b) {
       const int r = ti + 16 * a, c = tj + 16 * b;
-      if (c <= r) base[(long long)r * ld + c] = T[a][b];
+      base[(long long)r * ld + c] = (c <= r) ? T[a][b] : 0.0;  // strict upper of the tile: +0.0
     }
   if (tid == 0 && fail_j >= 0) atomicCAS(status, 0, (int)(k0 + fail_j + 1));
 }
@@ -655,12 +687,12 @@ cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, co
   return cudaGetLastError();
 }
 
-__global__ void check_diag_kernel(const double* L, int64_t n, int64_t ld, int* status) {
+__global__ void check_diag_kernel(const double* L, int64_t n, int64_t ld, int64_t base, int* status) {
   for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < n;
        k += (long long)gridDim.x * blockDim.x) {
     const double d = L[k * ld + k];
     if (!(d > 0.0) || !isfinite(d)) {
-      const int v = (int)(k + 1);
+      const int v = (int)(base + k + 1);
       int old = *(volatile int*)status;
       while (old == 0 || v < old) {
         const int prev = atomicCAS(status, old, v);
@@ -671,10 +703,10 @@ __global__ void check_diag_kernel(const double* L, int64_t n, int64_t ld, int* s
   }
 }
 
-cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st) {
+cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st, int64_t base) {
   Prof prof_(PROF_MISC, 0.0, st, 8.0 * n);
   if (n == 0) return cudaSuccess;
-  check_diag_kernel<<<grid_for(n, 256, 148), 256, 0, st>>>(L, n, ld, status);
+  check_diag_kernel<<<grid_for(n, 256, 148), 256, 0, st>>>(L, n, ld, base, status);
   return cudaGetLastError();
 }
 

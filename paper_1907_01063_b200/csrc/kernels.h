@@ -52,6 +52,10 @@ cudaError_t copy_lower_out(const double* src, int64_t lds, double* dst, int64_t 
                            cudaStream_t st);
 // zero the strict upper triangle in place
 cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st);
+// zero the strict upper of the rows x rows diagonal tile at (r0, r0)
+cudaError_t zero_tile_upper(double* A, int64_t ld, int64_t r0, int rows, cudaStream_t st);
+// rows >= n and columns >= n of the N x N matrix W become diag_pad * I
+cudaError_t init_pad(double* W, int64_t n, int64_t N, double diag_pad, cudaStream_t st);
 
 // ---- F1/F2: diagonal tile POTRF (K2) and panel TRSM (K3), NB = 128 ----
 // factor W[k0:k0+128, k0:k0+128] in place (lower); on failure status = k0 + j + 1
@@ -92,7 +96,7 @@ cudaError_t gemm128(bool a_t, bool a_tril, bool b_t, bool b_sym, const double* A
 // S (128x128, ld 128): Ssym = mirror(tril(S)) -> ws; Dbar = Phi(S) = tril(S) with halved diagonal
 cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, const int* status,
                     cudaStream_t st);
-// status = first k+1 with !(L[k][k] > 0 && finite), k < n
-cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st);
+// status = first base+k+1 with !(L[k][k] > 0 && finite), k < n
+cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st, int64_t base = 0);
 
 }  // namespace stancl

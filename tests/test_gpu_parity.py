@@ -241,18 +241,48 @@ def test_adjoint_zero_seed(sc):
 
 
 # ----------------------------------------------------------- host-buffer API
-def test_host_entry_points(sc):
-    n = 640
+def _check_host_output(out, want, tol, n):
+    lo = np.tril_indices(n)
+    assert relf(out[lo], want[lo]) <= tol
+    # +0.0 above the diagonal inside the 128 x 128 diagonal tiles; the rest of the
+    # strict upper triangle is not written (the sentinel survives)
+    i, j = np.triu_indices(n, 1)
+    in_tile = (i // 128) == (j // 128)
+    assert np.all(out[i[in_tile], j[in_tile]] == 0.0)
+    assert np.all(out[i[~in_tile], j[~in_tile]] == 7.0)
+
+
+@pytest.mark.parametrize("n", [100, 300, 640, 1024, 2048])
+def test_host_entry_points(sc, n):
+    # packed (lower-triangle) streamed transfers through the host-buffer C ABI
     K = se(n)
-    A = torch.from_numpy(K.copy()).pin_memory()
-    L = torch.empty_like(A).pin_memory()
+    G = K.copy()
+    G[np.triu_indices(n, 1)] = np.nan                       # upper of the host input is ignored
+    A = torch.from_numpy(G).pin_memory()
+    L = torch.full((n, n), 7.0, dtype=torch.float64).pin_memory()
     assert sc.cholesky_host(A, L) == 0
-    assert relf(L.numpy(), oracle.cholesky(K)) <= L_BAR_TOL
     Lo = oracle.cholesky(K)
+    _check_host_output(L.numpy(), Lo, L_BAR_TOL, n)
     W = inputs.lbar(n)
-    Ab = torch.empty((n, n), dtype=torch.float64).pin_memory()
-    assert sc.cholesky_adjoint_host(torch.from_numpy(Lo), torch.from_numpy(W), Ab) == 0
-    assert relf(Ab.numpy(), oracle.cholesky_adjoint(Lo, W)) <= A_BAR_TOL
+    Wg = W.copy()
+    Wg[np.triu_indices(n, 1)] = np.nan
+    Lg = Lo.copy()
+    Lg[np.triu_indices(n, 1)] = np.nan
+    Ab = torch.full((n, n), 7.0, dtype=torch.float64).pin_memory()
+    assert sc.cholesky_adjoint_host(torch.from_numpy(Lg), torch.from_numpy(Wg), Ab) == 0
+    _check_host_output(Ab.numpy(), oracle.cholesky_adjoint(Lo, W), A_BAR_TOL, n)
+
+
+def test_host_entry_points_errors(sc):
+    n = 400
+    A = inputs.toeplitz(n)
+    A[250, 250] = -1e12
+    L = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    assert sc.cholesky_host(torch.from_numpy(A).pin_memory(), L) == 251
+    Lb = np.eye(n)
+    Lb[333, 333] = 0.0
+    out = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    assert sc.cholesky_adjoint_host(torch.from_numpy(Lb), torch.from_numpy(np.eye(n)), out) == 334
 
 
 def test_kernel_launch_counter(sc):
