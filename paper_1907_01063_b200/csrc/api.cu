@@ -68,7 +68,7 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 struct AdjPlan {
   int64_t N;
-  size_t dinv, part, tmp, total;
+  size_t dinv, part, tmp, ctmp, total;
 };
 
 // split-K factor for W = C_bar^T L[k:N, 0:k] (persistent TMA GEMM, 128 x 64
@@ -111,7 +111,8 @@ AdjPlan adj_plan(int64_t n) {
   }
   p.part = al(part);
   p.tmp = al(4 * NB * NB * sizeof(double));
-  p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp;
+  p.ctmp = al((size_t)p.N * NB * sizeof(double));
+  p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp + p.ctmp;
   return p;
 }
 
@@ -220,7 +221,7 @@ int panel(double* W, int64_t ld, int64_t c0, int64_t N, int64_t OB, int* status,
     const int64_t h = c0 + NB;
     const double* L21 = W + h * ld + c0;
     CK(gemm_full(true, true, (int)(N - h), NB, NB, -1.0, 1, L21, ld, L21, ld, W + h * ld + h, ld, status, st,
-                 /*lower_only=*/1, PROF_LOOKAHEAD));
+                 /*lower_only=*/1, PROF_LOOKAHEAD, /*allow_persistent=*/false));
     CK(potrf_tile(W, ld, h, status, st));
     if (h + NB < N) CK(trsm_panel(W, ld, h, h + NB, N, status, st));
   }
@@ -335,6 +336,7 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
   double* T2 = T1 + NB * NB;
   double* T3 = T2 + NB * NB;
   double* T4 = T3 + NB * NB;
+  double* Ctmp = (double*)(base + plan.dinv + plan.part + plan.tmp);  // C_bar D^-1, m x 128
   const int nblk = (int)(N / NB);
   // D^-1 of every diagonal block depends only on L: one batched launch, off the
   // critical path (lower_triangular_inverse(D)); the streamed
@@ -350,16 +352,19 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
     double* Dbar = Wm + j * ld + j;      // D_adj
     if (m > 0) {
       // C_adj = C_adj * lower_triangular_inverse(D)
-      CK(gemm_full(true, false, (int)m, NB, NB, 1.0, 0, Cb, ld, Db, NB, Cb, ld, status, st, 0, PROF_TRMM));
+      // computed out of place (persistent TMA GEMM) into Ctmp, consumed from there
+      // by the two big products, and written back to A_bar afterwards
+      CK(gemm_full(true, false, (int)m, NB, NB, 1.0, 0, Cb, ld, Db, NB, Ctmp, NB, status, st, 0, PROF_TRMM));
       // B_adj = B_adj - C_adj * R
       if (j > 0)
-        CK(gemm_full(true, false, (int)m, (int)j, NB, -1.0, 1, Cb, ld, R, ld, Wm + k * ld, ld, status, st));
+        CK(gemm_full(true, false, (int)m, (int)j, NB, -1.0, 1, Ctmp, NB, R, ld, Wm + k * ld, ld, status, st));
       // [R_adj D_adj] -= C_adj^T [B C]   (PAPER.md:311 and the C_adj^T B term of 319),
       // split-K over the m rows with a fixed-order reduction
       int splits, kps;
       splitk_choice(m, k, &splits, &kps);
-      CK(gemm_splitk_tn(NB, (int)k, (int)m, splits, kps, Cb, ld, Lw + k * ld, ld, Pbuf, status, st));
+      CK(gemm_splitk_tn(NB, (int)k, (int)m, splits, kps, Ctmp, NB, Lw + k * ld, ld, Pbuf, status, st));
       CK(splitk_reduce_sub(Pbuf, splits, NB, (int)k, Wm + j * ld, ld, status, st));
+      CK(copy_block(Ctmp, NB, Cb, ld, m, NB, st));
     }
     // D_adj = transpose(D) * D_adj; copy_lower_tri_to_upper_tri
     CK(gemm128(true, true, false, false, D, ld, Dbar, ld, T1, NB, status, st));

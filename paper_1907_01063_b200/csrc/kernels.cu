@@ -218,6 +218,25 @@ cudaError_t init_pad(double* W, int64_t n, int64_t N, double diag_pad, cudaStrea
   return cudaGetLastError();
 }
 
+// dst[rows x cols] (ldd) <- src (lds); cols even, 16-B aligned rows
+__global__ void copy_block_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
+                                  int64_t ldd, int64_t rows, int64_t cols) {
+  const long long half = rows * cols / 2;
+  for (long long h = blockIdx.x * (long long)blockDim.x + threadIdx.x; h < half;
+       h += (long long)gridDim.x * blockDim.x) {
+    const long long e = 2 * h, r = e / cols, c = e - r * cols;
+    *reinterpret_cast<double2*>(dst + r * ldd + c) = *reinterpret_cast<const double2*>(src + r * lds + c);
+  }
+}
+
+cudaError_t copy_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+                       cudaStream_t st) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  Prof prof_(PROF_MISC, 0.0, st, 16.0 * rows * cols);
+  copy_block_kernel<<<grid_for(rows * cols / 2, 256), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
+  return cudaGetLastError();
+}
+
 cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st) {
   Prof prof_(PROF_MISC, 0.0, st, 4.0 * n * n);
   if (n == 0) return cudaSuccess;
@@ -446,7 +465,8 @@ cudaError_t gemm_full_cfg(bool a_kmaj, bool b_kmaj, const GemmArgs& p, cudaStrea
 
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-                      int64_t ldc, const int* status, cudaStream_t st, int lower_only, int prof_kind) {
+                      int64_t ldc, const int* status, cudaStream_t st, int lower_only, int prof_kind,
+                      bool allow_persistent) {
   if (M == 0 || N == 0) return cudaSuccess;
   Prof prof_(prof_kind, 2.0 * M * N * K, st, (beta ? 16.0 : 8.0) * M * N + 8.0 * ((double)M * K + (double)N * K));
   GemmArgs p{A, lda, B, ldb, C, ldc, M, N, K, K, sign, beta, lower_only, status, cfgsel().pingpong};
@@ -457,7 +477,7 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
     if (N != gemm::CfgBig::BN) return cudaErrorInvalidValue;
     return gemm_full_cfg<gemm::CfgBig>(a_kmaj, b_kmaj, p, st);
   }
-  if (cfgsel().tma_gemm) return gemm_full_persist(a_kmaj, b_kmaj, p, st);
+  if (cfgsel().tma_gemm && allow_persistent) return gemm_full_persist(a_kmaj, b_kmaj, p, st);
   switch (cfgsel().gemm) {
     case CFG_BIG: return gemm_full_cfg<gemm::CfgBig>(a_kmaj, b_kmaj, p, st);
     case CFG_W8: return gemm_full_cfg<gemm::CfgW8>(a_kmaj, b_kmaj, p, st);
@@ -583,8 +603,10 @@ cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* D
 constexpr int G128_AP = NB + 4, G128_BP = 32 + 4;
 constexpr int G128_SMEM = (32 * G128_AP + NB * G128_BP) * (int)sizeof(double);
 
-__global__ void __launch_bounds__(128) gemm128_kernel(bool a_t, bool a_tril, bool b_t, bool b_sym,
-                                                      const double* __restrict__ A, int64_t lda,
+// All 64 global loads of a thread are issued before any is used (fully unrolled,
+// compile-time layout flags), so the slice staging costs one L2 latency, not 64.
+template <bool A_T, bool A_TRIL, bool B_T, bool B_SYM>
+__global__ void __launch_bounds__(128) gemm128_kernel(const double* __restrict__ A, int64_t lda,
                                                       const double* __restrict__ B, int64_t ldb,
                                                       double* __restrict__ C, int64_t ldc,
                                                       const int* status) {
@@ -594,38 +616,35 @@ __global__ void __launch_bounds__(128) gemm128_kernel(bool a_t, bool a_tril, boo
   double* Bs = sm + 32 * G128_AP;  // [128][G128_BP]  Bs[k][n]
   const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
   const int tid = threadIdx.x;
-  for (int idx = tid; idx < 32 * NB; idx += 128) {
-    int m, k;
-    double v;
-    if (a_t) {
-      k = idx >> 5;
-      m = idx & 31;
-      v = (a_tril && m0 + m > k) ? 0.0 : A[(long long)k * lda + m0 + m];
+  double va[32], vb[32];
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const int idx = tid + q * 128;
+    if (A_T) {
+      const int k = idx >> 5, m = idx & 31;
+      va[q] = (A_TRIL && m0 + m > k) ? 0.0 : __ldg(A + (long long)k * lda + m0 + m);
     } else {
-      m = idx >> 7;
-      k = idx & (NB - 1);
-      v = (a_tril && k > m0 + m) ? 0.0 : A[(long long)(m0 + m) * lda + k];
+      const int m = idx >> 7, k = idx & (NB - 1);
+      va[q] = (A_TRIL && k > m0 + m) ? 0.0 : __ldg(A + (long long)(m0 + m) * lda + k);
     }
-    As[m * G128_AP + k] = v;
+    if (B_SYM) {
+      const int k = idx >> 5, gn = n0 + (idx & 31);
+      vb[q] = (k >= gn) ? __ldg(B + (long long)k * ldb + gn) : __ldg(B + (long long)gn * ldb + k);
+    } else if (B_T) {
+      const int n = idx >> 7, k = idx & (NB - 1);
+      vb[q] = __ldg(B + (long long)(n0 + n) * ldb + k);
+    } else {
+      const int k = idx >> 5, n = idx & 31;
+      vb[q] = __ldg(B + (long long)k * ldb + n0 + n);
+    }
   }
-  for (int idx = tid; idx < 32 * NB; idx += 128) {
-    int k, n;
-    double v;
-    if (b_sym) {
-      k = idx >> 5;
-      n = idx & 31;
-      const int gn = n0 + n;
-      v = (k >= gn) ? B[(long long)k * ldb + gn] : B[(long long)gn * ldb + k];
-    } else if (b_t) {
-      n = idx >> 7;
-      k = idx & (NB - 1);
-      v = B[(long long)(n0 + n) * ldb + k];
-    } else {
-      k = idx >> 5;
-      n = idx & 31;
-      v = B[(long long)k * ldb + n0 + n];
-    }
-    Bs[k * G128_BP + n] = v;
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const int idx = tid + q * 128;
+    if (A_T) As[(idx & 31) * G128_AP + (idx >> 5)] = va[q];
+    else As[(idx >> 7) * G128_AP + (idx & (NB - 1))] = va[q];
+    if (B_T && !B_SYM) Bs[(idx & (NB - 1)) * G128_BP + (idx >> 7)] = vb[q];
+    else Bs[(idx >> 5) * G128_BP + (idx & 31)] = vb[q];
   }
   __syncthreads();
   const int lane = tid & 31, warp = tid >> 5;
@@ -648,24 +667,33 @@ __global__ void __launch_bounds__(128) gemm128_kernel(bool a_t, bool a_tril, boo
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int r = m0 + wm * 16 + i * 8 + g, c = n0 + wn * 16 + j * 8 + 2 * t;
-      C[(long long)r * ldc + c] = acc[i][j][0];
-      C[(long long)r * ldc + c + 1] = acc[i][j][1];
+      *reinterpret_cast<double2*>(C + (long long)r * ldc + c) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
+}
+
+template <bool A_T, bool A_TRIL, bool B_T, bool B_SYM>
+static cudaError_t gemm128_launch(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
+                                  int64_t ldc, const int* status, cudaStream_t st) {
+  auto kern = gemm128_kernel<A_T, A_TRIL, B_T, B_SYM>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G128_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  kern<<<dim3(4, 4), 128, G128_SMEM, st>>>(A, lda, B, ldb, C, ldc, status);
+  return cudaGetLastError();
 }
 
 cudaError_t gemm128(bool a_t, bool a_tril, bool b_t, bool b_sym, const double* A, int64_t lda,
                     const double* B, int64_t ldb, double* C, int64_t ldc, const int* status,
                     cudaStream_t st) {
   Prof prof_(PROF_SMALL, 2.0 * NB * NB * NB, st, 24.0 * NB * NB);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(gemm128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         G128_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  gemm128_kernel<<<dim3(4, 4), 128, G128_SMEM, st>>>(a_t, a_tril, b_t, b_sym, A, lda, B, ldb, C, ldc, status);
-  return cudaGetLastError();
+  // the three products of the symbolic diagonal step (api.cu) -- and only those
+  if (a_t && a_tril && !b_t && !b_sym) return gemm128_launch<true, true, false, false>(A, lda, B, ldb, C, ldc, status, st);
+  if (a_t && !a_tril && !b_t && b_sym) return gemm128_launch<true, false, false, true>(A, lda, B, ldb, C, ldc, status, st);
+  if (!a_t && !a_tril && !b_t && !b_sym) return gemm128_launch<false, false, false, false>(A, lda, B, ldb, C, ldc, status, st);
+  return cudaErrorInvalidValue;
 }
 
 // S -> Ssym = mirror(tril S) and D_bar = Phi(S)

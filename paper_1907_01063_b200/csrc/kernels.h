@@ -50,6 +50,9 @@ cudaError_t copy_lower_pad(const double* src, int64_t n, int64_t lds, double* ds
 // dst[n x n] (ldd) <- lower(src) (lds), strict upper written +0.0
 cudaError_t copy_lower_out(const double* src, int64_t lds, double* dst, int64_t n, int64_t ldd,
                            cudaStream_t st);
+// dst[rows x cols] (ldd) <- src[rows x cols] (lds); cols even, 16-B aligned rows
+cudaError_t copy_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+                       cudaStream_t st);
 // zero the strict upper triangle in place
 cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st);
 // zero the strict upper of the rows x rows diagonal tile at (r0, r0)
@@ -67,11 +70,13 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
 // ---- DMMA GEMM family (F3, R1, R2, R3, R5) ----
 // C[M x N] = beta*C + sign * op(A) op(B)   (see gemm_dmma.cuh)
 //   a_kmaj: A is M x K row-major (else K x M);  b_kmaj: B is N x K (else K x N)
-// lower_only: store only r >= c (relative to C); prof_kind: profiling class
+// lower_only: store only r >= c (relative to C); prof_kind: profiling class;
+// allow_persistent = false keeps the one-tile-per-CTA kernel (for work issued on
+// the lookahead side stream, which must not hold SMs the trailing update needs)
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st, int lower_only = 0,
-                      int prof_kind = 1);
+                      int prof_kind = 1, bool allow_persistent = true);
 // lower tiles of square C[M x M] -= A A'^T style: C -= A B^T, A, B both k-major (SYRK)
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                           double* C, int64_t ldc, const int* status, cudaStream_t st);
