@@ -47,6 +47,7 @@ SIGNATURES = {
     "stan_cl_get_stream": (_P, []),
     "stan_cl_set_block_size": (_I, [_I]),
     "stan_cl_get_block_size": (_I, []),
+    "stan_cl_set_adjoint_block_size": (_I, [_I]),
     "stan_cl_workspace_bytes": (ctypes.c_size_t, [_I64]),
     "stan_cl_status_string": (ctypes.c_char_p, [_I]),
     "stan_cl_kernel_launches": (ctypes.c_longlong, []),

@@ -34,7 +34,8 @@ struct State {
   std::vector<cudaEvent_t> xev;  // per-block events of the streamed host transfers
   void* mat[2] = {nullptr, nullptr};  // cached N x N working matrices (padded / host paths)
   size_t mat_cap[2] = {0, 0};
-  int nb = 0;  // forward outer block: 0 = auto, 128 or 256
+  int nb = 0;      // forward outer block: 0 = auto, 128 or 256
+  int adj_nb = 0;  // adjoint block: 0 = auto, 128 or 256
   void* ws = nullptr;  // library-owned persistent workspace
   size_t ws_cap = 0;
   int* h_status = nullptr;  // pinned host word for the synchronous calls
@@ -67,15 +68,16 @@ constexpr size_t kAlign = 256;
 inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 
 struct AdjPlan {
-  int64_t N;
+  int64_t N;    // padded order (multiple of B)
+  int64_t B;    // adjoint block size: 128 or 256
   size_t dinv, part, tmp, ctmp, total;
 };
 
-// split-K factor for W = C_bar^T L[k:N, 0:k] (persistent TMA GEMM, 128 x 64
-// output tiles, 32-deep slabs): minimise rounds-of-148 x per-item K (+ a fixed
-// per-item cost) plus the reduction's extra reads
-void splitk_choice(int64_t m, int64_t k, int* splits_out, int* kps_out) {
-  const int ntiles = (int)(k / 64);
+// split-K factor for W = C_bar^T L[k:N, 0:k] (M = B rows; persistent TMA GEMM,
+// 128 x 64 output tiles, 32-deep slabs): minimise rounds-of-148 x per-item K
+// (+ a fixed per-item cost) plus the reduction's extra reads
+void splitk_choice(int64_t m, int64_t k, int64_t B, int* splits_out, int* kps_out) {
+  const int ntiles = (int)((B / 128) * (k / 64));
   const int kmax = (int)(m / 32);
   double best = 1e300;
   int bs = 1;
@@ -84,7 +86,7 @@ void splitk_choice(int64_t m, int64_t k, int* splits_out, int* kps_out) {
     const int eff_s = (int)((m + kps - 1) / kps);
     const int64_t items = (int64_t)ntiles * eff_s;
     const int64_t rounds = (items + 147) / 148;
-    const double t = (double)rounds * (double)(kps + 96) + 3.0 * eff_s * 64 * (double)k / (148.0 * 64);
+    const double t = (double)rounds * (double)(kps + 96) + 3.0 * eff_s * 64 * (double)k * (B / 128) / (148.0 * 64);
     if (t < best - 1e-9) {
       best = t;
       bs = s;
@@ -95,23 +97,29 @@ void splitk_choice(int64_t m, int64_t k, int* splits_out, int* kps_out) {
   *splits_out = (int)((m + kps - 1) / kps);
 }
 
+// adjoint block: 256 (fewer, longer-K steps) for large problems, else 128
+int64_t adj_block(int64_t n) {
+  if (g.adj_nb) return g.adj_nb;
+  return n >= 4096 ? 2 * NB : NB;
+}
+
 AdjPlan adj_plan(int64_t n) {
   AdjPlan p{};
-  p.N = round_up(n, NB);
-  const int64_t nblk = p.N / NB;
-  p.dinv = al((size_t)nblk * NB * NB * sizeof(double));
+  p.B = adj_block(n);
+  p.N = round_up(n, p.B);
+  p.dinv = al((size_t)p.N * p.B * sizeof(double));  // N/B blocks of B x B
   size_t part = 0;
-  for (int64_t k = p.N; k > 0; k -= NB) {
+  for (int64_t k = p.N; k > 0; k -= p.B) {
     const int64_t m = p.N - k;
     if (m == 0) continue;
     int s, kps;
-    splitk_choice(m, k, &s, &kps);
-    const size_t b = (size_t)s * NB * (size_t)k * sizeof(double);
+    splitk_choice(m, k, p.B, &s, &kps);
+    const size_t b = (size_t)s * p.B * (size_t)k * sizeof(double);
     if (b > part) part = b;
   }
   p.part = al(part);
-  p.tmp = al(4 * NB * NB * sizeof(double));
-  p.ctmp = al((size_t)p.N * NB * sizeof(double));
+  p.tmp = al(4 * (size_t)p.B * p.B * sizeof(double));
+  p.ctmp = al((size_t)p.N * p.B * sizeof(double));
   p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp + p.ctmp;
   return p;
 }
@@ -321,32 +329,64 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
 // ------------------------------------------------------------------ adjoint
 // Blocked reverse sweep on the working matrix Wm (initially
 // tril(L_bar)) with factor Lw, both N x N with leading dimension ld.
-// rows_ready (optional): event per 128-row block, recorded when rows of that
-// block of Lw / Wm have arrived and its D^-1 is in the workspace (streamed H2D);
-// out (optional): column block j of the result is shipped to the host as soon as
-// it is final (after the step that Phi-s D_bar(j))
+// D^-1 of the B x B diagonal blocks of Lw (B = 128 or 256): the 128 x 128
+// inverses by substitution (tri_inverse_batched); for B = 256 the off-diagonal
+// block of [[D11, 0], [D21, D22]]^-1 is -D22^-1 D21 D11^-1 (two batched 128^3
+// products).  Blocks [b0, b0 + nb) of size B; Dinv holds N/B blocks of B x B.
+int block_inverses(const double* Lw, int64_t ld, int64_t B, int64_t b0, int64_t nb, double* Dinv, double* scratch,
+                   int* status, cudaStream_t st) {
+  const double* Lb = Lw + b0 * B * ld + b0 * B;
+  double* Db = Dinv + b0 * B * B;
+  if (B == NB) {
+    CK(tri_inverse_batched(Lb, ld, (int)nb, Db, status, st));
+    return STAN_CL_OK;
+  }
+  // B = 256: the 2*nb diagonal 128-inverses straight into the 256 layout, then
+  // T = D21 X11 and X21 = -X22 T, both batched over the nb blocks
+  CK(cudaMemsetAsync(Db, 0, (size_t)nb * B * B * sizeof(double), st));
+  CK(tri_inverse_batched(Lb, ld, (int)(2 * nb), Db, status, st, B, B * B, 2));
+  const double* D21 = Lb + NB * ld;  // rows 128.., cols 0..128 of the first block
+  CK(gemm_small(NB, false, false, false, D21, ld, Db, B, scratch, NB, status, st, 1.0, (int)nb,
+                B * ld + B, B * B, (int64_t)NB * NB));
+  CK(gemm_small(NB, false, false, false, Db + NB * B + NB, B, scratch, NB, Db + NB * B, B, status, st, -1.0,
+                (int)nb, B * B, (int64_t)NB * NB, B * B));
+  return STAN_CL_OK;
+}
+
+// Blocked reverse sweep with block B = plan.B on the working
+// matrix Wm (initially tril(L_bar)) with factor Lw, both N x N with leading
+// dimension ld.
+// rows_ready (optional): event per 128-row block, recorded when the rows of that
+// block of Lw / Wm have arrived and the D^-1 covering it is in the workspace
+// (streamed H2D); out (optional): column block j of the result is shipped to the
+// host as soon as it is final (after the step that Phi-s D_bar(j)).
 int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* status,
                     const AdjPlan& plan, const cudaEvent_t* rows_ready = nullptr,
                     const HostOut* out = nullptr, const cudaEvent_t* col_done = nullptr) {
   cudaStream_t st = g.stream;
+  const int64_t B = plan.B;
   char* base = (char*)g.ws + al(sizeof(int) * 64);
   double* Dinv = (double*)base;
   double* Pbuf = (double*)(base + plan.dinv);
   double* T1 = (double*)(base + plan.dinv + plan.part);
-  double* T2 = T1 + NB * NB;
-  double* T3 = T2 + NB * NB;
-  double* T4 = T3 + NB * NB;
-  double* Ctmp = (double*)(base + plan.dinv + plan.part + plan.tmp);  // C_bar D^-1, m x 128
-  const int nblk = (int)(N / NB);
-  // D^-1 of every diagonal block depends only on L: one batched launch, off the
+  double* T2 = T1 + B * B;
+  double* T3 = T2 + B * B;
+  double* T4 = T3 + B * B;
+  double* Ctmp = (double*)(base + plan.dinv + plan.part + plan.tmp);  // C_bar D^-1, m x B
+  const int64_t nblk = N / B;
+  // D^-1 of every diagonal block depends only on L: computed up front, off the
   // critical path (lower_triangular_inverse(D)); the streamed
-  // host path computes it per block as the rows arrive
-  if (!rows_ready) CK(tri_inverse_batched(Lw, ld, nblk, Dinv, status, st));
-  for (int64_t k = N; k > 0; k -= NB) {
-    const int64_t j = k - NB, m = N - k;
-    if (rows_ready) CK(cudaStreamWaitEvent(st, rows_ready[j / NB], 0));
+  // host path computes it per block as the rows arrive.  Pbuf is free here.
+  if (!rows_ready) {
+    int rc = block_inverses(Lw, ld, B, 0, nblk, Dinv, Pbuf, status, st);
+    if (rc) return rc;
+  }
+  for (int64_t k = N; k > 0; k -= B) {
+    const int64_t j = k - B, m = N - k;
+    if (rows_ready)
+      for (int64_t r = j; r < k; r += NB) CK(cudaStreamWaitEvent(st, rows_ready[r / NB], 0));
     const double* D = Lw + j * ld + j;
-    const double* Db = Dinv + (j / NB) * NB * NB;
+    const double* Db = Dinv + (j / B) * B * B;
     const double* R = Lw + j * ld;       // L(j:k, 0:j)
     double* Cb = Wm + k * ld + j;        // C_adj = L_adj(k:N, j:k)
     double* Dbar = Wm + j * ld + j;      // D_adj
@@ -354,31 +394,32 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
       // C_adj = C_adj * lower_triangular_inverse(D)
       // computed out of place (persistent TMA GEMM) into Ctmp, consumed from there
       // by the two big products, and written back to A_bar afterwards
-      CK(gemm_full(true, false, (int)m, NB, NB, 1.0, 0, Cb, ld, Db, NB, Ctmp, NB, status, st, 0, PROF_TRMM));
+      CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, Ctmp, B, status, st, 0, PROF_TRMM));
       // B_adj = B_adj - C_adj * R
       if (j > 0)
-        CK(gemm_full(true, false, (int)m, (int)j, NB, -1.0, 1, Ctmp, NB, R, ld, Wm + k * ld, ld, status, st));
+        CK(gemm_full(true, false, (int)m, (int)j, (int)B, -1.0, 1, Ctmp, B, R, ld, Wm + k * ld, ld, status, st));
       // [R_adj D_adj] -= C_adj^T [B C]   (PAPER.md:311 and the C_adj^T B term of 319),
       // split-K over the m rows with a fixed-order reduction
       int splits, kps;
-      splitk_choice(m, k, &splits, &kps);
-      CK(gemm_splitk_tn(NB, (int)k, (int)m, splits, kps, Ctmp, NB, Lw + k * ld, ld, Pbuf, status, st));
-      CK(splitk_reduce_sub(Pbuf, splits, NB, (int)k, Wm + j * ld, ld, status, st));
-      CK(copy_block(Ctmp, NB, Cb, ld, m, NB, st));
+      splitk_choice(m, k, B, &splits, &kps);
+      CK(gemm_splitk_tn((int)B, (int)k, (int)m, splits, kps, Ctmp, B, Lw + k * ld, ld, Pbuf, status, st));
+      CK(splitk_reduce_sub(Pbuf, splits, (int)B, (int)k, Wm + j * ld, ld, status, st));
+      CK(copy_block(Ctmp, B, Cb, ld, m, B, st));
     }
     // D_adj = transpose(D) * D_adj; copy_lower_tri_to_upper_tri
-    CK(gemm128(true, true, false, false, D, ld, Dbar, ld, T1, NB, status, st));
+    CK(gemm_small((int)B, true, true, false, D, ld, Dbar, ld, T1, B, status, st));
     // D = transpose(lower_triangular_inverse(D)); D_adj = D * transpose(D * D_adj)
     // computed as S = D^-T sym(P) D^-1
-    CK(gemm128(true, false, false, true, Db, NB, T1, NB, T2, NB, status, st));
-    CK(gemm128(false, false, false, false, T2, NB, Db, NB, T3, NB, status, st));
+    CK(gemm_small((int)B, true, false, true, Db, B, T1, B, T2, B, status, st));
+    CK(gemm_small((int)B, false, false, false, T2, B, Db, B, T3, B, status, st));
     // copy_lower_tri_to_upper_tri; diagonal * 0.5; set_zeros_in_upper_tri
-    CK(phi_sym(T3, T4, Dbar, ld, status, st));
+    CK(phi_sym(T3, T4, Dbar, ld, status, st, (int)B));
     // R_adj = R_adj - D_adj * R
-    if (j > 0) CK(gemm_full(true, false, NB, (int)j, NB, -1.0, 1, T4, NB, R, ld, Wm + j * ld, ld, status, st));
+    if (j > 0)
+      CK(gemm_full(true, false, (int)B, (int)j, (int)B, -1.0, 1, T4, B, R, ld, Wm + j * ld, ld, status, st));
     if (out) {  // column block j is final: ship rows j.. of it
-      CK(cudaEventRecord(col_done[j / NB], st));
-      CK(cudaStreamWaitEvent(g.d2h, col_done[j / NB], 0));
+      CK(cudaEventRecord(col_done[j / B], st));
+      CK(cudaStreamWaitEvent(g.d2h, col_done[j / B], 0));
       int rc = copy_rect_d2h(*out, Wm, ld, j, N, j, k, g.d2h);
       if (rc) return rc;
     }
@@ -528,8 +569,10 @@ int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_ba
   CK(cudaMemsetAsync(status, 0, sizeof(int), st));
   CK(init_pad(Lw, n, N, 1.0, st));
   CK(init_pad(Wm, n, N, 0.0, st));
+  const int64_t B = plan.B;
   cudaEvent_t* ready = g.xev.data() + 2;
   cudaEvent_t* col_done = ready + nblk;
+  double* scratch = (double*)((char*)g.ws + al(sizeof(int) * 64) + plan.dinv);  // Pbuf, free until the loop
   CK(cudaEventRecord(g.xev[0], st));
   CK(cudaStreamWaitEvent(g.h2d, g.xev[0], 0));
   for (int64_t b = nblk - 1; b >= 0; --b) {  // bottom-up: the order the reverse sweep needs
@@ -542,7 +585,10 @@ int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_ba
       CK(zero_tile_upper(Wm, N, r0, (int)(r1 - r0), g.h2d));  // only the lower triangle of L_bar is read
       CK(check_diag(Lw + r0 * N + r0, r1 - r0, N, status, g.h2d, r0));
     }
-    CK(tri_inverse_batched(Lw + r0 * N + r0, N, 1, Dinv + b * NB * NB, status, g.h2d));
+    if (r0 % B == 0) {  // all rows of diagonal block r0 / B are in: its inverse
+      rc = block_inverses(Lw, N, B, r0 / B, 1, Dinv, scratch, status, g.h2d);
+      if (rc) return rc;
+    }
     CK(cudaEventRecord(ready[b], g.h2d));
   }
   HostOut out{A_bar, n};
@@ -569,6 +615,14 @@ int stan_cl_set_block_size(int nb) {
 }
 
 int stan_cl_get_block_size(void) { return g.nb; }
+
+int stan_cl_set_adjoint_block_size(int nb) {
+  if (nb == 0 || nb == NB || nb == 2 * NB) {
+    g.adj_nb = nb;
+    return STAN_CL_OK;
+  }
+  return STAN_CL_EINVAL;
+}
 
 size_t stan_cl_workspace_bytes(int64_t n) {
   if (n <= 0) return 0;

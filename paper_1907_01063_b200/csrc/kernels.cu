@@ -555,7 +555,8 @@ constexpr int TRI_PACKED = NB * (NB + 1) / 2;  // D lower triangle, row i at i(i
 constexpr int TINV_SMEM = (TRI_PACKED + NB * TP) * (int)sizeof(double);
 
 __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, int64_t ld,
-                                                             double* Dinv, const int* status) {
+                                                             double* Dinv, int64_t ldo, int64_t ostride,
+                                                             int per, int64_t ohalf, const int* status) {
   if (*status != 0) return;
   extern __shared__ double sm[];
   double* D = sm;               // packed lower: D[i][k] at i(i+1)/2 + k
@@ -577,15 +578,17 @@ __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, in
     x[i] = -s / di[i];
   }
   __syncthreads();
-  double* dst = Dinv + (long long)b * NB * NB;
+  // block b lands in output group b / per (stride ostride), sub-block b % per
+  // (offset ohalf): per = 2 places consecutive 128-blocks on the diagonal of 256 x 256 blocks
+  double* dst = Dinv + (long long)(b / per) * ostride + (long long)(b % per) * ohalf;
   for (int idx = c; idx < NB * NB; idx += NB) {
     const int i = idx >> 7, k = idx & (NB - 1);
-    dst[idx] = X[k * TP + i];
+    dst[(long long)i * ldo + k] = X[k * TP + i];
   }
 }
 
 cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* Dinv,
-                                const int* status, cudaStream_t st) {
+                                const int* status, cudaStream_t st, int64_t ldo, int64_t ostride, int per) {
   Prof prof_(PROF_TRINV, (double)nblk * NB * NB * NB / 3.0, st, 12.0 * nblk * NB * NB);
   if (nblk == 0) return cudaSuccess;
   static bool attr = false;
@@ -595,7 +598,10 @@ cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* D
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  tri_inverse_kernel<<<nblk, NB, TINV_SMEM, st>>>(L, ld, Dinv, status);
+  if (ldo == 0) ldo = NB;
+  if (ostride == 0) ostride = (int64_t)NB * NB;
+  if (per < 1) per = 1;
+  tri_inverse_kernel<<<nblk, NB, TINV_SMEM, st>>>(L, ld, Dinv, ldo, ostride, per, NB * ldo + NB, status);
   return cudaGetLastError();
 }
 
@@ -603,115 +609,123 @@ cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* D
 constexpr int G128_AP = NB + 4, G128_BP = 32 + 4;
 constexpr int G128_SMEM = (32 * G128_AP + NB * G128_BP) * (int)sizeof(double);
 
-// All 64 global loads of a thread are issued before any is used (fully unrolled,
-// compile-time layout flags), so the slice staging costs one L2 latency, not 64.
-template <bool A_T, bool A_TRIL, bool B_T, bool B_SYM>
-__global__ void __launch_bounds__(128) gemm128_kernel(const double* __restrict__ A, int64_t lda,
-                                                      const double* __restrict__ B, int64_t ldb,
-                                                      double* __restrict__ C, int64_t ldc,
-                                                      const int* status) {
+// C[S x S] = sign * op(A) op(B) over K = S (S = 128 or 256), batched over
+// blockIdx.z with element strides sA/sB/sC.  A_T: A given as K x M; A_TRIL: only
+// the lower triangle of A's storage is read; B_SYM: B read as sym(tril(B)).
+// 128 threads per 32 x 32 output tile; K staged through shared memory in
+// 128-deep chunks whose 64 global loads per thread are all issued before use.
+template <int S, bool A_T, bool A_TRIL, bool B_SYM>
+__global__ void __launch_bounds__(128) gemmS_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                                                    const double* __restrict__ B, int64_t ldb, int64_t sB,
+                                                    double* __restrict__ C, int64_t ldc, int64_t sC,
+                                                    double sign, const int* status) {
   if (*status != 0) return;
   extern __shared__ double sm[];
-  double* As = sm;                 // [32][G128_AP]   As[m][k]
-  double* Bs = sm + 32 * G128_AP;  // [128][G128_BP]  Bs[k][n]
+  double* As = sm;                 // [32][G128_AP]   As[m][k - k0]
+  double* Bs = sm + 32 * G128_AP;  // [128][G128_BP]  Bs[k - k0][n]
+  A += (long long)blockIdx.z * sA;
+  B += (long long)blockIdx.z * sB;
+  C += (long long)blockIdx.z * sC;
   const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
-  const int tid = threadIdx.x;
-  double va[32], vb[32];
-#pragma unroll
-  for (int q = 0; q < 32; ++q) {
-    const int idx = tid + q * 128;
-    if (A_T) {
-      const int k = idx >> 5, m = idx & 31;
-      va[q] = (A_TRIL && m0 + m > k) ? 0.0 : __ldg(A + (long long)k * lda + m0 + m);
-    } else {
-      const int m = idx >> 7, k = idx & (NB - 1);
-      va[q] = (A_TRIL && k > m0 + m) ? 0.0 : __ldg(A + (long long)(m0 + m) * lda + k);
-    }
-    if (B_SYM) {
-      const int k = idx >> 5, gn = n0 + (idx & 31);
-      vb[q] = (k >= gn) ? __ldg(B + (long long)k * ldb + gn) : __ldg(B + (long long)gn * ldb + k);
-    } else if (B_T) {
-      const int n = idx >> 7, k = idx & (NB - 1);
-      vb[q] = __ldg(B + (long long)(n0 + n) * ldb + k);
-    } else {
-      const int k = idx >> 5, n = idx & 31;
-      vb[q] = __ldg(B + (long long)k * ldb + n0 + n);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < 32; ++q) {
-    const int idx = tid + q * 128;
-    if (A_T) As[(idx & 31) * G128_AP + (idx >> 5)] = va[q];
-    else As[(idx >> 7) * G128_AP + (idx & (NB - 1))] = va[q];
-    if (B_T && !B_SYM) Bs[(idx & (NB - 1)) * G128_BP + (idx >> 7)] = vb[q];
-    else Bs[(idx >> 5) * G128_BP + (idx & 31)] = vb[q];
-  }
-  __syncthreads();
-  const int lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
   double acc[2][2][2] = {};
+  for (int k0 = 0; k0 < S; k0 += NB) {
+    double va[32], vb[32];
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int idx = tid + q * 128;
+      if (A_T) {
+        const int k = k0 + (idx >> 5), m = m0 + (idx & 31);
+        va[q] = (A_TRIL && m > k) ? 0.0 : __ldg(A + (long long)k * lda + m);
+      } else {
+        const int m = m0 + (idx >> 7), k = k0 + (idx & (NB - 1));
+        va[q] = (A_TRIL && k > m) ? 0.0 : __ldg(A + (long long)m * lda + k);
+      }
+      const int k = k0 + (idx >> 5), gn = n0 + (idx & 31);
+      if (B_SYM) vb[q] = (k >= gn) ? __ldg(B + (long long)k * ldb + gn) : __ldg(B + (long long)gn * ldb + k);
+      else vb[q] = __ldg(B + (long long)k * ldb + gn);
+    }
+    if (k0) __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 32; ++q) {
+      const int idx = tid + q * 128;
+      if (A_T) As[(idx & 31) * G128_AP + (idx >> 5)] = va[q];
+      else As[(idx >> 7) * G128_AP + (idx & (NB - 1))] = va[q];
+      Bs[(idx >> 5) * G128_BP + (idx & 31)] = vb[q];
+    }
+    __syncthreads();
 #pragma unroll 8
-  for (int k4 = 0; k4 < NB; k4 += 4) {
-    double af[2], bf[2];
+    for (int k4 = 0; k4 < NB; k4 += 4) {
+      double af[2], bf[2];
 #pragma unroll
-    for (int i = 0; i < 2; ++i) af[i] = As[(wm * 16 + i * 8 + g) * G128_AP + k4 + t];
+      for (int i = 0; i < 2; ++i) af[i] = As[(wm * 16 + i * 8 + g) * G128_AP + k4 + t];
 #pragma unroll
-    for (int j = 0; j < 2; ++j) bf[j] = Bs[(k4 + t) * G128_BP + wn * 16 + j * 8 + g];
+      for (int j = 0; j < 2; ++j) bf[j] = Bs[(k4 + t) * G128_BP + wn * 16 + j * 8 + g];
 #pragma unroll
-    for (int i = 0; i < 2; ++i)
+      for (int i = 0; i < 2; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+    }
   }
 #pragma unroll
   for (int i = 0; i < 2; ++i)
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int r = m0 + wm * 16 + i * 8 + g, c = n0 + wn * 16 + j * 8 + 2 * t;
-      *reinterpret_cast<double2*>(C + (long long)r * ldc + c) = make_double2(acc[i][j][0], acc[i][j][1]);
+      *reinterpret_cast<double2*>(C + (long long)r * ldc + c) = make_double2(sign * acc[i][j][0], sign * acc[i][j][1]);
     }
 }
 
-template <bool A_T, bool A_TRIL, bool B_T, bool B_SYM>
-static cudaError_t gemm128_launch(const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
-                                  int64_t ldc, const int* status, cudaStream_t st) {
-  auto kern = gemm128_kernel<A_T, A_TRIL, B_T, B_SYM>;
+template <int S, bool A_T, bool A_TRIL, bool B_SYM>
+static cudaError_t gemmS_launch(const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB,
+                                double* C, int64_t ldc, int64_t sC, double sign, int batch, const int* status,
+                                cudaStream_t st) {
+  auto kern = gemmS_kernel<S, A_T, A_TRIL, B_SYM>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G128_SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  kern<<<dim3(4, 4), 128, G128_SMEM, st>>>(A, lda, B, ldb, C, ldc, status);
+  kern<<<dim3(S / 32, S / 32, batch), 128, G128_SMEM, st>>>(A, lda, sA, B, ldb, sB, C, ldc, sC, sign, status);
   return cudaGetLastError();
 }
 
-cudaError_t gemm128(bool a_t, bool a_tril, bool b_t, bool b_sym, const double* A, int64_t lda,
-                    const double* B, int64_t ldb, double* C, int64_t ldc, const int* status,
-                    cudaStream_t st) {
-  Prof prof_(PROF_SMALL, 2.0 * NB * NB * NB, st, 24.0 * NB * NB);
-  // the three products of the symbolic diagonal step (api.cu) -- and only those
-  if (a_t && a_tril && !b_t && !b_sym) return gemm128_launch<true, true, false, false>(A, lda, B, ldb, C, ldc, status, st);
-  if (a_t && !a_tril && !b_t && b_sym) return gemm128_launch<true, false, false, true>(A, lda, B, ldb, C, ldc, status, st);
-  if (!a_t && !a_tril && !b_t && !b_sym) return gemm128_launch<false, false, false, false>(A, lda, B, ldb, C, ldc, status, st);
+cudaError_t gemm_small(int S, bool a_t, bool a_tril, bool b_sym, const double* A, int64_t lda, const double* B,
+                       int64_t ldb, double* C, int64_t ldc, const int* status, cudaStream_t st, double sign,
+                       int batch, int64_t sA, int64_t sB, int64_t sC) {
+  Prof prof_(PROF_SMALL, 2.0 * S * S * S * batch, st, 24.0 * S * S * batch);
+#define STANCL_GS(SS, AT, AL, BS)                                                                           \
+  if (S == SS && a_t == AT && a_tril == AL && b_sym == BS)                                                  \
+    return gemmS_launch<SS, AT, AL, BS>(A, lda, sA, B, ldb, sB, C, ldc, sC, sign, batch, status, st);
+  STANCL_GS(128, true, true, false)
+  STANCL_GS(128, true, false, true)
+  STANCL_GS(128, false, false, false)
+  STANCL_GS(256, true, true, false)
+  STANCL_GS(256, true, false, true)
+  STANCL_GS(256, false, false, false)
+#undef STANCL_GS
   return cudaErrorInvalidValue;
 }
 
-// S -> Ssym = mirror(tril S) and D_bar = Phi(S)
+// S (n x n, ld n; n = 128 or 256) -> Ssym = mirror(tril S) and D_bar = Phi(S)
+//
 __global__ void phi_sym_kernel(const double* __restrict__ S, double* __restrict__ Ssym,
-                               double* __restrict__ Dbar, int64_t ldd, const int* status) {
+                               double* __restrict__ Dbar, int64_t ldd, int n, const int* status) {
   if (*status != 0) return;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < NB * NB; idx += gridDim.x * blockDim.x) {
-    const int a = idx >> 7, b = idx & (NB - 1);
-    const double low = (a >= b) ? S[a * NB + b] : S[b * NB + a];
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n * n; idx += gridDim.x * blockDim.x) {
+    const int a = idx / n, b = idx - a * n;
+    const double low = (a >= b) ? S[a * n + b] : S[b * n + a];
     Ssym[idx] = low;
     Dbar[(long long)a * ldd + b] = (a > b) ? low : (a == b ? 0.5 * low : 0.0);
   }
 }
 
 cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, const int* status,
-                    cudaStream_t st) {
-  Prof prof_(PROF_MISC, 0.0, st, 24.0 * NB * NB);
-  phi_sym_kernel<<<64, 256, 0, st>>>(S, Ssym, Dbar, ldd, status);
+                    cudaStream_t st, int n) {
+  Prof prof_(PROF_MISC, 0.0, st, 24.0 * n * n);
+  phi_sym_kernel<<<64, 256, 0, st>>>(S, Ssym, Dbar, ldd, n, status);
   return cudaGetLastError();
 }
 

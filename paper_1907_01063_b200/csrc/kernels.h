@@ -89,18 +89,23 @@ cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double*
                               const int* status, cudaStream_t st);
 
 // ---- adjoint diagonal-block helpers (R4, R5) ----
-// Dinv[b] = (W[b*128.., b*128..])^-1 for b in [0, nblk), lower, by substitution
+// (L[b*128.., b*128..])^-1 for b in [0, nblk), lower, by substitution; block b is
+// written with leading dimension ldo at Dinv + (b/per)*ostride + (b%per)*(128*ldo+128)
+// (defaults: contiguous 128 x 128 blocks; per = 2 fills the diagonal halves of
+// 256 x 256 blocks)
 cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* Dinv,
-                                const int* status, cudaStream_t st);
-// C[128x128] (ldc) = op(A) op(B) over K = 128; a_t: A given as K x M; a_tril: only the
-// lower triangle of A's storage is read (upper taken as 0); b_t: B given as N x K;
-// b_sym: B read as sym(tril(B)) i.e. B[max][min]
-cudaError_t gemm128(bool a_t, bool a_tril, bool b_t, bool b_sym, const double* A, int64_t lda,
-                    const double* B, int64_t ldb, double* C, int64_t ldc, const int* status,
-                    cudaStream_t st);
-// S (128x128, ld 128): Ssym = mirror(tril(S)) -> ws; Dbar = Phi(S) = tril(S) with halved diagonal
+                                const int* status, cudaStream_t st, int64_t ldo = 0, int64_t ostride = 0,
+                                int per = 1);
+// C[S x S] (ldc) = sign * op(A) op(B) over K = S, S in {128, 256}, batched over
+// `batch` problems with element strides sA/sB/sC.  a_t: A given as K x M;
+// a_tril: only the lower triangle of A's storage is read (upper taken as 0);
+// b_sym: B read as sym(tril(B)) i.e. B[max][min]; B is otherwise K x N.
+cudaError_t gemm_small(int S, bool a_t, bool a_tril, bool b_sym, const double* A, int64_t lda, const double* B,
+                       int64_t ldb, double* C, int64_t ldc, const int* status, cudaStream_t st,
+                       double sign = 1.0, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0);
+// S (n x n, ld n): Ssym = mirror(tril(S)) -> ws; Dbar = Phi(S) = tril(S) with halved diagonal
 cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, const int* status,
-                    cudaStream_t st);
+                    cudaStream_t st, int n = 128);
 // status = first base+k+1 with !(L[k][k] > 0 && finite), k < n
 cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st, int64_t base = 0);
 

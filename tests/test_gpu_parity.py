@@ -206,6 +206,30 @@ def test_adjoint_integer_exact(sc, n, band):
     assert np.array_equal(host(sc.cholesky_adjoint(dev(L), dev(W))), want)
 
 
+@pytest.mark.parametrize("n", [300, 1024, 2048])
+def test_adjoint_blocking_invariance(sc, n):
+    # adjoint block 128 vs 256: both within the bar of the oracle and of each other
+    # (SPEC.md:492); the integer-exact banded family is bit-identical across both
+    L = oracle.cholesky(se(n))
+    W = inputs.lbar(n)
+    want = oracle.cholesky_adjoint(L, W)
+    Li = inputs.unit_lower_pm1(n, seed=3, band=2)
+    Wi = inputs.int_lbar(n, seed=4)
+    want_i = oracle.cholesky_adjoint(Li, Wi)
+    lib = sc.load()
+    outs = []
+    try:
+        for nb in (128, 256):
+            assert lib.stan_cl_set_adjoint_block_size(nb) == 0
+            outs.append(host(sc.cholesky_adjoint(dev(L), dev(W))))
+            assert np.array_equal(host(sc.cholesky_adjoint(dev(Li), dev(Wi))), want_i)
+    finally:
+        lib.stan_cl_set_adjoint_block_size(0)
+    for o in outs:
+        assert relf(o, want) <= A_BAR_TOL
+    assert relf(outs[0], outs[1]) <= 1e-10
+
+
 def test_adjoint_in_place_and_upper_garbage(sc):
     n = 384
     L = oracle.cholesky(se(n))
