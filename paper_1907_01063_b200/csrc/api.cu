@@ -15,6 +15,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <algorithm>
+#include <map>
+#include <tuple>
 #include <mutex>
 #include <vector>
 
@@ -33,6 +35,7 @@ struct State {
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> xev;  // per-block events of the streamed host transfers
   void* mat[2] = {nullptr, nullptr};  // cached N x N working matrices (padded / host paths)
+  cudaStream_t cap = nullptr;         // capture stream for the CUDA-graph cache
   size_t mat_cap[2] = {0, 0};
   int nb = 0;      // forward outer block: 0 = auto, 128 or 256
   int adj_nb = 0;  // adjoint block: 0 = auto, 128 or 256
@@ -477,26 +480,119 @@ int read_status() {
 
 }  // namespace
 
+// ------------------------------------------------------------- graph cache
+// The first call with a given (operation, order, buffers, block sizes) runs
+// eagerly (it sizes every workspace); the second captures the same enqueue
+// sequence -- including the lookahead side stream and the copy streams, joined
+// by events -- into a CUDA graph, and later calls replay it.  This removes the
+// per-launch CPU cost of ~1000 launches per call (latency-bound small n).
+// Used for the device entry points when n <= 4096 (the latency-bound regime,
+// where it saves ~10%); at large n the captured graph loses the stream priority
+// that lets the lookahead panel overtake the trailing update, so eager launches
+// are faster there (measured: n=16384 +2%, host path +35%).  STAN_CL_GRAPH=0
+// disables, =2 forces it for every size.  Off while per-launch profiling is on.
+struct GraphKey {
+  int op;
+  int64_t n;
+  const void* p[4];
+  int64_t a, b;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(op, n, p[0], p[1], p[2], p[3], a, b) < std::tie(o.op, o.n, o.p[0], o.p[1], o.p[2], o.p[3], o.a, o.b);
+  }
+};
+struct GraphEntry {
+  cudaGraphExec_t exec = nullptr;
+  long long launches = 0;
+  int seen = 0;
+  bool broken = false;
+};
+std::map<GraphKey, GraphEntry> g_graphs;
+
+int graph_mode() {
+  static const int m = [] {
+    const char* e = getenv("STAN_CL_GRAPH");
+    return e ? atoi(e) : 1;
+  }();
+  return m;
+}
+bool graphs_enabled(int64_t n) {
+  const int m = graph_mode();
+  return m != 0 && !prof_active() && (m == 2 || n <= 4096);
+}
+
+void clear_graphs() {
+  for (auto& kv : g_graphs)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  g_graphs.clear();
+}
+
+template <class F>
+int run_cached(const GraphKey& key, F&& enqueue) {
+  if (!graphs_enabled(key.op >= 2 ? 1 << 30 : key.n)) return enqueue();  // host paths: eager
+  auto it = g_graphs.find(key);
+  if (it == g_graphs.end()) {
+    if (g_graphs.size() >= 16) clear_graphs();
+    it = g_graphs.emplace(key, GraphEntry{}).first;
+  }
+  GraphEntry& e = it->second;
+  if (e.broken || e.seen++ == 0) return enqueue();
+  if (!e.exec) {
+    if (!g.cap) CK(cudaStreamCreateWithFlags(&g.cap, cudaStreamNonBlocking));
+    cudaStream_t user = g.stream;
+    g.stream = g.cap;
+    const long long l0 = launches();
+    cudaError_t ce = cudaStreamBeginCapture(g.cap, cudaStreamCaptureModeThreadLocal);
+    int rc = ce == cudaSuccess ? enqueue() : STAN_CL_ECUDA;
+    cudaGraph_t graph = nullptr;
+    cudaError_t ee = cudaStreamEndCapture(g.cap, &graph);
+    g.stream = user;
+    const long long captured = launches() - l0;
+    count_launch((int)-captured);  // nothing ran yet: replays count
+    if (rc != STAN_CL_OK || ce != cudaSuccess || ee != cudaSuccess || !graph) {
+      cudaGetLastError();
+      if (graph) cudaGraphDestroy(graph);
+      e.broken = true;  // fall back to eager launches for this key
+      return enqueue();
+    }
+    cudaError_t ie = cudaGraphInstantiate(&e.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+      cudaGetLastError();
+      e.exec = nullptr;
+      e.broken = true;
+      return enqueue();
+    }
+    e.launches = captured;
+  }
+  CK(cudaGraphLaunch(e.exec, g.stream));
+  count_launch((int)e.launches);
+  return STAN_CL_OK;
+}
+
 // ===================================================================== C ABI
 extern "C" {
 
 int stan_cl_cholesky_async(int64_t n, const double* A, double* L, int* d_info) {
-  return cholesky_enqueue(n, A, L, d_info);
+  if (n <= 0) return cholesky_enqueue(n, A, L, d_info);
+  return run_cached(GraphKey{0, n, {A, L, d_info, nullptr}, g.nb, 0},
+                    [&] { return cholesky_enqueue(n, A, L, d_info); });
 }
 
 int stan_cl_cholesky(int64_t n, const double* A, double* L) {
-  int rc = cholesky_enqueue(n, A, L, nullptr);
+  int rc = stan_cl_cholesky_async(n, A, L, nullptr);
   if (rc || n == 0) return rc;
   return read_status();
 }
 
 int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_bar, double* A_bar,
                                    int* d_info) {
-  return adjoint_enqueue(n, L, L_bar, A_bar, d_info);
+  if (n <= 0) return adjoint_enqueue(n, L, L_bar, A_bar, d_info);
+  return run_cached(GraphKey{1, n, {L, L_bar, A_bar, d_info}, g.adj_nb, 0},
+                    [&] { return adjoint_enqueue(n, L, L_bar, A_bar, d_info); });
 }
 
 int stan_cl_cholesky_adjoint(int64_t n, const double* L, const double* L_bar, double* A_bar) {
-  int rc = adjoint_enqueue(n, L, L_bar, A_bar, nullptr);
+  int rc = stan_cl_cholesky_adjoint_async(n, L, L_bar, A_bar, nullptr);
   if (rc || n == 0) return rc;
   return read_status();
 }
@@ -518,10 +614,7 @@ int stan_cl_gp_exp_quad_cov(int64_t n, const double* x, double alpha, double rho
 // factored; the adjoint uploads row blocks bottom-up (the order the reverse
 // sweep consumes them) and ships each column block of A_bar as soon as it is
 // final.
-int stan_cl_cholesky_host(int64_t n, const double* A, double* L) {
-  if (n < 0) return STAN_CL_EINVAL;
-  if (n == 0) return STAN_CL_OK;
-  if (!A || !L) return STAN_CL_EINVAL;
+int cholesky_host_enqueue(int64_t n, const double* A, double* L) {
   int64_t OB = g.nb;
   if (!OB) OB = (n % (2 * NB) == 0) ? 2 * NB : (n % NB == 0) ? NB : (n > 1024 ? 2 * NB : NB);
   const int64_t N = round_up(n, OB);
@@ -548,13 +641,20 @@ int stan_cl_cholesky_host(int64_t n, const double* A, double* L) {
   if (rc) return rc;
   CK(cudaEventRecord(g.xev[2], g.d2h));
   CK(cudaStreamWaitEvent(st, g.xev[2], 0));
+  return STAN_CL_OK;
+}
+
+int stan_cl_cholesky_host(int64_t n, const double* A, double* L) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!A || !L) return STAN_CL_EINVAL;
+  int rc = run_cached(GraphKey{2, n, {A, L, nullptr, nullptr}, g.nb, 0},
+                      [&] { return cholesky_host_enqueue(n, A, L); });
+  if (rc) return rc;
   return read_status();
 }
 
-int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar) {
-  if (n < 0) return STAN_CL_EINVAL;
-  if (n == 0) return STAN_CL_OK;
-  if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
+int adjoint_host_enqueue(int64_t n, const double* L, const double* L_bar, double* A_bar) {
   const AdjPlan plan = adj_plan(n);
   const int64_t N = plan.N, nblk = N / NB;
   int rc = ensure_ws(plan.total);
@@ -596,6 +696,16 @@ int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_ba
   if (rc) return rc;
   CK(cudaEventRecord(g.xev[1], g.d2h));
   CK(cudaStreamWaitEvent(st, g.xev[1], 0));
+  return STAN_CL_OK;
+}
+
+int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
+  int rc = run_cached(GraphKey{3, n, {L, L_bar, A_bar, nullptr}, g.adj_nb, 0},
+                      [&] { return adjoint_host_enqueue(n, L, L_bar, A_bar); });
+  if (rc) return rc;
   return read_status();
 }
 
@@ -669,6 +779,11 @@ int stan_cl_profile_read_bytes(int kind, double* bytes) {
 }
 
 int stan_cl_finalize(void) {
+  clear_graphs();
+  if (g.cap) {
+    cudaStreamDestroy(g.cap);
+    g.cap = nullptr;
+  }
   if (g.ws) {
     cudaStreamSynchronize(g.stream);
     cudaFree(g.ws);

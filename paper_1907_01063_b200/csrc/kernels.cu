@@ -76,6 +76,7 @@ Prof::~Prof() {
   }
 }
 void prof_enable(unsigned mask) { g_prof.mask = mask; }
+bool prof_active() { return g_prof.mask != 0; }
 void prof_collect() {
   for (auto& r : g_prof.recs) {
     cudaEventSynchronize(r.e1);

@@ -35,6 +35,7 @@ struct Prof {
   cudaEvent_t e0_ = nullptr, e1_ = nullptr;
 };
 void prof_enable(unsigned mask);  // bit k enables class k
+bool prof_active();
 void prof_reset();
 void prof_read(int kind, double* ms, double* flops, long long* count, double* bytes = nullptr);
 

@@ -313,3 +313,34 @@ def test_kernel_launch_counter(sc):
     before = sc.kernel_launches()
     sc.cholesky(dev(se(256)))
     assert sc.kernel_launches() > before
+
+
+@pytest.mark.parametrize("n", [300, 1024])
+def test_graph_replay_same_buffers(sc, n):
+    # the 2nd call with the same buffers captures a CUDA graph, later calls replay
+    # it: results must follow the buffer CONTENTS of every call
+    A = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    L = torch.empty_like(A)
+    W = torch.empty_like(A)
+    Ab = torch.empty_like(A)
+    before = sc.kernel_launches()
+    for it in range(4):
+        K = se(n, seed=100 + it)
+        A.copy_(torch.from_numpy(K))
+        sc.cholesky(A, out=L)
+        Lo = oracle.cholesky(K)
+        assert relf(host(L), Lo) <= L_BAR_TOL, it
+        Wn = inputs.lbar(n, seed=200 + it)
+        L.copy_(torch.from_numpy(Lo))
+        W.copy_(torch.from_numpy(Wn))
+        sc.cholesky_adjoint(L, W, out=Ab)
+        assert relf(host(Ab), oracle.cholesky_adjoint(Lo, Wn)) <= A_BAR_TOL, it
+    assert sc.kernel_launches() > before      # replays are counted
+    Ah = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    Lh = torch.empty_like(Ah).pin_memory()
+    for it in range(3):
+        K = se(n, seed=300 + it)
+        Ah.copy_(torch.from_numpy(K))
+        assert sc.cholesky_host(Ah, Lh) == 0
+        lo = np.tril_indices(n)
+        assert relf(Lh.numpy()[lo], oracle.cholesky(K)[lo]) <= L_BAR_TOL, it
