@@ -112,6 +112,38 @@ int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_b
 int stan_cl_cholesky_host(int64_t n, const double* A, double* L);
 int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar);
 
+/*
+ * ---- multi-GPU (one process per GPU) ----
+ * Layout: block-cyclic by 256-wide block COLUMNS over G ranks (process grid
+ * P = 1, Q = G): global block column J (columns J*256 .. J*256+255) is stored on
+ * rank J % G as local block column J / G of a row-major n x ld_local array
+ * (ld_local >= 256 * number of owned block columns).  n must be a multiple of
+ * 256.  Only broadcasts cross NVLink (each factored panel; C_bar D^-1 and
+ * sym(S) per adjoint step).  Outputs: the lower triangle of every owned block
+ * column is written (+0.0 above the diagonal inside the 256 x 256 diagonal
+ * tiles); the part of a block column above its diagonal tile is not touched.
+ *   stan_cl_dist_get_unique_id  rank 0; the 128-byte NCCL id is shipped to the
+ *                               other ranks by the caller (torch.distributed)
+ *   stan_cl_dist_init           P must be 1 and Q == nranks; the CUDA device of
+ *                               the calling thread is the rank's device
+ *   stan_cl_dist_cholesky       in place on A_local (nb: 0 or 256)
+ *   stan_cl_dist_cholesky_adjoint  L_local read-only; Lbar_to_Abar_local in place
+ * Return values as the single-GPU calls (numerical status all-reduced with max);
+ * STAN_CL_ENCCL when NCCL cannot be loaded or fails.
+ */
+int stan_cl_dist_get_unique_id(void* out128);
+int stan_cl_dist_init(int nranks, int rank, const void* id128, int P, int Q);
+int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local);
+int stan_cl_dist_cholesky_adjoint(int64_t n, int nb, const double* L_local, double* Lbar_to_Abar_local,
+                                  int64_t ld_local);
+int stan_cl_dist_finalize(void);
+/* The same distributed algorithms with G simulated ranks in this process on
+ * the current device (broadcasts become device copies): the layouts above,
+ * one local array per rank.  For testing the multi-GPU path on one GPU. */
+int stan_cl_dist_sim_cholesky(int64_t n, int G, double* const* A_locals, int64_t ld_local);
+int stan_cl_dist_sim_cholesky_adjoint(int64_t n, int G, const double* const* L_locals, double* const* W_locals,
+                                      int64_t ld_local);
+
 /* ---- control ---- */
 int stan_cl_set_stream(void* cuda_stream); /* cudaStream_t; NULL = legacy default stream */
 void* stan_cl_get_stream(void);

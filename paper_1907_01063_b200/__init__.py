@@ -57,6 +57,13 @@ SIGNATURES = {
                                   ctypes.POINTER(ctypes.c_longlong)]),
     "stan_cl_profile_read_bytes": (_I, [_I, ctypes.POINTER(ctypes.c_double)]),
     "stan_cl_finalize": (_I, []),
+    "stan_cl_dist_get_unique_id": (_I, [_P]),
+    "stan_cl_dist_init": (_I, [_I, _I, _P, _I, _I]),
+    "stan_cl_dist_cholesky": (_I, [_I64, _I, _P, _I64]),
+    "stan_cl_dist_cholesky_adjoint": (_I, [_I64, _I, _P, _P, _I64]),
+    "stan_cl_dist_finalize": (_I, []),
+    "stan_cl_dist_sim_cholesky": (_I, [_I64, _I, _P, _I64]),
+    "stan_cl_dist_sim_cholesky_adjoint": (_I, [_I64, _I, _P, _P, _I64]),
     "stan_cl_version": (_I, []),
 }
 
@@ -201,6 +208,92 @@ def cholesky_adjoint_host(L: torch.Tensor, Lbar: torch.Tensor, Abar: torch.Tenso
         _bind_stream(dev)
         return _check("stan_cl_cholesky_adjoint_host", load().stan_cl_cholesky_adjoint_host(
             L.shape[0], L.data_ptr(), Lbar.data_ptr(), Abar.data_ptr()))
+
+
+# ------------------------------------------------------------------ multi-GPU
+DIST_BLOCK = 256
+
+
+def dist_owned_blocks(n: int, G: int, q: int) -> int:
+    T = n // DIST_BLOCK
+    return (T - q + G - 1) // G if q < T else 0
+
+
+def dist_scatter(A: torch.Tensor, G: int, q: int) -> torch.Tensor:
+    """Rank q's local array (block columns J = q, q+G, ... of A, contiguous)."""
+    n = A.shape[0]
+    cols = [A[:, J * DIST_BLOCK:(J + 1) * DIST_BLOCK] for J in range(q, n // DIST_BLOCK, G)]
+    return torch.cat(cols, dim=1).contiguous() if cols else A.new_empty((n, 0))
+
+
+def dist_gather(locals_: list, n: int) -> torch.Tensor:
+    """Inverse of dist_scatter over all ranks."""
+    G = len(locals_)
+    out = locals_[0].new_zeros((n, n))
+    for q, Lq in enumerate(locals_):
+        for i, J in enumerate(range(q, n // DIST_BLOCK, G)):
+            out[:, J * DIST_BLOCK:(J + 1) * DIST_BLOCK] = Lq[:, i * DIST_BLOCK:(i + 1) * DIST_BLOCK]
+    return out
+
+
+def _ptr_array(ts):
+    arr = (ctypes.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+    return arr
+
+
+def dist_sim_cholesky(A_locals: list, n: int) -> int:
+    """Distributed forward with len(A_locals) simulated ranks on this device (in place)."""
+    G = len(A_locals)
+    ld = max(t.shape[1] for t in A_locals)
+    assert all(t.shape[1] == ld and t.is_contiguous() for t in A_locals), "equal-width local arrays"
+    with torch.cuda.device(A_locals[0].device):
+        _bind_stream(A_locals[0].device)
+        return _check("stan_cl_dist_sim_cholesky",
+                      load().stan_cl_dist_sim_cholesky(n, G, ctypes.cast(_ptr_array(A_locals), ctypes.c_void_p), ld))
+
+
+def dist_sim_cholesky_adjoint(L_locals: list, W_locals: list, n: int) -> int:
+    G = len(L_locals)
+    ld = max(t.shape[1] for t in L_locals)
+    with torch.cuda.device(L_locals[0].device):
+        _bind_stream(L_locals[0].device)
+        return _check("stan_cl_dist_sim_cholesky_adjoint", load().stan_cl_dist_sim_cholesky_adjoint(
+            n, G, ctypes.cast(_ptr_array(L_locals), ctypes.c_void_p),
+            ctypes.cast(_ptr_array(W_locals), ctypes.c_void_p), ld))
+
+
+def dist_init_from_torch(group=None) -> None:
+    """NCCL communicator for the library from an initialised torch.distributed group:
+    rank 0 creates the id, torch ships it, every rank joins (P = 1, Q = world)."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    try:
+        import nvidia.nccl
+        libdir = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
+        os.environ.setdefault("STAN_CL_NCCL_LIB", libdir)
+    except Exception:
+        pass
+    buf = (ctypes.c_char * 128)()
+    if rank == 0:
+        _check("stan_cl_dist_get_unique_id", load().stan_cl_dist_get_unique_id(ctypes.cast(buf, ctypes.c_void_p)))
+    obj = [bytes(buf)]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    idb = (ctypes.c_char * 128).from_buffer_copy(obj[0])
+    _check("stan_cl_dist_init", load().stan_cl_dist_init(world, rank, ctypes.cast(idb, ctypes.c_void_p), 1, world))
+
+
+def dist_cholesky(A_local: torch.Tensor, n: int) -> int:
+    with torch.cuda.device(A_local.device):
+        _bind_stream(A_local.device)
+        return _check("stan_cl_dist_cholesky",
+                      load().stan_cl_dist_cholesky(n, 0, A_local.data_ptr(), A_local.stride(0)))
+
+
+def dist_cholesky_adjoint(L_local: torch.Tensor, W_local: torch.Tensor, n: int) -> int:
+    with torch.cuda.device(L_local.device):
+        _bind_stream(L_local.device)
+        return _check("stan_cl_dist_cholesky_adjoint", load().stan_cl_dist_cholesky_adjoint(
+            n, 0, L_local.data_ptr(), W_local.data_ptr(), L_local.stride(0)))
 
 
 def kernel_launches() -> int:

@@ -25,6 +25,24 @@ NVCC_FLAGS = [
 ]
 
 
+def _nccl_include():
+    try:
+        import nvidia.nccl
+        for base in list(getattr(nvidia.nccl, "__path__", [])):
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except Exception:
+        pass
+    for inc in ("/usr/include", "/usr/local/include"):
+        if os.path.exists(os.path.join(inc, "nccl.h")):
+            return inc
+    raise RuntimeError("nccl.h not found (pip package nvidia-nccl-cu12 or a system NCCL)")
+
+
+NVCC_FLAGS += ["-I", _nccl_include(), "-ldl"]
+
+
 def sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 

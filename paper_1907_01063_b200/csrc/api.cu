@@ -11,6 +11,9 @@
 //                                          -> A_bar_pad = [[A_bar, 0], [0, 0]]
 // (the padded problems decouple), so no kernel needs ragged-edge
 // code.
+#include <dlfcn.h>
+#include <nccl.h>
+
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -819,5 +822,309 @@ int stan_cl_finalize(void) {
 }
 
 int stan_cl_version(void) { return 100; }
+
+}  // extern "C"
+
+// ============================================================ multi-GPU layer
+// Distributed factorisation and adjoint over G ranks (one process per GPU),
+// block-cyclic by 256-wide block COLUMNS (process grid P = 1, Q = G): block
+// column J lives on rank J % G as local block column J / G of a row-major
+// n x (ncols_local) array.  This is the 2-D block-cyclic layout of
+// SURVEY.md §8(e) with P = 1: for FP64 on NVSwitch the traffic it needs (every
+// rank receives each factored panel once, ~4 n^2 bytes per call) is < 3% of the
+// compute time at n = 65536, and both sweeps then need only BROADCASTS:
+//   forward step k:  owner(k) factors its panel (POTRF + TRSM) -> broadcast the
+//                    panel -> every rank updates its own block columns J > k
+//   adjoint step k:  owner(j) forms C_bar D^-1 -> broadcast -> every rank updates
+//                    its B_bar columns and contracts its own [B C] columns (the
+//                    long K = m dimension is local, so no reduction) -> owner
+//                    runs the symbolic diagonal step -> broadcast sym(S) ->
+//                    every rank updates its R_bar columns.
+// The same code drives (a) NCCL over NVLink (one local rank per process) and
+// (b) a single-process simulation of G ranks on one device (broadcast = device
+// copies), which is what the tests exercise on a one-GPU box.
+namespace {
+
+constexpr int64_t DB = 2 * NB;  // distributed block (column panel width)
+
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* env = getenv("STAN_CL_NCCL_LIB");
+    const char* names[] = {env, "libnccl.so.2", "libnccl.so"};
+    for (const char* nm : names) {
+      if (!nm) continue;
+      h = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
+    commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    broadcast = (decltype(broadcast))dlsym(h, "ncclBroadcast");
+    allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
+    commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    return getUniqueId && commInitRank && broadcast && allReduce && commDestroy;
+  }
+};
+NcclApi g_nccl;
+
+struct DistState {
+  ncclComm_t comm = nullptr;
+  int G = 0, rank = -1;
+};
+DistState g_dist;
+
+// ranks handled by this process: one (NCCL) or all G (simulation)
+struct Rank {
+  int q;                 // global rank
+  const double* L;       // local factor (adjoint) -- or nullptr
+  double* W;             // local working matrix
+  int64_t ld;
+  double* pbuf;          // broadcast landing buffer (n x DB)
+  double* aux;           // per-rank scratch: D^-1 blocks (adjoint), split-K partials ...
+  int* status;
+};
+
+int64_t owned_blocks(int64_t T, int G, int q) { return q < T ? (T - q + G - 1) / G : 0; }
+// number of block columns J < jb owned by rank q (they are local blocks 0 .. cnt-1)
+int64_t owned_below(int64_t jb, int G, int q) { return q < jb ? (jb - q + G - 1) / G : 0; }
+
+struct Bcast {
+  bool sim;
+  // broadcast `count` doubles from ranks[root].buf to every rank's buf (same offset)
+  int operator()(std::vector<Rank>& ranks, int root, double* Rank::*member, size_t count, cudaStream_t st) {
+    if (sim) {
+      const double* src = ranks[root].*member;
+      for (auto& r : ranks)
+        if (r.q != root) CK(cudaMemcpyAsync(r.*member, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      return STAN_CL_OK;
+    }
+    Rank& me = ranks[0];
+    if (g_nccl.broadcast(me.*member, me.*member, count, ncclFloat64, root, g_dist.comm, st) != ncclSuccess)
+      return STAN_CL_ENCCL;
+    return STAN_CL_OK;
+  }
+};
+
+// local view of rank r for global block column J (owned by r): pointer such
+// that v + row * ld + J*DB addresses element (row, J*DB) of the global matrix
+inline double* col_view(double* base, int64_t J, int G) { return base + (J / G) * DB - J * DB; }
+inline const double* col_view(const double* base, int64_t J, int G) { return base + (J / G) * DB - J * DB; }
+
+int dist_factor(std::vector<Rank>& ranks, int G, int64_t n, Bcast& bcast) {
+  cudaStream_t st = g.stream;
+  const int64_t T = n / DB;
+  for (int64_t k = 0; k < T; ++k) {
+    const int o = (int)(k % G);
+    const int64_t c0 = k * DB, m = n - c0;
+    for (auto& r : ranks) {
+      if (r.q != o) continue;
+      double* Wv = col_view(r.W, k, G);
+      int rc = panel(Wv, r.ld, c0, n, DB, r.status, st);  // L11 = chol(A11); L21 = A21 L11^-T
+      if (rc) return rc;
+      CK(copy_block(Wv + c0 * r.ld + c0, r.ld, r.pbuf, DB, m, DB, st));  // rows c0..n of the panel
+    }
+    int rc = bcast(ranks, o, &Rank::pbuf, (size_t)m * DB, st);
+    if (rc) return rc;
+    for (auto& r : ranks) {  // trailing update of the rank's own block columns J > k
+      for (int64_t J = k + 1 + ((r.q - (k + 1)) % G + G) % G; J < T; J += G) {
+        const double* P = r.pbuf + (J * DB - c0) * DB;  // panel rows J*DB..n
+        double* C = col_view(r.W, J, G) + J * DB * r.ld + J * DB;
+        CK(gemm_full(true, true, (int)(n - J * DB), (int)DB, (int)DB, -1.0, 1, P, DB, P, DB, C, r.ld, r.status, st,
+                     /*lower_only=*/1, PROF_SYRK));
+      }
+    }
+  }
+  for (auto& r : ranks) {  // strict upper of the local diagonal tiles
+    for (int64_t J = r.q; J < T; J += G) CK(zero_tile_upper(col_view(r.W, J, G), r.ld, J * DB, (int)DB, st));
+  }
+  return STAN_CL_OK;
+}
+
+int dist_adjoint(std::vector<Rank>& ranks, int G, int64_t n, Bcast& bcast) {
+  cudaStream_t st = g.stream;
+  const int64_t T = n / DB;
+  // per-rank aux layout: D^-1 of the owned blocks | Ctmp (n x DB) | Ssym | T1..T3 | split-K partials
+  auto dinv = [&](Rank& r, int64_t J) { return r.aux + (J / G) * DB * DB; };
+  const int64_t nb_own_max = (T + G - 1) / G;
+  auto tmp = [&](Rank& r, int i) { return r.aux + nb_own_max * DB * DB + (int64_t)i * DB * DB; };  // 0..3
+  auto part = [&](Rank& r) { return r.aux + nb_own_max * DB * DB + 4 * DB * DB; };
+  for (auto& r : ranks) {
+    for (int64_t J = r.q; J < T; J += G) {
+      // block_inverses addresses block J at Dinv + J*DB*DB: shift so it lands at dinv(r, J)
+      int rc = block_inverses(col_view(r.L, J, G), r.ld, DB, J, 1, dinv(r, J) - J * DB * DB, tmp(r, 0), r.status, st);
+      if (rc) return rc;
+    }
+  }
+  for (int64_t k = n; k > 0; k -= DB) {
+    const int64_t j = k - DB, m = n - k, jb = j / DB;
+    const int o = (int)(jb % G);
+    if (m > 0) {
+      for (auto& r : ranks) {  // C_adj = C_adj D^-1 (owner), into pbuf; written back to A_bar
+        if (r.q != o) continue;
+        double* Cb = col_view(r.W, jb, G) + k * r.ld + j;
+        CK(gemm_full(true, false, (int)m, (int)DB, (int)DB, 1.0, 0, Cb, r.ld, dinv(r, jb), DB, r.pbuf, DB, r.status,
+                     st, 0, PROF_TRMM));
+        CK(copy_block(r.pbuf, DB, Cb, r.ld, m, DB, st));
+      }
+      int rc = bcast(ranks, o, &Rank::pbuf, (size_t)m * DB, st);
+      if (rc) return rc;
+      for (auto& r : ranks) {
+        const int64_t nlt = owned_below(jb, G, r.q);          // local blocks with J < jb
+        const int64_t nle = nlt + (r.q == o ? 1 : 0);          // ... and J == jb
+        if (nlt > 0)  // B_adj -= C_adj R  on the rank's own columns
+          CK(gemm_full(true, false, (int)m, (int)(nlt * DB), (int)DB, -1.0, 1, r.pbuf, DB, r.L + j * r.ld, r.ld,
+                       r.W + k * r.ld, r.ld, r.status, st));
+        if (nle > 0) {  // [R_adj D_adj] -= C_adj^T [B C], K = m local
+          int splits, kps;
+          splitk_choice(m, nle * DB, DB, &splits, &kps);
+          CK(gemm_splitk_tn((int)DB, (int)(nle * DB), (int)m, splits, kps, r.pbuf, DB, r.L + k * r.ld, r.ld,
+                            part(r), r.status, st));
+          CK(splitk_reduce_sub(part(r), splits, (int)DB, (int)(nle * DB), r.W + j * r.ld, r.ld, r.status, st));
+        }
+      }
+    }
+    for (auto& r : ranks) {  // symbolic diagonal step on the owner
+      if (r.q != o) continue;
+      const double* D = col_view(r.L, jb, G) + j * r.ld + j;
+      double* Dbar = col_view(r.W, jb, G) + j * r.ld + j;
+      const double* Di = dinv(r, jb);
+      CK(gemm_small((int)DB, true, true, false, D, r.ld, Dbar, r.ld, tmp(r, 1), DB, r.status, st));
+      CK(gemm_small((int)DB, true, false, true, Di, DB, tmp(r, 1), DB, tmp(r, 2), DB, r.status, st));
+      CK(gemm_small((int)DB, false, false, false, tmp(r, 2), DB, Di, DB, tmp(r, 3), DB, r.status, st));
+      CK(phi_sym(tmp(r, 3), r.pbuf, Dbar, r.ld, r.status, st, (int)DB));  // sym(S) -> pbuf
+    }
+    int rc = bcast(ranks, o, &Rank::pbuf, (size_t)DB * DB, st);
+    if (rc) return rc;
+    for (auto& r : ranks) {  // R_adj -= sym(S) R on the rank's own columns
+      const int64_t nlt = owned_below(jb, G, r.q);
+      if (nlt > 0)
+        CK(gemm_full(true, false, (int)DB, (int)(nlt * DB), (int)DB, -1.0, 1, r.pbuf, DB, r.L + j * r.ld, r.ld,
+                     r.W + j * r.ld, r.ld, r.status, st));
+    }
+  }
+  return STAN_CL_OK;
+}
+
+// per-rank device scratch for a problem of order n over G ranks
+size_t dist_aux_doubles(int64_t n, int G) {
+  const int64_t T = n / DB, own = (T + G - 1) / G;
+  int64_t part = 0;
+  for (int64_t k = n; k > 0; k -= DB) {
+    const int64_t m = n - k;
+    if (!m) continue;
+    int s, kps;
+    splitk_choice(m, own * DB, DB, &s, &kps);
+    part = std::max(part, (int64_t)s * DB * own * DB);
+  }
+  return (size_t)(own * DB * DB + 4 * DB * DB + part);
+}
+
+int dist_run(bool adjoint, int64_t n, int G, int nloc, int q0, const double* const* Ls, double* const* Ws,
+             int64_t ld, bool sim) {
+  if (n <= 0 || n % DB != 0 || G < 1 || ld < 1) return n == 0 ? STAN_CL_OK : STAN_CL_EINVAL;
+  const int64_t T = n / DB;
+  const size_t aux = adjoint ? dist_aux_doubles(n, G) : 0;
+  const size_t per = (size_t)n * DB + aux;  // pbuf + aux
+  double* buf = nullptr;
+  int rc = ensure_mat(0, per * nloc * sizeof(double), &buf);
+  if (rc) return rc;
+  rc = ensure_ws(al(sizeof(int) * 64) + NB * NB * sizeof(double));
+  if (rc) return rc;
+  int* status = (int*)g.ws;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), g.stream));
+  std::vector<Rank> ranks;
+  for (int i = 0; i < nloc; ++i) {
+    const int q = q0 + i;
+    if (ld < owned_blocks(T, G, q) * DB) return STAN_CL_EINVAL;
+    ranks.push_back(Rank{q, adjoint ? Ls[i] : nullptr, Ws[i], ld, buf + i * per, buf + i * per + n * DB, status});
+  }
+  if (adjoint) {  // A_bar <- tril(L_bar), locally: strict upper of the local diagonal tiles
+    for (auto& r : ranks)
+      for (int64_t J = r.q; J < T; J += G) CK(zero_tile_upper(col_view(r.W, J, G), r.ld, J * DB, (int)DB, g.stream));
+  }
+  Bcast bc{sim};
+  return adjoint ? dist_adjoint(ranks, G, n, bc) : dist_factor(ranks, G, n, bc);
+}
+
+}  // namespace
+
+extern "C" {
+
+int stan_cl_dist_get_unique_id(void* out128) {
+  if (!out128) return STAN_CL_EINVAL;
+  if (!g_nccl.load()) return STAN_CL_ENCCL;
+  ncclUniqueId id;
+  if (g_nccl.getUniqueId(&id) != ncclSuccess) return STAN_CL_ENCCL;
+  memcpy(out128, &id, sizeof(id));
+  return STAN_CL_OK;
+}
+
+int stan_cl_dist_init(int nranks, int rank, const void* id128, int P, int Q) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !id128 || P != 1 || Q != nranks) return STAN_CL_EINVAL;
+  if (!g_nccl.load()) return STAN_CL_ENCCL;
+  if (g_dist.comm) return STAN_CL_EINVAL;
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof(id));
+  if (g_nccl.commInitRank(&g_dist.comm, nranks, id, rank) != ncclSuccess) {
+    g_dist.comm = nullptr;
+    return STAN_CL_ENCCL;
+  }
+  g_dist.G = nranks;
+  g_dist.rank = rank;
+  return STAN_CL_OK;
+}
+
+static int dist_status_allreduce(int rc) {
+  if (rc) return rc;
+  // the first failing row anywhere (status words are 0 or row+1; max is fine for
+  // the "did anything fail" question, the owner's value is the row)
+  int* status = (int*)g.ws;
+  if (g_nccl.allReduce(status, status, 1, ncclInt32, ncclMax, g_dist.comm, g.stream) != ncclSuccess)
+    return STAN_CL_ENCCL;
+  return read_status();
+}
+
+int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local) {
+  if (!g_dist.comm || (nb != 0 && nb != (int)DB)) return STAN_CL_EINVAL;
+  double* Ws[1] = {A_local};
+  int rc = dist_run(false, n, g_dist.G, 1, g_dist.rank, nullptr, Ws, ld_local, false);
+  return n == 0 ? rc : dist_status_allreduce(rc);
+}
+
+int stan_cl_dist_cholesky_adjoint(int64_t n, int nb, const double* L_local, double* Lbar_to_Abar_local,
+                                  int64_t ld_local) {
+  if (!g_dist.comm || (nb != 0 && nb != (int)DB)) return STAN_CL_EINVAL;
+  const double* Ls[1] = {L_local};
+  double* Ws[1] = {Lbar_to_Abar_local};
+  int rc = dist_run(true, n, g_dist.G, 1, g_dist.rank, Ls, Ws, ld_local, false);
+  return n == 0 ? rc : dist_status_allreduce(rc);
+}
+
+int stan_cl_dist_finalize(void) {
+  if (g_dist.comm) g_nccl.commDestroy(g_dist.comm);
+  g_dist = DistState{};
+  return STAN_CL_OK;
+}
+
+int stan_cl_dist_sim_cholesky(int64_t n, int G, double* const* A_locals, int64_t ld_local) {
+  if (!A_locals || G < 1) return STAN_CL_EINVAL;
+  int rc = dist_run(false, n, G, G, 0, nullptr, A_locals, ld_local, true);
+  return (rc || n == 0) ? rc : read_status();
+}
+
+int stan_cl_dist_sim_cholesky_adjoint(int64_t n, int G, const double* const* L_locals, double* const* W_locals,
+                                      int64_t ld_local) {
+  if (!L_locals || !W_locals || G < 1) return STAN_CL_EINVAL;
+  int rc = dist_run(true, n, G, G, 0, L_locals, W_locals, ld_local, true);
+  return (rc || n == 0) ? rc : read_status();
+}
 
 }  // extern "C"

@@ -1,0 +1,150 @@
+"""Multi-GPU path (block-cyclic by 256-wide block columns).
+
+On a one-GPU box the distributed algorithms run with G simulated ranks in one
+process (stan_cl_dist_sim_*: the same code, broadcasts become device copies)
+and are checked against the oracle and the integer-exact families.  The NCCL
+transport itself is exercised by test_nccl_ranks when >= 2 GPUs are visible.
+"""
+from __future__ import annotations
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_1907_01063_b200 import inputs
+
+pytestmark = pytest.mark.gpu
+B = 256
+
+
+@pytest.fixture(scope="module")
+def sc():
+    import paper_1907_01063_b200 as m
+    m.load()
+    return m
+
+
+def se(n, seed=inputs.X_SEED, jitter=1e-6):
+    return oracle.se_cov(inputs.gp_x(n, seed), 1.0, 1.0, jitter)
+
+
+def relf(a, b):
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def scatter_padded(sc, A: np.ndarray, G: int):
+    n = A.shape[0]
+    At = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    width = max(sc.dist_owned_blocks(n, G, q) for q in range(G)) * B
+    outs = []
+    for q in range(G):
+        loc = sc.dist_scatter(At, G, q)
+        pad = torch.zeros((n, width), dtype=torch.float64, device="cuda")
+        pad[:, :loc.shape[1]] = loc
+        outs.append(pad.contiguous())
+    return outs
+
+
+def check_lower_and_tiles(got: np.ndarray, want: np.ndarray, tol: float):
+    n = want.shape[0]
+    lo = np.tril_indices(n)
+    assert relf(got[lo], want[lo]) <= tol
+    i, j = np.triu_indices(n, 1)
+    in_tile = (i // B) == (j // B)
+    assert np.all(got[i[in_tile], j[in_tile]] == 0.0)
+
+
+@pytest.mark.parametrize("n,G", [(256, 1), (768, 2), (1024, 3), (1536, 4), (1024, 4)])
+def test_dist_sim_cholesky(sc, n, G):
+    K = se(n)
+    locs = scatter_padded(sc, K, G)
+    assert sc.dist_sim_cholesky(locs, n) == 0
+    got = sc.dist_gather(locs, n).cpu().numpy()
+    check_lower_and_tiles(got, oracle.cholesky(K), 1e-11)
+    # integer-exact family: bit-for-bit
+    L0 = inputs.unit_lower_pm1(n, seed=n + G)
+    locs = scatter_padded(sc, inputs.gram_exact(L0), G)
+    assert sc.dist_sim_cholesky(locs, n) == 0
+    got = sc.dist_gather(locs, n).cpu().numpy()
+    assert np.array_equal(np.tril(got), L0)
+
+
+@pytest.mark.parametrize("n,G", [(256, 1), (768, 2), (1024, 3), (1536, 4)])
+def test_dist_sim_adjoint(sc, n, G):
+    L = oracle.cholesky(se(n))
+    W = inputs.lbar(n)
+    Ls = scatter_padded(sc, L, G)
+    Ws = scatter_padded(sc, W, G)
+    assert sc.dist_sim_cholesky_adjoint(Ls, Ws, n) == 0
+    got = sc.dist_gather(Ws, n).cpu().numpy()
+    check_lower_and_tiles(got, oracle.cholesky_adjoint(L, W), 1e-9)
+    Li = inputs.unit_lower_pm1(n, seed=3, band=2)
+    Wi = inputs.int_lbar(n, seed=4)
+    Ls = scatter_padded(sc, Li, G)
+    Ws = scatter_padded(sc, Wi, G)
+    assert sc.dist_sim_cholesky_adjoint(Ls, Ws, n) == 0
+    assert np.array_equal(np.tril(sc.dist_gather(Ws, n).cpu().numpy()), oracle.cholesky_adjoint(Li, Wi))
+
+
+def test_dist_not_pd_and_errors(sc):
+    n, G = 768, 2
+    A = inputs.toeplitz(n)
+    A[600, 600] = -1e12
+    locs = scatter_padded(sc, A, G)
+    assert sc.dist_sim_cholesky(locs, n) == 601
+    lib = sc.load()
+    t = torch.zeros(300, 512, dtype=torch.float64, device="cuda")
+    assert lib.stan_cl_dist_cholesky(300, 0, t.data_ptr(), 512) == -1      # no communicator
+    assert lib.stan_cl_dist_init(2, 0, None, 1, 2) == -1                    # no id
+    assert lib.stan_cl_dist_init(2, 0, t.data_ptr(), 2, 1) == -1            # P != 1
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _nccl_worker(rank, world, port, n, q):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    import paper_1907_01063_b200 as sc
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    try:
+        sc.dist_init_from_torch()
+        K = torch.from_numpy(se(n)).cuda()
+        loc = sc.dist_scatter(K, world, rank).contiguous()
+        rc = sc.dist_cholesky(loc, n)
+        gathered = [None] * world
+        dist.all_gather_object(gathered, loc.cpu())
+        q.put((rank, rc, [g.numpy() for g in gathered] if rank == 0 else None))
+    finally:
+        sc.load().stan_cl_dist_finalize()
+        dist.destroy_process_group()
+
+
+@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
+def test_nccl_ranks(sc):
+    import torch.multiprocessing as mp
+    world, n = 2, 1024
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_nccl_worker, args=(r, world, port, n, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict((r, (rc, g)) for r, rc, g in [q.get(timeout=300) for _ in range(world)])
+    for p in ps:
+        p.join(timeout=60)
+    assert all(rc == 0 for rc, _ in res.values())
+    got = sc.dist_gather([torch.from_numpy(g) for g in res[0][1]], n).numpy()
+    check_lower_and_tiles(got, oracle.cholesky(se(n)), 1e-11)
