@@ -44,7 +44,7 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
                0x100: "display_clock_setting"}
 
 
-def config(n: int, world: int) -> dict:
+def config(n: int, world: int, mode: str = "single") -> dict:
     return {
         "workload": f"SE-kernel GP covariance n={n} (1-D x~U(-10,10), alpha=rho=1, jitter 1e-6): "
                     "SE build + Cholesky + adjoint (BASELINE.json configs[3])",
@@ -52,7 +52,10 @@ def config(n: int, world: int) -> dict:
         "flops_per_step": n ** 3,
         "flop_convention": "n^3/3 (Cholesky) + 2n^3/3 (adjoint)",
         "l2": "inputs exceed L2 (one n x n FP64 matrix = %.1f GiB vs 126 MB L2); no flush needed" % (8 * n * n / 2 ** 30),
-        "parallelism": "replicas" if world > 1 else "single",
+        "parallelism": {"single": "single GPU",
+                        "replicas": f"replicas: {world} independent problems, one per GPU",
+                        "dist": f"block-cyclic 256-wide block columns over {world} GPUs (P=1, Q={world}), "
+                                "NCCL broadcasts of panels / C_bar D^-1 / sym(S)"}[mode],
     }
 
 
@@ -186,6 +189,20 @@ def bench_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
+def setup_dist(sc, world: int, local_rank: int) -> bool:
+    """NCCL communicator of the library; every rank must succeed, else replicas."""
+    import torch
+    ok = 1
+    try:
+        sc.dist_init_from_torch()
+    except Exception as e:  # noqa: BLE001
+        print(f"[bench] dist init failed on this rank: {e}", file=sys.stderr, flush=True)
+        ok = 0
+    t = torch.tensor([ok], dtype=torch.int32, device=torch.device("cuda", local_rank))
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MIN)
+    return bool(t.item())
+
+
 def bench_ours(args, rank: int, world: int, local_rank: int):
     import numpy as np
     import torch
@@ -196,16 +213,53 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.set_device(dev)
     n = args.n
     sc.load()
-    xs, ls = replica_seeds(rank)
-    x = torch.from_numpy(inputs.gp_x(n, seed=xs)).to(dev)
-    Lbar = torch.from_numpy(inputs.lbar(n, seed=ls)).to(dev)
-    K = torch.empty((n, n), dtype=torch.float64, device=dev)
-    Abar = torch.empty_like(K)
+    mode = "single"
+    if world > 1:
+        mode = "replicas"
+        if args.mode in ("auto", "dist") and n % sc.DIST_BLOCK == 0 and setup_dist(sc, world, local_rank):
+            mode = "dist"
+    e2e_fn = None
+    if mode == "dist":
+        # one problem of order n, block columns cyclic over the ranks (strong scaling)
+        x = torch.from_numpy(inputs.gp_x(n)).to(dev)
+        w = sc.dist_owned_blocks(n, world, rank) * sc.DIST_BLOCK
+        Lbar_loc = sc.dist_scatter(torch.from_numpy(inputs.lbar(n)), world, rank).contiguous().to(dev)
+        K_loc = torch.empty((n, w), dtype=torch.float64, device=dev)
+        W_loc = torch.empty_like(K_loc)
 
-    def step():
-        sc.gp_exp_quad_cov(x, ALPHA, RHO, JITTER, out=K)      # F0
-        sc.cholesky(K, out=K)                                 # F1-F4 (in place)
-        sc.cholesky_adjoint(K, Lbar, out=Abar)                # R0-R5
+        def step():
+            sc.gp_exp_quad_cov_cols(x, K_loc, world, rank, ALPHA, RHO, JITTER)   # F0 (owned columns)
+            sc.dist_cholesky(K_loc, n)                                          # F1-F4, NCCL panel broadcasts
+            W_loc.copy_(Lbar_loc)
+            sc.dist_cholesky_adjoint(K_loc, W_loc, n)                           # R0-R5, NCCL broadcasts
+
+        Kh = torch.empty((n, w), dtype=torch.float64).pin_memory()
+        Lbh = Lbar_loc.cpu().pin_memory()
+        Lh = torch.empty_like(Kh).pin_memory()
+        Abh = torch.empty_like(Kh).pin_memory()
+        sc.gp_exp_quad_cov_cols(x, K_loc, world, rank, ALPHA, RHO, JITTER)
+        Kh.copy_(K_loc)
+
+        def e2e_fn():
+            K_loc.copy_(Kh, non_blocking=True)
+            sc.dist_cholesky(K_loc, n)
+            Lh.copy_(K_loc, non_blocking=True)
+            W_loc.copy_(Lbh, non_blocking=True)
+            sc.dist_cholesky_adjoint(K_loc, W_loc, n)
+            Abh.copy_(W_loc, non_blocking=True)
+        e2e_bytes = (2 * 8 * n * w, 2 * 8 * n * w)
+        e2e_path = "per rank: pinned H2D of its K and L_bar block columns, dist_cholesky + dist_cholesky_adjoint, D2H of L and A_bar"
+    else:
+        xs, ls = replica_seeds(rank)
+        x = torch.from_numpy(inputs.gp_x(n, seed=xs)).to(dev)
+        Lbar = torch.from_numpy(inputs.lbar(n, seed=ls)).to(dev)
+        K = torch.empty((n, n), dtype=torch.float64, device=dev)
+        Abar = torch.empty_like(K)
+
+        def step():
+            sc.gp_exp_quad_cov(x, ALPHA, RHO, JITTER, out=K)      # F0
+            sc.cholesky(K, out=K)                                 # F1-F4 (in place)
+            sc.cholesky_adjoint(K, Lbar, out=Abar)                # R0-R5
 
     def barrier():
         if world > 1:
@@ -244,7 +298,8 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
     barrier()
     ms_max = max_over_ranks(e0.elapsed_time(e1) / args.steps, world, dev)
     flops = float(n) ** 3
-    value = world * flops / (ms_max / 1e3) / 1e9
+    jobs = world if mode == "replicas" else 1                  # dist: one problem over all ranks
+    value = jobs * flops / (ms_max / 1e3) / 1e9
     clocks = sampler.summary()
 
     # roofline of the dominant kernel class: algorithmic flops / event-timed duration
@@ -266,7 +321,22 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
 
     # end-to-end through the public host-buffer API (pinned host in/out)
     e2e = None
-    if args.e2e_steps > 0:
+    if args.e2e_steps > 0 and e2e_fn is not None:
+        e2e_fn()
+        torch.cuda.synchronize()
+        barrier()
+        f0 = torch.cuda.Event(enable_timing=True)
+        f1 = torch.cuda.Event(enable_timing=True)
+        f0.record()
+        for _ in range(args.e2e_steps):
+            e2e_fn()
+        f1.record()
+        torch.cuda.synchronize()
+        ems = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps, world, dev)
+        e2e = {"value": flops / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
+               "h2d_bytes_per_step": int(e2e_bytes[0]) * world, "d2h_bytes_per_step": int(e2e_bytes[1]) * world,
+               "path": e2e_path}
+    elif args.e2e_steps > 0:
         Kh = torch.empty((n, n), dtype=torch.float64).pin_memory()
         sc.gp_exp_quad_cov(x, ALPHA, RHO, JITTER, out=K)
         Kh.copy_(K)
@@ -291,7 +361,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
         f1.record()
         torch.cuda.synchronize()
         ems = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps, world, dev)
-        e2e = {"value": world * flops / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
+        e2e = {"value": jobs * flops / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": 3 * 8 * n * n, "d2h_bytes_per_step": 2 * 8 * n * n,
                "path": "stan_cl_cholesky_host(K) + stan_cl_cholesky_adjoint_host(L, L_bar), pinned host buffers"}
         del Kh, Lh, Lbh, Abh
@@ -301,10 +371,11 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
     cpu = None if args.no_cpu_baseline else cpu_baseline_entry(args.oracle_n)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": "strong" if mode == "dist" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config(n, world),
-        "fp64_peak_frac": (flops / (ms_max / 1e3) / 1e12) / FP64_PEAK_TFLOPS,
+        "config": config(n, world, mode),
+        "fp64_peak_frac": (jobs * flops / (ms_max / 1e3) / 1e12) / (FP64_PEAK_TFLOPS * world),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks,
         "kernel_classes_warmup_step": classes,
@@ -322,6 +393,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--oracle-n", type=int, default=ORACLE_SAMPLE_N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", choices=["auto", "dist", "replicas"], default="auto",
+                    help="N>1: distributed (strong scaling, default) or independent replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -340,6 +413,11 @@ def main():
     finally:
         if world > 1:
             import torch
+            try:
+                import paper_1907_01063_b200 as sc
+                sc.load().stan_cl_dist_finalize()
+            except Exception:  # noqa: BLE001
+                pass
             torch.distributed.destroy_process_group()
 
 

@@ -137,6 +137,9 @@ int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local);
 int stan_cl_dist_cholesky_adjoint(int64_t n, int nb, const double* L_local, double* Lbar_to_Abar_local,
                                   int64_t ld_local);
 int stan_cl_dist_finalize(void);
+/* the SE covariance's owned block columns for rank q of G (the layout above) */
+int stan_cl_gp_exp_quad_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter,
+                                 double* K_local, int64_t ld_local, int G, int q);
 /* The same distributed algorithms with G simulated ranks in this process on
  * the current device (broadcasts become device copies): the layouts above,
  * one local array per rank.  For testing the multi-GPU path on one GPU. */

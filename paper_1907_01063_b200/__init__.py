@@ -63,6 +63,7 @@ SIGNATURES = {
     "stan_cl_dist_cholesky_adjoint": (_I, [_I64, _I, _P, _P, _I64]),
     "stan_cl_dist_finalize": (_I, []),
     "stan_cl_dist_sim_cholesky": (_I, [_I64, _I, _P, _I64]),
+    "stan_cl_gp_exp_quad_cov_cols": (_I, [_I64, _P, _D, _D, _D, _P, _I64, _I, _I]),
     "stan_cl_dist_sim_cholesky_adjoint": (_I, [_I64, _I, _P, _P, _I64]),
     "stan_cl_version": (_I, []),
 }
@@ -280,6 +281,17 @@ def dist_init_from_torch(group=None) -> None:
     dist.broadcast_object_list(obj, src=0, group=group)
     idb = (ctypes.c_char * 128).from_buffer_copy(obj[0])
     _check("stan_cl_dist_init", load().stan_cl_dist_init(world, rank, ctypes.cast(idb, ctypes.c_void_p), 1, world))
+
+
+def gp_exp_quad_cov_cols(x: torch.Tensor, K_local: torch.Tensor, G: int, q: int, alpha: float = 1.0,
+                         rho: float = 1.0, jitter: float = 0.0) -> torch.Tensor:
+    """Rank q's owned block columns of the SE covariance, into K_local (n x ld)."""
+    n = x.shape[0]
+    with torch.cuda.device(x.device):
+        _bind_stream(x.device)
+        _check("stan_cl_gp_exp_quad_cov_cols", load().stan_cl_gp_exp_quad_cov_cols(
+            n, x.data_ptr(), float(alpha), float(rho), float(jitter), K_local.data_ptr(), K_local.stride(0), G, q))
+    return K_local
 
 
 def dist_cholesky(A_local: torch.Tensor, n: int) -> int:

@@ -1114,6 +1114,17 @@ int stan_cl_dist_finalize(void) {
   return STAN_CL_OK;
 }
 
+int stan_cl_gp_exp_quad_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter,
+                                 double* K_local, int64_t ld_local, int G, int q) {
+  if (n < 0 || G < 1 || q < 0 || q >= G || n % DB != 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!x || !K_local) return STAN_CL_EINVAL;
+  if (!(rho != 0.0) || !(rho - rho == 0.0)) return STAN_CL_EINVAL;
+  if (ld_local < owned_blocks(n / DB, G, q) * DB) return STAN_CL_EINVAL;
+  CK(se_cov_cols(n, x, alpha, rho, jitter, K_local, ld_local, G, q, g.stream));
+  return STAN_CL_OK;
+}
+
 int stan_cl_dist_sim_cholesky(int64_t n, int G, double* const* A_locals, int64_t ld_local) {
   if (!A_locals || G < 1) return STAN_CL_EINVAL;
   int rc = dist_run(false, n, G, G, 0, nullptr, A_locals, ld_local, true);

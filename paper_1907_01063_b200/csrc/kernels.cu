@@ -136,6 +136,35 @@ cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double 
   return cudaGetLastError();
 }
 
+// the owned 256-wide block columns J = q, q+G, ... of K, stored contiguously
+// (local column lc*256 + c  <->  global column (lc*G + q)*256 + c)
+__global__ void se_cov_cols_kernel(int64_t n, const double* __restrict__ x, double sq_alpha,
+                                   double neg_half_inv_rho2, double jitter, double* __restrict__ K,
+                                   int64_t ld, int64_t ncols, int G, int q) {
+  const long long total = (long long)n * ncols;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
+       idx += (long long)gridDim.x * blockDim.x) {
+    const long long i = idx / ncols, lcol = idx - i * ncols;
+    const long long j = ((lcol >> 8) * G + q) * 256 + (lcol & 255);
+    const double d = x[i] - x[j];
+    const double e = __dmul_rn(__dmul_rn(d, d), neg_half_inv_rho2);
+    double v = __dmul_rn(sq_alpha, exp(e));
+    if (i == j) v = __dadd_rn(v, jitter);
+    K[i * ld + lcol] = v;
+  }
+}
+
+cudaError_t se_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
+                        int64_t ld, int G, int q, cudaStream_t st) {
+  const int64_t T = n / 256, own = q < T ? (T - q + G - 1) / G : 0;
+  const int64_t ncols = own * 256;
+  if (n == 0 || ncols == 0) return cudaSuccess;
+  Prof prof_(PROF_SE, 0.0, st, 8.0 * n * ncols + 8.0 * n);
+  se_cov_cols_kernel<<<grid_for((long long)n * ncols, 256), 256, 0, st>>>(n, x, alpha * alpha, -0.5 / (rho * rho),
+                                                                          jitter, K, ld, ncols, G, q);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------- K11
 __global__ void copy_lower_pad_kernel(const double* __restrict__ src, int64_t n, int64_t lds,
                                       double* __restrict__ dst, int64_t N, int64_t ldd,

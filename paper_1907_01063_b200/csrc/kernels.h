@@ -43,6 +43,10 @@ void prof_read(int kind, double* ms, double* flops, long long* count, double* by
 cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
                    cudaStream_t st);
 
+// owned 256-wide block columns of K for rank q of G (block-column-cyclic layout)
+cudaError_t se_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
+                        int64_t ld, int G, int q, cudaStream_t st);
+
 // ---- layout helpers (K11) ----
 // dst[N x N] (ldd) <- lower(src[n x n], lds) with +0.0 strict upper; rows/cols >= n
 // become diag_pad * I (diag_pad = 1 for L/A, 0 for adjoints).  N >= n.

@@ -90,6 +90,17 @@ def test_dist_sim_adjoint(sc, n, G):
     assert np.array_equal(np.tril(sc.dist_gather(Ws, n).cpu().numpy()), oracle.cholesky_adjoint(Li, Wi))
 
 
+@pytest.mark.parametrize("n,G", [(768, 2), (1024, 3)])
+def test_se_cov_cols(sc, n, G):
+    x = torch.from_numpy(inputs.gp_x(n)).cuda()
+    K = sc.gp_exp_quad_cov(x, 1.3, 0.7, 1e-6)
+    for q in range(G):
+        w = sc.dist_owned_blocks(n, G, q) * B
+        loc = torch.empty((n, w), dtype=torch.float64, device="cuda")
+        sc.gp_exp_quad_cov_cols(x, loc, G, q, 1.3, 0.7, 1e-6)
+        assert torch.equal(loc, sc.dist_scatter(K, G, q))
+
+
 def test_dist_not_pd_and_errors(sc):
     n, G = 768, 2
     A = inputs.toeplitz(n)
