@@ -102,6 +102,7 @@ using CfgT = Cfg<128, 64, 4, 2, 4>;  // 8 consumer warps of 32 x 32 + 1 producer
 using CfgT2 = Cfg<128, 64, 4, 2, 3, 2, false>;  // same, 2 CTAs/SM, C straight from global
 using CfgT2P = Cfg<128, 64, 4, 2, 2, 2, true>;  // 2 CTAs/SM, double-buffered ring, C prefetch
 using CfgT32 = Cfg<128, 64, 4, 2, 3, 1, true, 32>;  // 32-deep slabs (two TMA boxes per operand)
+using CfgT128 = Cfg<128, 128, 2, 4, 3, 1, true, 16>;  // 128x128 tiles, 8 consumer warps of 64x32
 
 constexpr int align1k(int b) { return (b + 1023) / 1024 * 1024; }
 // shared slab of ROWS rows/cols and depth BKS: k-major = BKS/16 dense sub-tiles of

@@ -28,6 +28,7 @@ cudaError_t launch(GemmArgs p, int splits) {
   if (g_impl == 2) return launch_tma<tg::CfgT2, AK, BK, MODE>(p, splits, 0);
   if (g_impl == 3) return launch_tma<tg::CfgT2P, AK, BK, MODE>(p, splits, 0);
   if (g_impl == 4) return launch_tma<tg::CfgT32, AK, BK, MODE>(p, splits, 0);
+  if (g_impl == 5) return launch_tma<tg::CfgT128, AK, BK, MODE>(p, splits, 0);
   return launch_gemm<gemm::CfgW8, AK, BK, MODE>(p, splits, 0);
 }
 template <bool AK, bool BK, int MODE>
@@ -46,7 +47,7 @@ double timeit(GemmArgs p, int splits, int reps = 5) {
   if (e != cudaSuccess) printf("ERR %s\n", cudaGetErrorString(e));
   return best;
 }
-const char* NAMES[] = {"w8", "tma", "tma2", "tma2p", "tma32"};
+const char* NAMES[] = {"w8", "tma", "tma2", "tma2p", "tma32", "tma128"};
 
 // run once with impl 0 and impl 1 from the same C0 and compare
 template <bool AK, bool BK, int MODE>
@@ -94,7 +95,7 @@ int main() {
     GemmArgs sk{B, 128, B, 2048, nullptr, 2048, 128, 2048, 4096, 1024, 1.0, 0, 0, nullptr, 0};
     check<false, false, MODE_SPLITK>(sk, 4, C, C1, C2, (size_t)4 * 128 * 2048, d, "splitk_n2048_k4096");
   }
-  for (int impl : {1, 4}) {
+  for (int impl : {0, 4}) {
     g_impl = impl;
     for (int K : {128, 256}) {
       GemmArgs s{A, K, A, K, C, M, M, M, K, K, -1.0, 1, 1, nullptr, 0};
