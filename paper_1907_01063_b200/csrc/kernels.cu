@@ -367,65 +367,73 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
 }
 
 // ----------------------------------------------------------------------- F2
-// X L11^T = A21 by substitution (no explicit inverse, R11), 64 rows
-// per CTA.  Four threads own a row, thread p holding columns p + 4q (q = 0..31)
-// in registers; column j is finished by its owner with an IEEE division and
-// broadcast with a warp shuffle; L11^T is staged in shared memory
-// (LT[j][l] = L11[l][j], broadcast reads).
+// X L11^T = A21 by substitution (no explicit inverse, R11).  The
+// 128-wide panel is solved in two 64-wide halves (L11 = [[La, 0], [Lb, Lc]]):
+//   Xa = Aa La^-T;   Ac -= Xa Lb^T  (DMMA GEMM, K = 64);   Xc = Ac Lc^-T
+// which is the same column-by-column elimination as one 128-wide substitution,
+// with the cross-half updates done on the tensor cores.  Substitution kernel:
+// 64 rows per CTA, four threads own a row, thread p holding columns p + 4q in
+// registers; column j is finished by its owner with an IEEE division and
+// broadcast with a warp shuffle; Lw^T is staged in shared memory
+// (LT[j][l] = Lw[l][j], broadcast reads).
 constexpr int TRSM_ROWS = 64;
-constexpr int TRSM_SMEM = (NB * TP + NB) * (int)sizeof(double);
+constexpr int TRSM_W = 64;
+constexpr int TRSM_TP = TRSM_W + 1;
+constexpr int TRSM_SMEM = (TRSM_W * TRSM_TP + TRSM_W) * (int)sizeof(double);
 
-__global__ void __launch_bounds__(256, 1) trsm_panel_kernel(double* W, int64_t ld, int64_t k0,
+__global__ void __launch_bounds__(256, 2) trsm_panel_kernel(double* W, int64_t ld, int64_t k0,
                                                             int64_t r0, const int* status) {
   if (*status != 0) return;
-  extern __shared__ double sm[];
-  double* LT = sm;
-  double* dg = sm + NB * TP;
+  __shared__ double LT[TRSM_W * TRSM_TP];
+  __shared__ double dg[TRSM_W];
   const int tid = threadIdx.x, lane = tid & 31;
   const double* L11 = W + k0 * ld + k0;
-  for (int idx = tid; idx < NB * NB; idx += 256) {
-    const int l = idx >> 7, j = idx & (NB - 1);
+  for (int idx = tid; idx < TRSM_W * TRSM_W; idx += 256) {
+    const int l = idx / TRSM_W, j = idx % TRSM_W;
     if (j <= l) {
       const double v = L11[(long long)l * ld + j];
-      LT[j * TP + l] = v;
+      LT[j * TRSM_TP + l] = v;
       if (j == l) dg[j] = v;
     }
   }
+  constexpr int Q = TRSM_W / 4;
   const int r = tid >> 2, p = tid & 3;
   const long long row = r0 + (long long)blockIdx.x * TRSM_ROWS + r;
   double* P = W + row * ld + k0;
-  double x[32];
+  double x[Q];
 #pragma unroll
-  for (int q = 0; q < 32; ++q) x[q] = P[p + 4 * q];
+  for (int q = 0; q < Q; ++q) x[q] = P[p + 4 * q];
   __syncthreads();
   const int owner_base = lane & ~3;
 #pragma unroll
-  for (int j = 0; j < NB; ++j) {
+  for (int j = 0; j < TRSM_W; ++j) {
     if (p == (j & 3)) x[j >> 2] = x[j >> 2] / dg[j];
     const double v = __shfl_sync(0xffffffffu, x[j >> 2], owner_base | (j & 3));
-    const double* lt = LT + j * TP;
+    const double* lt = LT + j * TRSM_TP;
 #pragma unroll
-    for (int q = (j >> 2); q < 32; ++q) {
+    for (int q = (j >> 2); q < Q; ++q) {
       if (p + 4 * q > j) x[q] = fma(-v, lt[p + 4 * q], x[q]);
     }
   }
 #pragma unroll
-  for (int q = 0; q < 32; ++q) P[p + 4 * q] = x[q];
+  for (int q = 0; q < Q; ++q) P[p + 4 * q] = x[q];
 }
 
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st, 16.0 * (r1 - r0) * NB + 4.0 * NB * NB);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(trsm_panel_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         TRSM_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
   const int blocks = (int)((r1 - r0) / TRSM_ROWS);
-  trsm_panel_kernel<<<blocks, 256, TRSM_SMEM, st>>>(W, ld, k0, r0, status);
+  trsm_panel_kernel<<<blocks, 256, 0, st>>>(W, ld, k0, r0, status);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // Ac -= Xa Lb^T: A = Xa (rows x 64, k-major), B = Lb (64 x 64, n x k), C = Ac
+  double* Xa = W + r0 * ld + k0;
+  const double* Lb = W + (k0 + TRSM_W) * ld + k0;
+  GemmArgs p{Xa, ld, Lb, ld, Xa + TRSM_W, ld, (int)(r1 - r0), TRSM_W, TRSM_W, TRSM_W, -1.0, 1, 0, status, 0};
+  e = launch_gemm<gemm::CfgW8, true, true, MODE_FULL>(p, 1, st);
+  if (e != cudaSuccess) return e;
+  trsm_panel_kernel<<<blocks, 256, 0, st>>>(W, ld, k0 + TRSM_W, r0, status);
   return cudaGetLastError();
 }
 
