@@ -128,6 +128,16 @@ def traffic_from_profiles(kind: str):
         return None
 
 
+def host_path_bytes(n: int, adj_block: int) -> tuple[int, int]:
+    """Bytes the host entry points move per call pair (include/stan_cl.h):
+    lower-triangle rectangles, rows [r, r+128) x columns [0, r+128) for K (H2D),
+    L (D2H), and L, L_bar (H2D); A_bar ships per adjoint block column, rows
+    [j, n) x columns [j, j+B) (D2H)."""
+    tri = sum(8 * (min(r + 128, n) - r) * min(r + 128, n) for r in range(0, n, 128))
+    cols = sum(8 * (n - j) * (min(j + adj_block, n) - j) for j in range(0, n, adj_block))
+    return 3 * tri, tri + cols
+
+
 def max_over_ranks(value: float, world: int, device=None) -> float:
     """Max of a per-rank scalar over all ranks (timing rule: max over ranks)."""
     if world <= 1:
@@ -361,8 +371,9 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
         f1.record()
         torch.cuda.synchronize()
         ems = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps, world, dev)
+        hb = host_path_bytes(n, 256 if n >= 4096 else 128)
         e2e = {"value": jobs * flops / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
-               "h2d_bytes_per_step": 3 * 8 * n * n, "d2h_bytes_per_step": 2 * 8 * n * n,
+               "h2d_bytes_per_step": hb[0], "d2h_bytes_per_step": hb[1],
                "path": "stan_cl_cholesky_host(K) + stan_cl_cholesky_adjoint_host(L, L_bar), pinned host buffers"}
         del Kh, Lh, Lbh, Abh
 

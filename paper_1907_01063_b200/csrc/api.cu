@@ -413,10 +413,11 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
       CK(copy_block(Ctmp, B, Cb, ld, m, B, st));
     }
     // D_adj = transpose(D) * D_adj; copy_lower_tri_to_upper_tri
-    CK(gemm_small((int)B, true, true, false, D, ld, Dbar, ld, T1, B, status, st));
+    // (only the lower tiles of P = D^T D_adj are formed, stored mirrored)
+    CK(gemm_small((int)B, true, true, false, D, ld, Dbar, ld, T1, B, status, st, 1.0, 1, 0, 0, 0, /*c_sym=*/true));
     // D = transpose(lower_triangular_inverse(D)); D_adj = D * transpose(D * D_adj)
     // computed as S = D^-T sym(P) D^-1
-    CK(gemm_small((int)B, true, false, true, Db, B, T1, B, T2, B, status, st));
+    CK(gemm_small((int)B, true, false, false, Db, B, T1, B, T2, B, status, st));
     CK(gemm_small((int)B, false, false, false, T2, B, Db, B, T3, B, status, st));
     // copy_lower_tri_to_upper_tri; diagonal * 0.5; set_zeros_in_upper_tri
     CK(phi_sym(T3, T4, Dbar, ld, status, st, (int)B));
@@ -996,8 +997,9 @@ int dist_adjoint(std::vector<Rank>& ranks, int G, int64_t n, Bcast& bcast) {
       const double* D = col_view(r.L, jb, G) + j * r.ld + j;
       double* Dbar = col_view(r.W, jb, G) + j * r.ld + j;
       const double* Di = dinv(r, jb);
-      CK(gemm_small((int)DB, true, true, false, D, r.ld, Dbar, r.ld, tmp(r, 1), DB, r.status, st));
-      CK(gemm_small((int)DB, true, false, true, Di, DB, tmp(r, 1), DB, tmp(r, 2), DB, r.status, st));
+      CK(gemm_small((int)DB, true, true, false, D, r.ld, Dbar, r.ld, tmp(r, 1), DB, r.status, st, 1.0, 1, 0, 0, 0,
+                    /*c_sym=*/true));
+      CK(gemm_small((int)DB, true, false, false, Di, DB, tmp(r, 1), DB, tmp(r, 2), DB, r.status, st));
       CK(gemm_small((int)DB, false, false, false, tmp(r, 2), DB, Di, DB, tmp(r, 3), DB, r.status, st));
       CK(phi_sym(tmp(r, 3), r.pbuf, Dbar, r.ld, r.status, st, (int)DB));  // sym(S) -> pbuf
     }

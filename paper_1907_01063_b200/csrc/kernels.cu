@@ -379,7 +379,6 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
 constexpr int TRSM_ROWS = 64;
 constexpr int TRSM_W = 64;
 constexpr int TRSM_TP = TRSM_W + 1;
-constexpr int TRSM_SMEM = (TRSM_W * TRSM_TP + TRSM_W) * (int)sizeof(double);
 
 __global__ void __launch_bounds__(256, 2) trsm_panel_kernel(double* W, int64_t ld, int64_t k0,
                                                             int64_t r0, const int* status) {
@@ -652,7 +651,7 @@ constexpr int G128_SMEM = (32 * G128_AP + NB * G128_BP) * (int)sizeof(double);
 // the lower triangle of A's storage is read; B_SYM: B read as sym(tril(B)).
 // 128 threads per 32 x 32 output tile; K staged through shared memory in
 // 128-deep chunks whose 64 global loads per thread are all issued before use.
-template <int S, bool A_T, bool A_TRIL, bool B_SYM>
+template <int S, bool A_T, bool A_TRIL, bool B_SYM, bool C_SYM>
 __global__ void __launch_bounds__(128) gemmS_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
                                                     const double* __restrict__ B, int64_t ldb, int64_t sB,
                                                     double* __restrict__ C, int64_t ldc, int64_t sC,
@@ -665,6 +664,7 @@ __global__ void __launch_bounds__(128) gemmS_kernel(const double* __restrict__ A
   B += (long long)blockIdx.z * sB;
   C += (long long)blockIdx.z * sC;
   const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  if (C_SYM && m0 < n0) return;  // strictly upper tile: written as the mirror of (n0, m0)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
   double acc[2][2][2] = {};
@@ -711,15 +711,25 @@ __global__ void __launch_bounds__(128) gemmS_kernel(const double* __restrict__ A
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       const int r = m0 + wm * 16 + i * 8 + g, c = n0 + wn * 16 + j * 8 + 2 * t;
-      *reinterpret_cast<double2*>(C + (long long)r * ldc + c) = make_double2(sign * acc[i][j][0], sign * acc[i][j][1]);
+      if (!C_SYM) {
+        *reinterpret_cast<double2*>(C + (long long)r * ldc + c) = make_double2(sign * acc[i][j][0], sign * acc[i][j][1]);
+      } else {  // C = sym(tril(product)): element (r, c), r >= c, also lands at (c, r)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (r >= c + h) {
+            C[(long long)r * ldc + c + h] = sign * acc[i][j][h];
+            C[(long long)(c + h) * ldc + r] = sign * acc[i][j][h];
+          }
+        }
+      }
     }
 }
 
-template <int S, bool A_T, bool A_TRIL, bool B_SYM>
+template <int S, bool A_T, bool A_TRIL, bool B_SYM, bool C_SYM>
 static cudaError_t gemmS_launch(const double* A, int64_t lda, int64_t sA, const double* B, int64_t ldb, int64_t sB,
                                 double* C, int64_t ldc, int64_t sC, double sign, int batch, const int* status,
                                 cudaStream_t st) {
-  auto kern = gemmS_kernel<S, A_T, A_TRIL, B_SYM>;
+  auto kern = gemmS_kernel<S, A_T, A_TRIL, B_SYM, C_SYM>;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, G128_SMEM);
@@ -732,17 +742,17 @@ static cudaError_t gemmS_launch(const double* A, int64_t lda, int64_t sA, const 
 
 cudaError_t gemm_small(int S, bool a_t, bool a_tril, bool b_sym, const double* A, int64_t lda, const double* B,
                        int64_t ldb, double* C, int64_t ldc, const int* status, cudaStream_t st, double sign,
-                       int batch, int64_t sA, int64_t sB, int64_t sC) {
+                       int batch, int64_t sA, int64_t sB, int64_t sC, bool c_sym) {
   Prof prof_(PROF_SMALL, 2.0 * S * S * S * batch, st, 24.0 * S * S * batch);
-#define STANCL_GS(SS, AT, AL, BS)                                                                           \
-  if (S == SS && a_t == AT && a_tril == AL && b_sym == BS)                                                  \
-    return gemmS_launch<SS, AT, AL, BS>(A, lda, sA, B, ldb, sB, C, ldc, sC, sign, batch, status, st);
-  STANCL_GS(128, true, true, false)
-  STANCL_GS(128, true, false, true)
-  STANCL_GS(128, false, false, false)
-  STANCL_GS(256, true, true, false)
-  STANCL_GS(256, true, false, true)
-  STANCL_GS(256, false, false, false)
+#define STANCL_GS(SS, AT, AL, BS, CS)                                                                      \
+  if (S == SS && a_t == AT && a_tril == AL && b_sym == BS && c_sym == CS)                                   \
+    return gemmS_launch<SS, AT, AL, BS, CS>(A, lda, sA, B, ldb, sB, C, ldc, sC, sign, batch, status, st);
+  STANCL_GS(128, true, true, false, true)
+  STANCL_GS(128, true, false, false, false)
+  STANCL_GS(128, false, false, false, false)
+  STANCL_GS(256, true, true, false, true)
+  STANCL_GS(256, true, false, false, false)
+  STANCL_GS(256, false, false, false, false)
 #undef STANCL_GS
   return cudaErrorInvalidValue;
 }

@@ -105,9 +105,12 @@ cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* D
 // `batch` problems with element strides sA/sB/sC.  a_t: A given as K x M;
 // a_tril: only the lower triangle of A's storage is read (upper taken as 0);
 // b_sym: B read as sym(tril(B)) i.e. B[max][min]; B is otherwise K x N.
+// c_sym: only the lower tiles are computed and C = sym(tril(product)) is stored
+// (both triangles), so a consumer reads it as a plain matrix.
 cudaError_t gemm_small(int S, bool a_t, bool a_tril, bool b_sym, const double* A, int64_t lda, const double* B,
                        int64_t ldb, double* C, int64_t ldc, const int* status, cudaStream_t st,
-                       double sign = 1.0, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0);
+                       double sign = 1.0, int batch = 1, int64_t sA = 0, int64_t sB = 0, int64_t sC = 0,
+                       bool c_sym = false);
 // S (n x n, ld n): Ssym = mirror(tril(S)) -> ws; Dbar = Phi(S) = tril(S) with halved diagonal
 cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, const int* status,
                     cudaStream_t st, int n = 128);
