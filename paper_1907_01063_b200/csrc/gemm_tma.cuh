@@ -194,7 +194,11 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
   if (p.status && *p.status != 0) return;
   if ((int)blockIdx.x >= nitems) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* base = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-B aligned slab base (128B-swizzle atoms) as an OFFSET from the shared
+  // array: integer round-tripping the pointer would drop its address space and
+  // turn every fragment read into a generic 64-bit LD instead of an LDS
+  const unsigned sraw = (unsigned)__cvta_generic_to_shared(smem_raw);
+  unsigned char* base = smem_raw + ((1024u - (sraw & 1023u)) & 1023u);
   double* sA = reinterpret_cast<double*>(base + SM::A);
   double* sB = reinterpret_cast<double*>(base + SM::B);
   double* sC = reinterpret_cast<double*>(base + SM::C);
@@ -355,7 +359,7 @@ bool make_kmajor_map(CUtensorMap* map, const double* X, long long rows, long lon
                      int box_rows);
 
 template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
-cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st) {
+cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reserve_sms = 0) {
   using SM = tg::Smem<CF, A_KMAJ, B_KMAJ>;
   auto kern = gemm_tma_kernel<CF, A_KMAJ, B_KMAJ, MODE>;
   static bool attr_set = false;
@@ -383,7 +387,8 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st) {
   map.ntiles = ntiles;
   const int nitems = ntiles * (MODE == MODE_SPLITK ? splits : 1);
   if (nitems == 0) return cudaSuccess;
-  const int nsm = tma_num_sms() * CF::MINB;
+  // reserve_sms: SMs left free for kernels on other streams
+  const int nsm = (tma_num_sms() - (reserve_sms > 0 && reserve_sms < tma_num_sms() ? reserve_sms : 0)) * CF::MINB;
   const int grid = nitems < nsm ? nitems : nsm;
   kern<<<grid, CF::NCONS + 32, SM::TOTAL, st>>>(ma, mb, p, nitems, map);
   return cudaGetLastError();

@@ -448,10 +448,19 @@ struct CfgSel {
   int pingpong = 0;
   // persistent TMA-fed warp-specialised kernels (gemm_tma.cuh) per class:
   // STAN_CL_TMA="syrk,gemm,splitk" with 1 = TMA kernel, 0 = one-tile-per-CTA cp.async kernel
-  // default: the forward SYRK stays one-tile-per-CTA so the lookahead panel
-  // kernels on the side stream find SMs at CTA boundaries
-  int tma_syrk = 0, tma_gemm = 1, tma_splitk = 1;
+  int tma_syrk = 1, tma_gemm = 1, tma_splitk = 1;
+  // the persistent forward SYRK leaves SMs free so the lookahead panel kernels
+  // on the side stream always find SMs: reserve_big when the
+  // trailing order M >= reserve_m, else reserve_small (the panel is then
+  // relatively longer); STAN_CL_SYRK_RESERVE="big,small,m" overrides
+  int reserve_big = 8, reserve_small = 24, reserve_m = 8192;
+  int syrk_reserve(int M) const { return M >= reserve_m ? reserve_big : reserve_small; }
   CfgSel() {
+    const char* rs = getenv("STAN_CL_SYRK_RESERVE");
+    if (rs) {
+      int n = sscanf(rs, "%d,%d,%d", &reserve_big, &reserve_small, &reserve_m);
+      if (n == 1) reserve_small = reserve_big;
+    }
     const char* pp = getenv("STAN_CL_PINGPONG");
     if (pp) pingpong = atoi(pp);
     const char* ps = getenv("STAN_CL_TMA");
@@ -528,7 +537,7 @@ cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const doub
   if (M == 0) return cudaSuccess;
   Prof prof_(PROF_SYRK, (double)K * M * (M + 1.0), st, 8.0 * M * (M + 1.0) + 8.0 * (double)M * K);
   GemmArgs p{A, lda, B, ldb, C, ldc, M, M, K, K, -1.0, 1, 1, status, cfgsel().pingpong};
-  if (cfgsel().tma_syrk) return launch_tma<tg::CfgT32, true, true, MODE_LOWER>(p, 1, st);
+  if (cfgsel().tma_syrk) return launch_tma<tg::CfgT32, true, true, MODE_LOWER>(p, 1, st, cfgsel().syrk_reserve(M));
   switch (cfgsel().syrk) {
     case CFG_BIG: return launch_gemm<gemm::CfgBig, true, true, MODE_LOWER>(p, 1, st);
     case CFG_W8: return launch_gemm<gemm::CfgW8, true, true, MODE_LOWER>(p, 1, st);
