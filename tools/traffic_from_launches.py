@@ -6,10 +6,10 @@
 
 Kernel -> library profiling class (paper_1907_01063_b200.PROFILE_KINDS):
   gemm_dmma_kernel<..., 1, 1, 1> / gemm_tma_kernel<..., 1, 1, 1>   syrk      (MODE_LOWER)
-  gemm_tma_kernel<..., 1, 0, 0>                                    adj_gemm  (B_bar, R_bar updates)
+  gemm_tma_kernel<..., 1, 0, 0>                                    adj_gemm  (B_bar, R_bar updates, C_bar D^-1)
   gemm_tma_kernel<..., 0, 0, 2> / gemm_dmma_kernel<..., 0, 0, 2>   splitk
-  gemm_tma_kernel<..., 1, 1, 0>                                    lookahead
-  gemm_dmma_kernel<..., 1, 0, 0>                                   trmm      (in-place C_bar D^-1)
+  gemm_tma_kernel<..., 1, 1, 0>                                    lookahead (main-stream column update)
+  gemm_dmma_kernel<..., 1, 1, 0>                                   panel_gemm (side stream)
 """
 import collections
 import csv
@@ -17,7 +17,8 @@ import json
 import re
 import sys
 
-UNITS = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+UNITS = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9,
+         "%": 1.0, "inst": 1.0, "cycle": 1.0, "": 1.0}
 
 
 def classify(name: str):
@@ -33,7 +34,9 @@ def classify(name: str):
     if key == ("1", "0", "0"):
         return "adj_gemm" if kern == "gemm_tma_kernel" else "trmm"
     if key == ("1", "1", "0"):
-        return "lookahead"
+        # TMA: main-stream lookahead column; one-tile-per-CTA: side-stream panel
+        # GEMMs (in-panel lookahead, TRSM cross update)
+        return "lookahead" if kern == "gemm_tma_kernel" else "panel_gemm"
     return kern
 
 
