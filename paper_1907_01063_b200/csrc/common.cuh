@@ -36,6 +36,54 @@ __device__ __forceinline__ void dmma_8x8x4(double& c0, double& c1, double a, dou
                : "d"(a), "d"(b));
 }
 
+// ---- call-free correctly rounded square root, reciprocal and quotient -------
+// CUDA's IEEE sqrt() and '/' are an inline fast path plus a CALL to a slow
+// path; inside the unrolled panel kernels that call forces live register
+// arrays into local memory.  These sequences have no call.  For operands in
+// [2^-600, 2^600] they return the IEEE round-to-nearest result:
+//   sqrt_rcp_pos: two Newton steps on the MUFU rsqrt seed, then sq =
+//     s + (a - s^2) r/2 (the residual exact with FMA) and one Markstein
+//     reciprocal step y = r + r(1 - sq r);
+//   div_pos: q = x y, q' = q + (x - q b) y (Markstein: correctly rounded when
+//     y = RN(1/b); R12).
+// Validated bit-for-bit against sqrt() and '/' on 2^32 random operand pairs
+// with exponents in [-200, 200) (tools/potrf_lab.cu, profiles/r01_potrf_trsm_notes.md).
+// Pivots outside [2^-600, 2^600] are brought into range by an exact power-of-two
+// scaling (scaled_sqrt_rcp).
+__device__ __forceinline__ void sqrt_rcp_pos(double a, double& sq, double& y) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+  const double h = 0.5 * a;
+  double e = fma(-h * r, r, 0.5);
+  r = fma(r, e, r);
+  e = fma(-h * r, r, 0.5);
+  r = fma(r, e, r);
+  const double s = a * r;
+  sq = fma(fma(-s, s, a), 0.5 * r, s);
+  y = fma(r, fma(-sq, r, 1.0), r);
+}
+__device__ __forceinline__ void scaled_sqrt_rcp(double a, double& sq, double& y) {
+  // branch-free, so it schedules as one basic block with independent work
+  const bool tiny = a < 0x1p-600, huge = a > 0x1p600;
+  sqrt_rcp_pos(a * (tiny ? 0x1p800 : huge ? 0x1p-800 : 1.0), sq, y);
+  sq *= tiny ? 0x1p-400 : huge ? 0x1p400 : 1.0;
+  y *= tiny ? 0x1p400 : huge ? 0x1p-400 : 1.0;
+}
+__device__ __forceinline__ double rcp_pos(double b) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(b));
+  double e = fma(-b, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-b, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-b, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double div_pos(double x, double b, double y) {
+  const double q = x * y;
+  return fma(fma(-q, b, x), y, q);
+}
+
 // Device-side status word shared by the kernels of one call: 0 = fine,
 // k > 0 = first failing pivot row + 1 (LAPACK info).  Kernels that see a
 // nonzero word exit early (the result is unspecified on failure).

@@ -275,94 +275,178 @@ cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st) {
 }
 
 // ----------------------------------------------------------------------- F1
-// One CTA factors the 128 x 128 diagonal tile, right-looking column by column
-// (the "classic sequential algorithm", inner loop parallel).
-// The tile lives in REGISTERS: 256 threads as a 16 x 16 grid, thread (ti, tj)
-// owns rows ti + 16a and columns tj + 16b (a, b = 0..7; cyclic, so the active
-// trailing part stays balanced).  Per column j: the diagonal owner publishes
-// T[j][j]; the owners of column j take d = sqrt(T[j][j]) (IEEE), scale by an
-// IEEE division and publish the column; every thread then applies the rank-1
-// update to its elements with one FMA each (ascending j, R12).
+// One CTA factors the 128 x 128 diagonal tile (the "classic sequential
+// algorithm", inner loop parallel), blocked by 32 inside the CTA
+// with the tile staged in shared memory (pitch 129).  For each 32-column block:
+//   (a) warp 0 factors the 32 x 32 diagonal block alone: lane r holds row r in
+//       registers; per column J the pivot is shuffled to every lane, which
+//       computes sqrt and 1/sqrt (call-free, correctly rounded: common.cuh),
+//       divides by Markstein correction, publishes the column through shared
+//       memory and applies the rank-1 update;
+//   (b) the rows below are solved against the block (one thread per row,
+//       ascending j, quotients via the stored reciprocals);
+//   (c) the trailing lower part takes the rank-32 update (16 x 16 thread grid,
+//       up to 6 x 6 elements per thread).
+// Every element sees the fma(-l_rj, l_cj, a) updates of the unblocked
+// right-looking algorithm in ascending j and IEEE-identical square roots and
+// quotients (R12): the result is bit-identical to the column-by-column
+// kernel it replaced (tools/potrf_lab.cu).
 constexpr int TP = NB + 1;  // pitch of shared 128 x 128 staging tiles (doubles)
+constexpr int POTRF_SMEM = NB * TP * (int)sizeof(double);
+
+// column J of the warp factorization; templated so every register index is
+// static (a runtime-bounded loop would send row[] to local memory)
+template <int J>
+__device__ __forceinline__ void potrf_wstep(double (&row)[32], int lane, double* rc, double* col, int& bad) {
+  const double d = __shfl_sync(0xffffffffu, row[J], J);
+  bad = (bad < 0 && !(d > 0.0)) ? J : bad;  // warp-uniform
+  double sq, y;
+  scaled_sqrt_rcp(d, sq, y);
+  if (lane == J) {
+    row[J] = sq;
+    rc[J] = y;
+  } else {
+    row[J] = div_pos(row[J], sq, y);
+  }
+  col[lane] = row[J];
+  __syncwarp();
+#pragma unroll
+  for (int c = J + 1; c < 32; ++c) {
+    const double lc = col[c];
+    if (lane >= c) row[c] = fma(-row[J], lc, row[c]);
+  }
+  __syncwarp();
+  if constexpr (J + 1 < 32) potrf_wstep<J + 1>(row, lane, rc, col, bad);
+}
+
+// warp 0: factor the 32 x 32 diagonal block at (c0, c0) of S in place;
+// returns the first failing column (relative) or -1
+__device__ __forceinline__ int potrf_wblock(double* S, int c0, int lane, double* rc, double* col) {
+  double row[32];
+  double* Sr = S + (c0 + lane) * TP + c0;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) row[c] = (c <= lane) ? Sr[c] : 0.0;
+  int bad = -1;
+  potrf_wstep<0>(row, lane, rc + c0, col, bad);
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    if (c <= lane) Sr[c] = row[c];
+  return bad;
+}
 
 __global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t ld, int64_t k0,
                                                             int* status) {
   if (*status != 0) return;
-  __shared__ double colbuf[NB];
-  __shared__ double diag_s;
+  extern __shared__ double S[];
+  __shared__ double rc[NB];   // 1 / L[j][j]
+  __shared__ double colb[32];
   __shared__ int fail_j;
-  const int tid = threadIdx.x;
-  const int ti = tid >> 4, tj = tid & 15;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* base = W + k0 * ld + k0;
-  double T[8][8];
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int r = ti + 16 * a, c = tj + 16 * b;
-      T[a][b] = (c <= r) ? base[(long long)r * ld + c] : 0.0;
-    }
-  if (tid == 0) fail_j = -1;
-  bool failed = false;  // uniform across the CTA (every thread tests the same pivot)
-#pragma unroll
-  for (int jb = 0; jb < 8; ++jb) {
-    for (int jt = 0; jt < 16; ++jt) {
-      const int j = 16 * jb + jt;
-      // diagonal owner (ti == jt, tj == jt) publishes the updated pivot
-      if (ti == jt && tj == jt) diag_s = T[jb][jb];
-      __syncthreads();
-      const double s = diag_s;
-      if (!(s > 0.0)) {
-        if (tid == 0) fail_j = j;
-        failed = true;
-        break;
-      }
-      if (tj == jt) {  // owners of column j (register column jb)
-        const double d = sqrt(s);
-#pragma unroll
-        for (int a = 0; a < 8; ++a) {
-          const int r = ti + 16 * a;
-          if (r > j) {
-            const double l = T[a][jb] / d;
-            T[a][jb] = l;
-            colbuf[r] = l;
-          } else if (r == j) {
-            T[a][jb] = d;
-          }
-        }
-      }
-      __syncthreads();
-      double cr[8], cc[8];
-#pragma unroll
-      for (int a = 0; a < 8; ++a) cr[a] = colbuf[ti + 16 * a];
-#pragma unroll
-      for (int b = 0; b < 8; ++b) cc[b] = colbuf[tj + 16 * b];
-      // trailing update of columns c > j (rows r <= j of those columns are the
-      // strict upper triangle: never read or stored, so left unpredicated)
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        if (tj + 16 * b > j) {
-#pragma unroll
-          for (int a = 0; a < 8; ++a) T[a][b] = fma(-cr[a], cc[b], T[a][b]);
-        }
+  if ((((uintptr_t)base & 15) == 0) && ((ld & 1) == 0)) {
+#pragma unroll 4
+    for (int idx = tid; idx < NB * NB / 2; idx += 256) {
+      const int r = idx >> 6, c = (idx & 63) << 1;
+      if (c <= r) {
+        const double2 v = *reinterpret_cast<const double2*>(base + (long long)r * ld + c);
+        S[r * TP + c] = v.x;
+        S[r * TP + c + 1] = v.y;
       }
     }
-    if (failed) break;
+  } else {
+    for (int idx = tid; idx < NB * NB; idx += 256) {
+      const int r = idx >> 7, c = idx & (NB - 1);
+      if (c <= r) S[r * TP + c] = base[(long long)r * ld + c];
+    }
   }
+  if (tid == 0) fail_j = -1;
   __syncthreads();
-#pragma unroll
-  for (int a = 0; a < 8; ++a)
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int r = ti + 16 * a, c = tj + 16 * b;
-      base[(long long)r * ld + c] = (c <= r) ? T[a][b] : 0.0;  // strict upper of the tile: +0.0
+  for (int c0 = 0; c0 < NB; c0 += 32) {
+    // (a) the 32 x 32 diagonal block, warp 0
+    if (warp == 0) {
+      const int bad = potrf_wblock(S, c0, lane, rc, colb);
+      if (lane == 0 && bad >= 0) fail_j = c0 + bad;
     }
+    __syncthreads();
+    const int r0 = c0 + 32, R = NB - r0;
+    if (fail_j >= 0 || R == 0) break;
+    // (b) rows r0.. of block column c0: X <- X L^-T, ascending j
+    if (tid < R) {
+      double* Sx = S + (r0 + tid) * TP + c0;
+      double x[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) x[c] = Sx[c];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        x[j] = div_pos(x[j], S[(c0 + j) * TP + c0 + j], rc[c0 + j]);
+#pragma unroll
+        for (int c = j + 1; c < 32; ++c) x[c] = fma(-x[j], S[(c0 + c) * TP + c0 + j], x[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) Sx[c] = x[c];
+    }
+    __syncthreads();
+    // (c) trailing lower part: S[i][k] -= sum_j X[i][j] X[k][j], r0 <= k <= i
+    {
+      const int ti = tid >> 4, tj = tid & 15;
+      double acc[6][6];
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int b = 0; b < 6; ++b) {
+          const int i = ti + 16 * a, k = tj + 16 * b;
+          acc[a][b] = (i < R && k <= i) ? S[(r0 + i) * TP + r0 + k] : 0.0;
+        }
+#pragma unroll 4
+      for (int j = 0; j < 32; ++j) {
+        double xi[6], xk[6];
+#pragma unroll
+        for (int a = 0; a < 6; ++a) {
+          xi[a] = (16 * a < R) ? S[(r0 + ti + 16 * a) * TP + c0 + j] : 0.0;
+          xk[a] = (16 * a < R) ? S[(r0 + tj + 16 * a) * TP + c0 + j] : 0.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 6; ++a)
+#pragma unroll
+          for (int b = 0; b <= a; ++b)
+            if (16 * a < R) acc[a][b] = fma(-xi[a], xk[b], acc[a][b]);
+      }
+#pragma unroll
+      for (int a = 0; a < 6; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) {
+          const int i = ti + 16 * a, k = tj + 16 * b;
+          if (i < R && k <= i) S[(r0 + i) * TP + r0 + k] = acc[a][b];
+        }
+    }
+    __syncthreads();
+  }
+  if ((((uintptr_t)base & 15) == 0) && ((ld & 1) == 0)) {
+#pragma unroll 4
+    for (int idx = tid; idx < NB * NB / 2; idx += 256) {
+      const int r = idx >> 6, c = (idx & 63) << 1;
+      const double2 v = make_double2(c <= r ? S[r * TP + c] : 0.0, c + 1 <= r ? S[r * TP + c + 1] : 0.0);
+      *reinterpret_cast<double2*>(base + (long long)r * ld + c) = v;  // strict upper of the tile: +0.0
+    }
+  } else {
+    for (int idx = tid; idx < NB * NB; idx += 256) {
+      const int r = idx >> 7, c = idx & (NB - 1);
+      base[(long long)r * ld + c] = (c <= r) ? S[r * TP + c] : 0.0;
+    }
+  }
   if (tid == 0 && fail_j >= 0) atomicCAS(status, 0, (int)(k0 + fail_j + 1));
 }
 
 cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStream_t st) {
   Prof prof_(PROF_POTRF, (double)NB * NB * NB / 3.0, st, 8.0 * NB * (NB + 1));
-  potrf_tile_kernel<<<1, 256, 0, st>>>(W, ld, k0, status);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(potrf_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         POTRF_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  potrf_tile_kernel<<<1, 256, POTRF_SMEM, st>>>(W, ld, k0, status);
   return cudaGetLastError();
 }
 
@@ -373,7 +457,7 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
 // which is the same column-by-column elimination as one 128-wide substitution,
 // with the cross-half updates done on the tensor cores.  Substitution kernel:
 // 64 rows per CTA, four threads own a row, thread p holding columns p + 4q in
-// registers; column j is finished by its owner with an IEEE division and
+// registers; column j is finished by its owner with a (call-free, IEEE-exact) division and
 // broadcast with a warp shuffle; Lw^T is staged in shared memory
 // (LT[j][l] = Lw[l][j], broadcast reads).
 constexpr int TRSM_ROWS = 64;
@@ -384,7 +468,7 @@ __global__ void __launch_bounds__(256, 2) trsm_panel_kernel(double* W, int64_t l
                                                             int64_t r0, const int* status) {
   if (*status != 0) return;
   __shared__ double LT[TRSM_W * TRSM_TP];
-  __shared__ double dg[TRSM_W];
+  __shared__ double dg[TRSM_W], rdg[TRSM_W];  // L_jj and RN(1 / L_jj)
   const int tid = threadIdx.x, lane = tid & 31;
   const double* L11 = W + k0 * ld + k0;
   for (int idx = tid; idx < TRSM_W * TRSM_W; idx += 256) {
@@ -392,7 +476,10 @@ __global__ void __launch_bounds__(256, 2) trsm_panel_kernel(double* W, int64_t l
     if (j <= l) {
       const double v = L11[(long long)l * ld + j];
       LT[j * TRSM_TP + l] = v;
-      if (j == l) dg[j] = v;
+      if (j == l) {
+        dg[j] = v;
+        rdg[j] = rcp_pos(v);
+      }
     }
   }
   constexpr int Q = TRSM_W / 4;
@@ -406,7 +493,7 @@ __global__ void __launch_bounds__(256, 2) trsm_panel_kernel(double* W, int64_t l
   const int owner_base = lane & ~3;
 #pragma unroll
   for (int j = 0; j < TRSM_W; ++j) {
-    if (p == (j & 3)) x[j >> 2] = x[j >> 2] / dg[j];
+    if (p == (j & 3)) x[j >> 2] = div_pos(x[j >> 2], dg[j], rdg[j]);  // == x / L_jj (common.cuh)
     const double v = __shfl_sync(0xffffffffu, x[j >> 2], owner_base | (j & 3));
     const double* lt = LT + j * TRSM_TP;
 #pragma unroll
