@@ -111,6 +111,26 @@ def test_cholesky_blocking_invariance(sc, n):
             lib.stan_cl_set_block_size(0)
 
 
+@pytest.mark.parametrize("n", [256, 700])
+def test_cholesky_power_of_two_scaling(sc, n):
+    """chol(D A D) = D chol(A) for D = diag(2^e_i): with power-of-two scales every
+    product, sum, square root and quotient of the algorithm scales exactly, so
+    the GPU result must be D times its unscaled result BIT FOR BIT.  The scales
+    put pivots at 2^+-800, outside [2^-600, 2^600], which exercises the exact
+    rescaling of the call-free sqrt/reciprocal (R12).  The paper's
+    Toeplitz matrix keeps every intermediate normal under these scales (SE
+    entries down to 1e-87 would underflow)."""
+    A = inputs.toeplitz(n)
+    e = np.random.default_rng(n).integers(-400, 401, n).astype(np.float64)
+    e[:3] = [400, -400, 0]
+    d = np.exp2(e)
+    As = A * d[:, None] * d[None, :]
+    L = host(sc.cholesky(dev(A)))
+    Ls = host(sc.cholesky(dev(As)))
+    assert np.array_equal(Ls, L * d[:, None])
+    assert relf(L, oracle.cholesky(A)) <= L_BAR_TOL
+
+
 def test_cholesky_in_place_and_upper_garbage(sc):
     n = 384
     K = se(n)

@@ -150,6 +150,19 @@ def test_integer_exact_family(n, band):
     assert np.array_equal(oracle.cholesky(A), L0)
 
 
+def test_power_of_two_scaling_equivariance():
+    """chol(D A D) = D chol(A) for D = diag(2^e): every step of the method
+    (products, sums, sqrt, division) commutes exactly with power-of-two scaling
+    while intermediates stay normal, so the oracle must reproduce D L BIT FOR
+    BIT; a transposed or mis-indexed operand breaks the row scaling."""
+    n = 64
+    A = inputs.toeplitz(n)
+    e = np.random.default_rng(7).integers(-400, 401, n).astype(np.float64)
+    d = np.exp2(e)
+    L = oracle.cholesky(A)
+    assert np.array_equal(oracle.cholesky(A * d[:, None] * d[None, :]), L * d[:, None])
+
+
 def test_long_double_twin():
     A = np.array([[4.0, 2.0], [2.0, 5.0]])
     assert np.array_equal(oracle.cholesky_ld(A), np.array([[2.0, 0], [1.0, 2.0]]))
