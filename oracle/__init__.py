@@ -48,6 +48,10 @@ def _load():
             getattr(lib, name).restype = ctypes.c_int
         lib.oracle_cholesky_adjoint.argtypes = [I64, P, P, P]
         lib.oracle_cholesky_adjoint.restype = ctypes.c_int
+        lib.oracle_trsv.argtypes = [I64, P, P, ctypes.c_int, P]
+        lib.oracle_trsv.restype = ctypes.c_int
+        lib.oracle_gp_lpdf_grad.argtypes = [I64, P, P, D, D, D, P, P]
+        lib.oracle_gp_lpdf_grad.restype = ctypes.c_int
         _lib = lib
     return _lib
 
@@ -120,3 +124,34 @@ def cholesky_adjoint(L, Lbar) -> np.ndarray:
     if info != 0:
         raise ValueError(f"L[{info - 1}][{info - 1}] is not finite and > 0")
     return Abar
+
+
+def trsv(L, b, trans: bool = False) -> np.ndarray:
+    """x with L x = b (trans=False) or L^T x = b (trans=True); lower L (oracle.c)."""
+    L = _c(L)
+    b = _c(b)
+    n = L.shape[0]
+    assert L.shape == (n, n) and b.shape == (n,)
+    x = np.empty_like(b)
+    info = _load().oracle_trsv(n, _ptr(L), _ptr(b), int(bool(trans)), _ptr(x))
+    if info != 0:
+        raise ValueError(f"L[{info - 1}][{info - 1}] is zero or not finite")
+    return x
+
+
+def gp_lpdf_grad(x, y, alpha: float, rho: float, sigma: float) -> tuple[float, np.ndarray, np.ndarray]:
+    """(lp, [d/d alpha, d/d rho, d/d sigma], d lp/d y) of the zero-mean GP
+    regression log density with K = SE(x; alpha, rho) + sigma^2 I (oracle.c)."""
+    x = _c(x)
+    y = _c(y)
+    n = x.shape[0]
+    assert y.shape == (n,)
+    out = np.empty(4, dtype=np.float64)
+    ybar = np.empty(n, dtype=np.float64)
+    info = _load().oracle_gp_lpdf_grad(n, _ptr(x), _ptr(y), float(alpha), float(rho), float(sigma),
+                                       _ptr(out), _ptr(ybar))
+    if info > 0:
+        raise NotPositiveDefinite(info)
+    if info < 0:
+        raise MemoryError("oracle_gp_lpdf_grad: allocation failed")
+    return float(out[0]), out[1:].copy(), ybar

@@ -23,6 +23,10 @@
  *   oracle_cholesky_adjoint    pinned (closed-form 2x2, finite differences, log-det
  *                               and GP-density identities, paper's blocked algorithm,
  *                               torch autograd cross-check, integer-exact family)
+ *   oracle_trsv                pinned (integer-exact round trips, independent
+ *                               library solve)
+ *   oracle_gp_lpdf_grad        pinned (n = 1 closed form, independent Gaussian
+ *                               log-density, trace-form gradient, finite differences)
  */
 #include <math.h>
 #include <stdint.h>
@@ -158,5 +162,118 @@ int oracle_cholesky_adjoint(int64_t n, const double* L, const double* Lbar, doub
     }
   }
   free(M);
+  return 0;
+}
+
+/*
+ * Triangular solve with one right-hand side, the triangular_solve primitive of
+ * the paper (§3.3 describes its blocked GPU form and reverse
+ * mode), by plain substitution:
+ *   trans == 0:  L x = b     x_i = (b_i - sum_{j<i} L[i][j] x_j) / L[i][i],  i ascending
+ *   trans == 1:  L^T x = b   x_i = (b_i - sum_{j>i} L[j][i] x_j) / L[i][i],  i descending
+ * Sums in ascending j.  Reads only the lower triangle of L.  Returns 0, or
+ * k+1 for the first (in solve order) diagonal entry that is not finite and
+ * nonzero.  x may alias b.
+ */
+int oracle_trsv(int64_t n, const double* L, const double* b, int trans, double* x) {
+  for (int64_t k = 0; k < n; ++k) {
+    double d = L[IDX(k, k)];
+    if (d == 0.0 || !isfinite(d)) return (int)(k + 1);
+  }
+  if (x != b)
+    for (int64_t i = 0; i < n; ++i) x[i] = b[i];
+  if (!trans) {
+    for (int64_t i = 0; i < n; ++i) {
+      double s = x[i];
+      for (int64_t j = 0; j < i; ++j) s = s - L[IDX(i, j)] * x[j];
+      x[i] = s / L[IDX(i, i)];
+    }
+  } else {
+    for (int64_t i = n - 1; i >= 0; --i) {
+      double s = x[i];
+      for (int64_t j = i + 1; j < n; ++j) s = s - L[IDX(j, i)] * x[j];
+      x[i] = s / L[IDX(i, i)];
+    }
+  }
+  return 0;
+}
+
+/*
+ * Marginal log density of a zero-mean GP regression and its gradient: the
+ * per-gradient work of the paper's GP example (§4.2, the
+ * model of Betancourt 2017: y ~ multi_normal_cholesky(0, chol(K))), whose
+ * cost is the Cholesky + adjoint hot path:
+ *   K     = SE(x; alpha, rho) + sigma^2 I                      (oracle_se_cov)
+ *   L     = chol(K)                                            (oracle_cholesky)
+ *   z     = L^-1 y                                             (oracle_trsv)
+ *   lp    = -1/2 z.z - sum_i log L_ii - n/2 log(2 pi)
+ *   a     = L^-T z  (= K^-1 y)                                 (oracle_trsv)
+ *   L_bar = tril(a z^T) - diag(1 / L_ii)      (d lp / d L, lower part)
+ *   A_bar = cholesky_adjoint(L, L_bar)                         (oracle_cholesky_adjoint)
+ *   d lp / d theta = sum_{i >= j} A_bar[i][j] d K_ij / d theta  (A_bar's lower
+ *     entries are the adjoints of the symmetric pairs, R5), with
+ *     E_ij = exp((x_i - x_j)^2 (-0.5 / rho^2)):
+ *     d K_ij / d alpha = 2 alpha E_ij,  d K_ij / d rho = alpha^2 E_ij (x_i - x_j)^2 / rho^3,
+ *     d K_ij / d sigma = 2 sigma [i == j]
+ *   d lp / d y = -a.
+ * out[0] = lp, out[1..3] = d lp / d (alpha, rho, sigma); ybar (may be NULL) = -a.
+ * Returns 0, the Cholesky info (k+1) if K is not positive definite, or -2 on
+ * allocation failure.  Sums in ascending index order.
+ */
+int oracle_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alpha, double rho, double sigma,
+                        double* out, double* ybar) {
+  size_t nn = (size_t)n * (size_t)n;
+  double* K = (double*)malloc(sizeof(double) * (nn ? nn : 1));
+  double* L = (double*)malloc(sizeof(double) * (nn ? nn : 1));
+  double* z = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+  double* a = (double*)malloc(sizeof(double) * (size_t)(n ? n : 1));
+  if (!K || !L || !z || !a) {
+    free(K); free(L); free(z); free(a);
+    return -2;
+  }
+  oracle_se_cov(n, x, alpha, rho, sigma * sigma, K);
+  int info = oracle_cholesky(n, K, L);
+  if (info != 0) {
+    free(K); free(L); free(z); free(a);
+    return info;
+  }
+  oracle_trsv(n, L, y, 0, z);
+  double zz = 0.0, logdet = 0.0;
+  for (int64_t i = 0; i < n; ++i) zz = zz + z[i] * z[i];
+  for (int64_t i = 0; i < n; ++i) logdet = logdet + log(L[IDX(i, i)]);
+  const double log_2pi = 1.8378770664093454835606594728112;  /* log(2 pi) */
+  out[0] = -0.5 * zz - logdet - 0.5 * (double)n * log_2pi;
+  oracle_trsv(n, L, z, 1, a);
+  /* L_bar into K (K is no longer needed); A_bar in place of L_bar */
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double v = 0.0;
+      if (j < i) v = a[i] * z[j];
+      if (j == i) v = a[i] * z[i] - 1.0 / L[IDX(i, i)];
+      K[IDX(i, j)] = v;
+    }
+  info = oracle_cholesky_adjoint(n, L, K, K);
+  if (info != 0) {
+    free(K); free(L); free(z); free(a);
+    return info;
+  }
+  double g_alpha = 0.0, g_rho = 0.0, g_sigma = 0.0;
+  const double neg_half_inv_rho2 = -0.5 / (rho * rho);
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t j = 0; j <= i; ++j) {
+      double d = x[i] - x[j];
+      double e = exp(d * d * neg_half_inv_rho2);
+      double ab = K[IDX(i, j)];
+      g_alpha = g_alpha + ab * (2.0 * alpha * e);
+      g_rho = g_rho + ab * (alpha * alpha * e * (d * d) / (rho * rho * rho));
+      if (i == j) g_sigma = g_sigma + ab * (2.0 * sigma);
+    }
+  }
+  out[1] = g_alpha;
+  out[2] = g_rho;
+  out[3] = g_sigma;
+  if (ybar)
+    for (int64_t i = 0; i < n; ++i) ybar[i] = -a[i];
+  free(K); free(L); free(z); free(a);
   return 0;
 }

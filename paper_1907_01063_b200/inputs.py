@@ -6,6 +6,9 @@ integer test families.  Both the oracle and the CUDA path consume its output.
 
 Recipes:
   * ``gp_x``      x_i ~ Unif(-10, 10) i.i.d., unsorted (§4.2).
+  * ``gp_y``      y_i ~ N(f(x_i), sd 0.1), f(x) = beta (x + x^2 - x^3 + 100 sin 2x
+    - alpha) with alpha, beta fixing E[f] = 0, Var[f] = 1 under Unif(-10, 10)
+    ("1/10" read as the standard deviation, R16).
   * ``lbar``      L_bar = tril of N(0, 1) draws (the adjoint seed).
   * ``toeplitz``  A_ij = n - |i - j|, A_ii = n^2 (§3.3.3).
   * ``unit_lower_pm1``  unit-lower L with off-diagonal entries in {-1, 0, 1},
@@ -19,6 +22,7 @@ import numpy as np
 
 X_SEED = 42
 LBAR_SEED = 43
+Y_SEED = 44
 
 
 def rng(seed: int) -> np.random.Generator:
@@ -28,6 +32,32 @@ def rng(seed: int) -> np.random.Generator:
 def gp_x(n: int, seed: int = X_SEED) -> np.ndarray:
     """n inputs x_i ~ Unif(-10, +10)."""
     return -10.0 + 20.0 * rng(seed).random(n)
+
+
+def _gp_f_constants() -> tuple[float, float]:
+    """alpha = E[g], beta = 1 / sd[g] for g(x) = x + x^2 - x^3 + 100 sin 2x,
+    x ~ Unif(-10, 10), by 400-point Gauss-Legendre quadrature (exact for the
+    polynomial part; the sin part converges far below 1e-14)."""
+    t, w = np.polynomial.legendre.leggauss(400)
+    xs = 10.0 * t
+    w = w / 2.0  # density 1/20 times dx = 10 dt
+    g = xs + xs ** 2 - xs ** 3 + 100.0 * np.sin(2.0 * xs)
+    m = float(np.sum(w * g))
+    v = float(np.sum(w * (g - m) ** 2))
+    return m, 1.0 / np.sqrt(v)
+
+
+GP_F_ALPHA, GP_F_BETA = _gp_f_constants()
+
+
+def gp_f(x: np.ndarray) -> np.ndarray:
+    """The paper's GP toy-data mean function."""
+    return GP_F_BETA * (x + x ** 2 - x ** 3 + 100.0 * np.sin(2.0 * x) - GP_F_ALPHA)
+
+
+def gp_y(x: np.ndarray, seed: int = Y_SEED, sd: float = 0.1) -> np.ndarray:
+    """Targets y_i ~ N(f(x_i), sd)."""
+    return gp_f(x) + sd * rng(seed).standard_normal(x.shape[0])
 
 
 def lbar(n: int, seed: int = LBAR_SEED) -> np.ndarray:
