@@ -147,6 +147,40 @@ int stan_cl_dist_sim_cholesky(int64_t n, int G, double* const* A_locals, int64_t
 int stan_cl_dist_sim_cholesky_adjoint(int64_t n, int G, const double* const* L_locals, double* const* W_locals,
                                       int64_t ld_local);
 
+/* ---- NEXT rows around the hot path ---- */
+
+/*
+ * Triangular solve with one right-hand side (the paper's triangular_solve,
+ * PAPER.md:231-238 §3.3; NEXT-2):
+ *   trans == 0:  x = L^-1 b        trans != 0:  x = L^-T b
+ * L: n x n row-major (ld n), only the lower triangle is read; its diagonal must
+ * be positive (a Cholesky factor): the first L[k][k] that is not finite and
+ * > 0 returns k+1 (x unspecified).  b, x: n doubles; x may alias b (in place),
+ * any other overlap -> STAN_CL_EINVAL.  Device pointers; synchronous.
+ * Blocked substitution, one CTA per 64-row block, no inverse formed.
+ */
+int stan_cl_trsv(int64_t n, const double* L, const double* b, double* x, int trans);
+
+/*
+ * Marginal log density of zero-mean GP regression and its gradient -- the
+ * per-gradient work of the paper's GP example (§4.2, the model
+ * y ~ multi_normal_cholesky(0, chol(K)); NEXT-1):
+ *   K = alpha^2 exp((x_i - x_j)^2 (-0.5 / rho^2)) + sigma^2 [i == j]
+ *   out[0] = log p(y) = -1/2 y^T K^-1 y - 1/2 log det K - n/2 log(2 pi)
+ *   out[1], out[2], out[3] = d log p / d alpha, d rho, d sigma
+ *   y_bar (may be NULL) = d log p / d y = -K^-1 y
+ * The O(n^3) work is this library's Cholesky (stan_cl_cholesky) and its
+ * adjoint (stan_cl_cholesky_adjoint) with L_bar = tril(a z^T) - diag(1 / L_ii),
+ * z = L^-1 y, a = L^-T z; the hyperparameter gradient contracts A_bar's lower
+ * triangle with dK/dtheta.  x, y: n doubles; out: 4 doubles; y_bar: n doubles;
+ * all device pointers.  Returns 0, the Cholesky info k+1 if K is not positive
+ * definite (out unspecified), STAN_CL_EINVAL for n < 0, NULL x/y/out with
+ * n > 0, or rho == 0 / non-finite alpha, rho, sigma.  n == 0: out = {0, 0, 0, 0}.
+ * Library-owned workspace: two n x n matrices + O(n).  Synchronous.
+ */
+int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alpha, double rho, double sigma,
+                         double* out, double* y_bar);
+
 /* ---- control ---- */
 int stan_cl_set_stream(void* cuda_stream); /* cudaStream_t; NULL = legacy default stream */
 void* stan_cl_get_stream(void);
@@ -170,7 +204,8 @@ long long stan_cl_kernel_launches(void);
  * 1 adjoint DMMA GEMMs (B_bar, R_bar updates), 2 split-K long-K contraction,
  * 3 POTRF tile, 4 TRSM panel, 5 batched diagonal-block inverse, 6 128^3
  * products, 7 SE build, 8 other, 9 forward lookahead-column GEMMs,
- * 10 C_bar D^-1 products.  stan_cl_profile_enable(on): 0 = off, 1 = every
+ * 10 C_bar D^-1 products, 11 triangular solves and GP log-density /
+ * gradient kernels.  stan_cl_profile_enable(on): 0 = off, 1 = every
  * class, otherwise (mask << 1) enables class k when bit k of mask is set.
  * stan_cl_profile_read synchronises on the recorded events and returns the
  * summed milliseconds, the summed algorithmic flops and the launch count of a

@@ -39,6 +39,8 @@ SIGNATURES = {
     "stan_cl_cholesky": (_I, [_I64, _P, _P]),
     "stan_cl_cholesky_adjoint": (_I, [_I64, _P, _P, _P]),
     "stan_cl_gp_exp_quad_cov": (_I, [_I64, _P, _D, _D, _D, _P]),
+    "stan_cl_trsv": (_I, [_I64, _P, _P, _P, _I]),
+    "stan_cl_gp_lpdf_grad": (_I, [_I64, _P, _P, _D, _D, _D, _P, _P]),
     "stan_cl_cholesky_async": (_I, [_I64, _P, _P, _P]),
     "stan_cl_cholesky_adjoint_async": (_I, [_I64, _P, _P, _P, _P]),
     "stan_cl_cholesky_host": (_I, [_I64, _P, _P]),
@@ -165,6 +167,50 @@ def gp_exp_quad_cov(x: torch.Tensor, alpha: float = 1.0, rho: float = 1.0, jitte
                load().stan_cl_gp_exp_quad_cov(n, x.data_ptr(), float(alpha), float(rho), float(jitter),
                                               K.data_ptr()))
     return K
+
+
+def _dev_vector(t: torch.Tensor, name: str, n: int | None = None) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or t.dim() != 1:
+        raise ValueError(f"{name} must be a 1-D float64 CUDA tensor")
+    if n is not None and t.shape[0] != n:
+        raise ValueError(f"{name} must have {n} entries")
+    return t.contiguous()
+
+
+def trsv(L: torch.Tensor, b: torch.Tensor, trans: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """x = L^-1 b (trans=False) or L^-T b (trans=True), L lower with positive
+    diagonal (stan_cl_trsv).  ``out`` may be ``b`` (in place)."""
+    L = _dev_matrix(L, "L")
+    n = L.shape[0]
+    b = _dev_vector(b, "b", n)
+    x = torch.empty_like(b) if out is None else out
+    with torch.cuda.device(L.device):
+        _bind_stream(L.device)
+        rc = _check("stan_cl_trsv", load().stan_cl_trsv(n, L.data_ptr(), b.data_ptr(), x.data_ptr(),
+                                                        int(bool(trans))))
+    if rc > 0:
+        raise ValueError(f"L[{rc - 1}][{rc - 1}] is not finite and > 0")
+    return x
+
+
+def gp_lpdf_grad(x: torch.Tensor, y: torch.Tensor, alpha: float, rho: float, sigma: float,
+                 y_bar: bool = True) -> tuple[torch.Tensor, torch.Tensor | None]:
+    """Zero-mean GP regression log density and gradient (stan_cl_gp_lpdf_grad):
+    returns (out, ybar) with out = [lp, d/d alpha, d/d rho, d/d sigma] (cuda
+    float64[4]) and ybar = d lp / d y (or None)."""
+    x = _dev_vector(x, "x")
+    n = x.shape[0]
+    y = _dev_vector(y, "y", n)
+    out = torch.empty(4, dtype=torch.float64, device=x.device)
+    yb = torch.empty_like(y) if y_bar else None
+    with torch.cuda.device(x.device):
+        _bind_stream(x.device)
+        rc = _check("stan_cl_gp_lpdf_grad", load().stan_cl_gp_lpdf_grad(
+            n, x.data_ptr(), y.data_ptr(), float(alpha), float(rho), float(sigma), out.data_ptr(),
+            None if yb is None else yb.data_ptr()))
+    if rc > 0:
+        raise NotPositiveDefinite(rc)
+    return out, yb
 
 
 def cholesky_async(A: torch.Tensor, L: torch.Tensor, info: torch.Tensor | None = None) -> None:
@@ -313,7 +359,7 @@ def kernel_launches() -> int:
 
 
 PROFILE_KINDS = ["syrk", "adj_gemm", "splitk", "potrf", "trsm", "tri_inverse", "gemm128", "se_cov", "other",
-                 "lookahead", "trmm"]
+                 "lookahead", "trmm", "gp"]
 
 
 def profile_enable(on: bool = True, kinds=None) -> None:

@@ -37,9 +37,11 @@ struct State {
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the *_host entry points
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> xev;  // per-block events of the streamed host transfers
-  void* mat[2] = {nullptr, nullptr};  // cached N x N working matrices (padded / host paths)
+  // cached working buffers: 0, 1 = N x N matrices of the padded / host paths;
+  // 2, 3 = K/L and L_bar/A_bar of the GP gradient; 4 = O(n) GP / solve scratch
+  void* mat[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
   cudaStream_t cap = nullptr;         // capture stream for the CUDA-graph cache
-  size_t mat_cap[2] = {0, 0};
+  size_t mat_cap[5] = {0, 0, 0, 0, 0};
   int nb = 0;      // forward outer block: 0 = auto, 128 or 256
   int adj_nb = 0;  // adjoint block: 0 = auto, 128 or 256
   void* ws = nullptr;  // library-owned persistent workspace
@@ -67,6 +69,12 @@ bool ranges_overlap(const void* a, const void* b, size_t bytes) {
   const char* x = (const char*)a;
   const char* y = (const char*)b;
   return x < y + bytes && y < x + bytes;
+}
+// [a, a + abytes) and [b, b + bbytes) intersect
+bool ranges_overlap2(const void* a, size_t abytes, const void* b, size_t bbytes) {
+  const char* x = (const char*)a;
+  const char* y = (const char*)b;
+  return x < y + bbytes && y < x + abytes;
 }
 
 // ---------------------------------------------------------------- workspace
@@ -474,6 +482,30 @@ int adjoint_enqueue(int64_t n, const double* L, const double* Lbar, double* Abar
   return STAN_CL_OK;
 }
 
+// ---- NEXT-2: triangular solve; NEXT-1: GP log density + gradient ----------
+// O(n) scratch (slot 4): z, a (n each), hyper partial sums, then the solve's
+// ready flags + ticket (ints)
+struct VecScratch {
+  double* z;
+  double* a;
+  double* partial;
+  double* out;
+  int* flags;
+};
+int vec_scratch(int64_t n, VecScratch* v) {
+  const size_t nd = 2 * (size_t)n + gp_hyper_scratch_doubles() + 8;
+  const size_t bytes = nd * sizeof(double) + sizeof(int) * ((size_t)n / 64 + 4);
+  double* p = nullptr;
+  int rc = ensure_mat(4, bytes, &p);
+  if (rc) return rc;
+  v->z = p;
+  v->a = p + n;
+  v->partial = p + 2 * n;
+  v->out = v->partial + gp_hyper_scratch_doubles();
+  v->flags = (int*)(p + nd);
+  return STAN_CL_OK;
+}
+
 int read_status() {
   int rc = ensure_host_status();
   if (rc) return rc;
@@ -598,6 +630,64 @@ int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_b
 int stan_cl_cholesky_adjoint(int64_t n, const double* L, const double* L_bar, double* A_bar) {
   int rc = stan_cl_cholesky_adjoint_async(n, L, L_bar, A_bar, nullptr);
   if (rc || n == 0) return rc;
+  return read_status();
+}
+
+int stan_cl_trsv(int64_t n, const double* L, const double* b, double* x, int trans) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!L || !b || !x) return STAN_CL_EINVAL;
+  const size_t vb = (size_t)n * sizeof(double);
+  if (x != b && ranges_overlap(x, b, vb)) return STAN_CL_EINVAL;
+  if (ranges_overlap2(x, vb, L, (size_t)n * vb)) return STAN_CL_EINVAL;
+  int rc = ensure_ws(al(sizeof(int) * 64));
+  if (rc) return rc;
+  VecScratch v;
+  if ((rc = vec_scratch(n, &v))) return rc;
+  int* status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  CK(check_diag(L, n, n, status, st));
+  CK(trsv(L, n, n, b, x, trans != 0, v.flags, status, st));
+  return read_status();
+}
+
+int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alpha, double rho, double sigma,
+                         double* out, double* y_bar) {
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n > 0 && (!x || !y || !out)) return STAN_CL_EINVAL;
+  if (!(rho != 0.0) || !(rho - rho == 0.0) || !(alpha - alpha == 0.0) || !(sigma - sigma == 0.0))
+    return STAN_CL_EINVAL;
+  cudaStream_t st = g.stream;
+  if (n == 0) {
+    if (out) CK(cudaMemsetAsync(out, 0, 4 * sizeof(double), st));
+    return STAN_CL_OK;
+  }
+  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  double *K = nullptr, *W = nullptr;
+  int rc = ensure_mat(2, bytes, &K);
+  if (rc) return rc;
+  if ((rc = ensure_mat(3, bytes, &W))) return rc;
+  VecScratch v;
+  if ((rc = vec_scratch(n, &v))) return rc;
+  // size the shared workspace for the adjoint now: growing it later would
+  // move the status word the kernels below are given
+  if ((rc = ensure_ws(adj_plan(n).total))) return rc;
+  // K = SE + sigma^2 I;  L = chol(K) in place (the hot path's forward)
+  CK(se_cov(n, x, alpha, rho, sigma * sigma, K, st));
+  if ((rc = cholesky_enqueue(n, K, K, nullptr))) return rc;
+  if ((rc = read_status())) return rc;  // not positive definite: info
+  int* status = (int*)g.ws;
+  // z = L^-1 y, lp, a = L^-T z, L_bar
+  CK(trsv(K, n, n, y, v.z, false, v.flags, status, st));
+  CK(gp_lp(K, n, n, v.z, out, status, st));
+  CK(trsv(K, n, n, v.z, v.a, true, v.flags, status, st));
+  CK(gp_lbar(K, n, n, v.a, v.z, W, n, status, st));
+  // A_bar = cholesky_adjoint(L, L_bar), in place (the hot path's adjoint)
+  if ((rc = adjoint_enqueue(n, K, W, W, nullptr))) return rc;
+  status = (int*)g.ws;
+  CK(gp_hyper(W, n, n, x, alpha, rho, sigma, v.partial, out + 1, status, st));
+  if (y_bar) CK(negate(v.a, y_bar, n, status, st));
   return read_status();
 }
 
@@ -802,7 +892,7 @@ int stan_cl_finalize(void) {
   g.events.clear();
   for (cudaEvent_t e : g.xev) cudaEventDestroy(e);
   g.xev.clear();
-  for (int i = 0; i < 2; ++i) {
+  for (int i = 0; i < 5; ++i) {
     if (g.mat[i]) cudaFree(g.mat[i]);
     g.mat[i] = nullptr;
     g.mat_cap[i] = 0;

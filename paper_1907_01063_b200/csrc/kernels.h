@@ -22,7 +22,8 @@ enum ProfKind {
   PROF_MISC = 8,       // copies, reductions, Phi, checks
   PROF_LOOKAHEAD = 9,  // F3 lookahead column + in-panel update (DMMA)
   PROF_TRMM = 10,      // R1 C_bar <- C_bar D^-1 (DMMA)
-  PROF_KINDS = 11
+  PROF_GP = 11,        // NEXT-1/2: triangular solves, GP log density / gradient reductions
+  PROF_KINDS = 12
 };
 // RAII launch scope: counts the launch and, when profiling is on, brackets it
 // with CUDA events on its stream
@@ -116,5 +117,22 @@ cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, co
                     cudaStream_t st, int n = 128);
 // status = first base+k+1 with !(L[k][k] > 0 && finite), k < n
 cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st, int64_t base = 0);
+
+// ---- NEXT-1/NEXT-2 (gp.cu) ----
+// x = L^-1 b (trans = false) or L^-T b (trans = true); L lower, positive normal
+// diagonal.  flags: (ceil(n/64) + 1) ints of scratch (zeroed here).  x may alias b.
+cudaError_t trsv(const double* L, int64_t ld, int64_t n, const double* b, double* x, bool trans, int* flags,
+                 const int* status, cudaStream_t st);
+// out[0] = -1/2 z.z - sum log L_ii - n/2 log(2 pi)
+cudaError_t gp_lp(const double* L, int64_t ld, int64_t n, const double* z, double* out, const int* status,
+                  cudaStream_t st);
+// lower triangle of W <- tril(a z^T) - diag(1 / L_ii)
+cudaError_t gp_lbar(const double* L, int64_t ld, int64_t n, const double* a, const double* z, double* W,
+                    int64_t ldw, const int* status, cudaStream_t st);
+// out[0..2] = sum_{i>=j} A_bar_ij dK_ij/d(alpha, rho, sigma); partial: gp_hyper_scratch_doubles()
+size_t gp_hyper_scratch_doubles();
+cudaError_t gp_hyper(const double* A, int64_t lda, int64_t n, const double* x, double alpha, double rho,
+                     double sigma, double* partial, double* out, const int* status, cudaStream_t st);
+cudaError_t negate(const double* a, double* y, int64_t n, const int* status, cudaStream_t st);
 
 }  // namespace stancl
