@@ -181,6 +181,26 @@ int stan_cl_trsv(int64_t n, const double* L, const double* b, double* x, int tra
 int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alpha, double rho, double sigma,
                          double* out, double* y_bar);
 
+/*
+ * Batched small matrices (NEXT-4; "batched linear algebra"; one
+ * covariance per chain): batch independent n x n problems,
+ * 1 <= n <= 128, stored contiguously (matrix b at offset b*n*n, row-major).
+ *   stan_cl_cholesky_batched:         L_b = chol(A_b)                 (A may equal L)
+ *   stan_cl_cholesky_adjoint_batched: A_bar_b = adjoint(L_b, L_bar_b) (any of the
+ *                                     three may coincide; partial overlap -> EINVAL)
+ * Same per-matrix semantics as the single-matrix calls (lower triangles read,
+ * strict upper written +0.0).  info (device int[batch], may be NULL): LAPACK
+ * info of each matrix (forward: first failing pivot + 1; adjoint: first
+ * L[k][k] not finite and > 0, + 1).  Returns 0 when every matrix succeeded,
+ * k > 0 when matrix k-1 is the first that failed, negative on errors
+ * (n > 128 -> STAN_CL_EINVAL).  Forward: one CTA per matrix (the diagonal-tile
+ * kernel, identity padded); adjoint: the paper's diagonal-block step on
+ * 128 x 128 padded copies in chunks of 4096.  Device pointers; synchronous.
+ */
+int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* L, int* info);
+int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, const double* L_bar,
+                                     double* A_bar, int* info);
+
 /* ---- control ---- */
 int stan_cl_set_stream(void* cuda_stream); /* cudaStream_t; NULL = legacy default stream */
 void* stan_cl_get_stream(void);

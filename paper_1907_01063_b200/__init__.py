@@ -40,6 +40,8 @@ SIGNATURES = {
     "stan_cl_cholesky_adjoint": (_I, [_I64, _P, _P, _P]),
     "stan_cl_gp_exp_quad_cov": (_I, [_I64, _P, _D, _D, _D, _P]),
     "stan_cl_trsv": (_I, [_I64, _P, _P, _P, _I]),
+    "stan_cl_cholesky_batched": (_I, [_I64, _I64, _P, _P, _P]),
+    "stan_cl_cholesky_adjoint_batched": (_I, [_I64, _I64, _P, _P, _P, _P]),
     "stan_cl_gp_lpdf_grad": (_I, [_I64, _P, _P, _D, _D, _D, _P, _P]),
     "stan_cl_cholesky_async": (_I, [_I64, _P, _P, _P]),
     "stan_cl_cholesky_adjoint_async": (_I, [_I64, _P, _P, _P, _P]),
@@ -211,6 +213,43 @@ def gp_lpdf_grad(x: torch.Tensor, y: torch.Tensor, alpha: float, rho: float, sig
     if rc > 0:
         raise NotPositiveDefinite(rc)
     return out, yb
+
+
+def _dev_batch(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or t.dim() != 3 \
+            or t.shape[1] != t.shape[2]:
+        raise ValueError(f"{name} must be a (batch, n, n) float64 CUDA tensor")
+    return t.contiguous()
+
+
+def cholesky_batched(A: torch.Tensor, out: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """L_b = chol(A_b) for a (batch, n, n) tensor, n <= 128 (stan_cl_cholesky_batched).
+    Returns (L, info) with info the per-matrix LAPACK code (cuda int32)."""
+    A = _dev_batch(A, "A")
+    batch, n = A.shape[0], A.shape[1]
+    L = torch.empty_like(A) if out is None else out
+    info = torch.empty(batch, dtype=torch.int32, device=A.device)
+    with torch.cuda.device(A.device):
+        _bind_stream(A.device)
+        _check("stan_cl_cholesky_batched",
+               load().stan_cl_cholesky_batched(batch, n, A.data_ptr(), L.data_ptr(), info.data_ptr()))
+    return L, info
+
+
+def cholesky_adjoint_batched(L: torch.Tensor, Lbar: torch.Tensor,
+                             out: torch.Tensor | None = None) -> tuple[torch.Tensor, torch.Tensor]:
+    """A_bar_b = adjoint(L_b, L_bar_b) for (batch, n, n) tensors, n <= 128
+    (stan_cl_cholesky_adjoint_batched).  Returns (A_bar, info)."""
+    L = _dev_batch(L, "L")
+    Lbar = _dev_batch(Lbar, "Lbar")
+    batch, n = L.shape[0], L.shape[1]
+    Ab = torch.empty_like(L) if out is None else out
+    info = torch.empty(batch, dtype=torch.int32, device=L.device)
+    with torch.cuda.device(L.device):
+        _bind_stream(L.device)
+        _check("stan_cl_cholesky_adjoint_batched", load().stan_cl_cholesky_adjoint_batched(
+            batch, n, L.data_ptr(), Lbar.data_ptr(), Ab.data_ptr(), info.data_ptr()))
+    return Ab, info
 
 
 def cholesky_async(A: torch.Tensor, L: torch.Tensor, info: torch.Tensor | None = None) -> None:

@@ -691,6 +691,72 @@ int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alp
   return read_status();
 }
 
+// ---- NEXT-4: batched small matrices ----------------------------------------
+int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* L, int* info) {
+  if (batch < 0 || n < 0 || n > NB) return STAN_CL_EINVAL;
+  if (batch == 0 || n == 0) return STAN_CL_OK;
+  if (!A || !L) return STAN_CL_EINVAL;
+  const size_t bytes = (size_t)batch * (size_t)n * (size_t)n * sizeof(double);
+  if (A != L && ranges_overlap(A, L, bytes)) return STAN_CL_EINVAL;
+  int rc = ensure_ws(al(sizeof(int) * 64));
+  if (rc) return rc;
+  int* inf = info;
+  if (!inf) {
+    double* p = nullptr;
+    if ((rc = ensure_mat(4, sizeof(int) * (size_t)batch, &p))) return rc;
+    inf = (int*)p;
+  }
+  int* status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  CK(cudaMemsetAsync(inf, 0, sizeof(int) * (size_t)batch, st));
+  CK(potrf_batched(A, L, (int)n, batch, inf, st));
+  CK(batched_first_fail(inf, batch, status, st));
+  return read_status();
+}
+
+int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, const double* L_bar,
+                                     double* A_bar, int* info) {
+  if (batch < 0 || n < 0 || n > NB) return STAN_CL_EINVAL;
+  if (batch == 0 || n == 0) return STAN_CL_OK;
+  if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
+  const size_t bytes = (size_t)batch * (size_t)n * (size_t)n * sizeof(double);
+  if (L != A_bar && ranges_overlap(L, A_bar, bytes)) return STAN_CL_EINVAL;
+  if (L_bar != A_bar && ranges_overlap(L_bar, A_bar, bytes)) return STAN_CL_EINVAL;
+  int rc = ensure_ws(al(sizeof(int) * 64));
+  if (rc) return rc;
+  // padded 128 x 128 work tiles: Lp, Wp (-> T2), Dinv, T1 (-> T3); chunks bound
+  // the scratch and the 65535 grid-z limit of the batched products
+  const int64_t chunk = batch < 4096 ? batch : 4096;
+  const int64_t T2e = (int64_t)NB * NB;
+  double* w = nullptr;
+  if ((rc = ensure_mat(2, sizeof(double) * 4 * (size_t)chunk * (size_t)T2e, &w))) return rc;
+  double *Lp = w, *Wp = w + chunk * T2e, *Dinv = w + 2 * chunk * T2e, *T1 = w + 3 * chunk * T2e;
+  int* inf = info;
+  if (!inf) {
+    double* p = nullptr;
+    if ((rc = ensure_mat(4, sizeof(int) * (size_t)batch, &p))) return rc;
+    inf = (int*)p;
+  }
+  int* status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  CK(batched_check_diag(L, (int)n, batch, inf, st));
+  const int64_t nn = n * n;
+  for (int64_t b0 = 0; b0 < batch; b0 += chunk) {
+    const int64_t nb = batch - b0 < chunk ? batch - b0 : chunk;
+    CK(batched_pad(L + b0 * nn, L_bar + b0 * nn, (int)n, nb, Lp, Wp, st));
+    CK(tri_inverse_batched(Lp, NB, (int)nb, Dinv, status, st, NB, T2e, 1, T2e));
+    // P = D^T D_bar (lower tiles, mirrored); S = D^-T sym(P) D^-1
+    CK(gemm_small(NB, true, true, false, Lp, NB, Wp, NB, T1, NB, status, st, 1.0, (int)nb, T2e, T2e, T2e, true));
+    CK(gemm_small(NB, true, false, false, Dinv, NB, T1, NB, Wp, NB, status, st, 1.0, (int)nb, T2e, T2e, T2e));
+    CK(gemm_small(NB, false, false, false, Wp, NB, Dinv, NB, T1, NB, status, st, 1.0, (int)nb, T2e, T2e, T2e));
+    // A_bar = Phi(sym S), leading n x n block
+    CK(batched_phi_out(T1, (int)n, nb, A_bar + b0 * nn, st));
+  }
+  CK(batched_first_fail(inf, batch, status, st));
+  return read_status();
+}
+
 int stan_cl_gp_exp_quad_cov(int64_t n, const double* x, double alpha, double rho, double jitter,
                             double* K) {
   if (n < 0) return STAN_CL_EINVAL;

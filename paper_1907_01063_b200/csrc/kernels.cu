@@ -334,21 +334,28 @@ __device__ __forceinline__ int potrf_wblock(double* S, int c0, int lane, double*
   return bad;
 }
 
-__global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t ld, int64_t k0,
-                                                            int* status) {
-  if (*status != 0) return;
+// One tile: src (lds) -> dst (ldd), the leading nv x nv block (nv <= 128) is the
+// matrix; the rest of the 128 x 128 tile is identity padding (pivots 1, never
+// fails).  On failure status <- info_base + j + 1 (first failing column j).
+__device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, double* dst, int64_t ldd,
+                                                int nv, int* status, int64_t info_base) {
   extern __shared__ double S[];
   __shared__ double rc[NB];   // 1 / L[j][j]
   __shared__ double colb[32];
   __shared__ int fail_j;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double* base = W + k0 * ld + k0;
-  if ((((uintptr_t)base & 15) == 0) && ((ld & 1) == 0)) {
+  const double* base = src;
+  if (nv < NB) {
+    for (int idx = tid; idx < NB * NB; idx += 256) {
+      const int r = idx >> 7, c = idx & (NB - 1);
+      if (c <= r) S[r * TP + c] = (r < nv) ? base[(long long)r * lds + c] : (r == c ? 1.0 : 0.0);
+    }
+  } else if ((((uintptr_t)base & 15) == 0) && ((lds & 1) == 0)) {
 #pragma unroll 4
     for (int idx = tid; idx < NB * NB / 2; idx += 256) {
       const int r = idx >> 6, c = (idx & 63) << 1;
       if (c <= r) {
-        const double2 v = *reinterpret_cast<const double2*>(base + (long long)r * ld + c);
+        const double2 v = *reinterpret_cast<const double2*>(base + (long long)r * lds + c);
         S[r * TP + c] = v.x;
         S[r * TP + c + 1] = v.y;
       }
@@ -356,7 +363,7 @@ __global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t l
   } else {
     for (int idx = tid; idx < NB * NB; idx += 256) {
       const int r = idx >> 7, c = idx & (NB - 1);
-      if (c <= r) S[r * TP + c] = base[(long long)r * ld + c];
+      if (c <= r) S[r * TP + c] = base[(long long)r * lds + c];
     }
   }
   if (tid == 0) fail_j = -1;
@@ -421,20 +428,38 @@ __global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t l
     }
     __syncthreads();
   }
-  if ((((uintptr_t)base & 15) == 0) && ((ld & 1) == 0)) {
+  if (nv < NB) {
+    for (int idx = tid; idx < nv * nv; idx += 256) {
+      const int r = idx / nv, c = idx - r * nv;
+      dst[(long long)r * ldd + c] = (c <= r) ? S[r * TP + c] : 0.0;
+    }
+  } else if ((((uintptr_t)dst & 15) == 0) && ((ldd & 1) == 0)) {
 #pragma unroll 4
     for (int idx = tid; idx < NB * NB / 2; idx += 256) {
       const int r = idx >> 6, c = (idx & 63) << 1;
       const double2 v = make_double2(c <= r ? S[r * TP + c] : 0.0, c + 1 <= r ? S[r * TP + c + 1] : 0.0);
-      *reinterpret_cast<double2*>(base + (long long)r * ld + c) = v;  // strict upper of the tile: +0.0
+      *reinterpret_cast<double2*>(dst + (long long)r * ldd + c) = v;  // strict upper of the tile: +0.0
     }
   } else {
     for (int idx = tid; idx < NB * NB; idx += 256) {
       const int r = idx >> 7, c = idx & (NB - 1);
-      base[(long long)r * ld + c] = (c <= r) ? S[r * TP + c] : 0.0;
+      dst[(long long)r * ldd + c] = (c <= r) ? S[r * TP + c] : 0.0;
     }
   }
-  if (tid == 0 && fail_j >= 0) atomicCAS(status, 0, (int)(k0 + fail_j + 1));
+  if (tid == 0 && fail_j >= 0) atomicCAS(status, 0, (int)(info_base + fail_j + 1));
+}
+
+__global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t ld, int64_t k0,
+                                                            int* status) {
+  if (*status != 0) return;
+  double* base = W + k0 * ld + k0;
+  potrf_tile_body(base, ld, base, ld, NB, status, k0);
+}
+
+// NEXT-4: one CTA per independent n x n matrix (n <= 128), info[b] = LAPACK info
+__global__ void __launch_bounds__(256, 1) potrf_batched_kernel(const double* A, double* L, int n, int* info) {
+  const long long b = blockIdx.x;
+  potrf_tile_body(A + b * n * n, n, L + b * n * n, n, n, info + b, 0);
 }
 
 cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStream_t st) {
@@ -447,6 +472,20 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
     attr = true;
   }
   potrf_tile_kernel<<<1, 256, POTRF_SMEM, st>>>(W, ld, k0, status);
+  return cudaGetLastError();
+}
+
+cudaError_t potrf_batched(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st) {
+  Prof prof_(PROF_POTRF, (double)batch * n * n * n / 3.0, st, 8.0 * batch * n * (n + 1));
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(potrf_batched_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         POTRF_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  if (batch == 0) return cudaSuccess;
+  potrf_batched_kernel<<<(unsigned)batch, 256, POTRF_SMEM, st>>>(A, L, n, info);
   return cudaGetLastError();
 }
 
@@ -689,13 +728,15 @@ constexpr int TINV_SMEM = (TRI_PACKED + NB * TP) * (int)sizeof(double);
 
 __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, int64_t ld,
                                                              double* Dinv, int64_t ldo, int64_t ostride,
-                                                             int per, int64_t ohalf, const int* status) {
+                                                             int per, int64_t ohalf, int64_t istride,
+                                                             const int* status) {
   if (*status != 0) return;
   extern __shared__ double sm[];
   double* D = sm;               // packed lower: D[i][k] at i(i+1)/2 + k
   double* X = sm + TRI_PACKED;  // X[c][i] = (D^-1)[i][c]  (column c of the inverse, contiguous)
   const int b = blockIdx.x, c = threadIdx.x;
-  const double* src = L + (long long)b * NB * ld + (long long)b * NB;
+  // block b: the b-th diagonal block of L, or (istride > 0) the tile at b * istride
+  const double* src = istride > 0 ? L + (long long)b * istride : L + (long long)b * NB * ld + (long long)b * NB;
   for (int idx = c; idx < NB * NB; idx += NB) {
     const int i = idx >> 7, k = idx & (NB - 1);
     if (k <= i) D[i * (i + 1) / 2 + k] = src[(long long)i * ld + k];
@@ -721,7 +762,8 @@ __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, in
 }
 
 cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* Dinv,
-                                const int* status, cudaStream_t st, int64_t ldo, int64_t ostride, int per) {
+                                const int* status, cudaStream_t st, int64_t ldo, int64_t ostride, int per,
+                                int64_t istride) {
   Prof prof_(PROF_TRINV, (double)nblk * NB * NB * NB / 3.0, st, 12.0 * nblk * NB * NB);
   if (nblk == 0) return cudaSuccess;
   static bool attr = false;
@@ -734,7 +776,7 @@ cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* D
   if (ldo == 0) ldo = NB;
   if (ostride == 0) ostride = (int64_t)NB * NB;
   if (per < 1) per = 1;
-  tri_inverse_kernel<<<nblk, NB, TINV_SMEM, st>>>(L, ld, Dinv, ldo, ostride, per, NB * ldo + NB, status);
+  tri_inverse_kernel<<<nblk, NB, TINV_SMEM, st>>>(L, ld, Dinv, ldo, ostride, per, NB * ldo + NB, istride, status);
   return cudaGetLastError();
 }
 

@@ -101,7 +101,7 @@ cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double*
 // 256 x 256 blocks)
 cudaError_t tri_inverse_batched(const double* L, int64_t ld, int nblk, double* Dinv,
                                 const int* status, cudaStream_t st, int64_t ldo = 0, int64_t ostride = 0,
-                                int per = 1);
+                                int per = 1, int64_t istride = 0);
 // C[S x S] (ldc) = sign * op(A) op(B) over K = S, S in {128, 256}, batched over
 // `batch` problems with element strides sA/sB/sC.  a_t: A given as K x M;
 // a_tril: only the lower triangle of A's storage is read (upper taken as 0);
@@ -117,6 +117,18 @@ cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, co
                     cudaStream_t st, int n = 128);
 // status = first base+k+1 with !(L[k][k] > 0 && finite), k < n
 cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st, int64_t base = 0);
+
+// ---- NEXT-4: batched small matrices (n <= 128) ----
+// L_b = chol(A_b) for b < batch, n x n contiguous each (A may equal L); info[b]
+// (zeroed by the caller) = LAPACK info of matrix b
+cudaError_t potrf_batched(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st);
+// batched.cu: the adjoint of the batched factorization and helpers
+cudaError_t batched_pad(const double* L, const double* Lbar, int n, int64_t batch, double* Lp, double* Wp,
+                        cudaStream_t st);
+cudaError_t batched_check_diag(const double* L, int n, int64_t batch, int* info, cudaStream_t st);
+cudaError_t batched_phi_out(const double* S, int n, int64_t batch, double* Abar, cudaStream_t st);
+// status <- (first b with info[b] != 0) + 1, or 0
+cudaError_t batched_first_fail(const int* info, int64_t batch, int* status, cudaStream_t st);
 
 // ---- NEXT-1/NEXT-2 (gp.cu) ----
 // x = L^-1 b (trans = false) or L^-T b (trans = true); L lower, positive normal
