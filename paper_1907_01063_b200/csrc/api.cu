@@ -708,8 +708,12 @@ int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* 
   }
   int* status = (int*)g.ws;
   cudaStream_t st = g.stream;
-  CK(cudaMemsetAsync(inf, 0, sizeof(int) * (size_t)batch, st));
-  CK(potrf_batched(A, L, (int)n, batch, inf, st));
+  if (n <= 32) {
+    CK(potrf_batched_w32(A, L, (int)n, batch, inf, st));
+  } else {
+    CK(cudaMemsetAsync(inf, 0, sizeof(int) * (size_t)batch, st));
+    CK(potrf_batched(A, L, (int)n, batch, inf, st));
+  }
   CK(batched_first_fail(inf, batch, status, st));
   return read_status();
 }
@@ -724,6 +728,18 @@ int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, 
   if (L_bar != A_bar && ranges_overlap(L_bar, A_bar, bytes)) return STAN_CL_EINVAL;
   int rc = ensure_ws(al(sizeof(int) * 64));
   if (rc) return rc;
+  if (n <= 32) {  // one warp per matrix, no padded copies
+    int* inf = info;
+    if (!inf) {
+      double* p = nullptr;
+      if ((rc = ensure_mat(4, sizeof(int) * (size_t)batch, &p))) return rc;
+      inf = (int*)p;
+    }
+    cudaStream_t st = g.stream;
+    CK(adjoint_batched_w32(L, L_bar, A_bar, (int)n, batch, inf, st));
+    CK(batched_first_fail(inf, batch, (int*)g.ws, st));
+    return read_status();
+  }
   // padded 128 x 128 work tiles: Lp, Wp (-> T2), Dinv, T1 (-> T3); chunks bound
   // the scratch and the 65535 grid-z limit of the batched products
   const int64_t chunk = batch < 4096 ? batch : 4096;

@@ -475,6 +475,141 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
   return cudaGetLastError();
 }
 
+// ---- NEXT-4, n <= 32: one WARP per matrix, everything in registers/shared ----
+// forward: lane r holds row r (identity padded to 32) and runs the warp
+// factorization of the diagonal-tile kernel (same arithmetic)
+__global__ void __launch_bounds__(128) potrf_w32_kernel(const double* A, double* L, int n, int64_t batch,
+                                                       int* info) {
+  __shared__ double col[4][32], rcs[4][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+  if (b >= batch) return;  // warp-uniform
+  const double* Ab = A + b * n * n;
+  double row[32];
+#pragma unroll
+  for (int c = 0; c < 32; ++c)
+    row[c] = (lane < n) ? ((c <= lane && c < n) ? Ab[(int64_t)lane * n + c] : 0.0) : (c == lane ? 1.0 : 0.0);
+  int bad = -1;
+  potrf_wstep<0>(row, lane, rcs[warp], col[warp], bad);
+  double* Lb = L + b * n * n;
+  if (lane < n) {
+#pragma unroll
+    for (int c = 0; c < 32; ++c)
+      if (c < n) Lb[(int64_t)lane * n + c] = (c <= lane) ? row[c] : 0.0;
+  }
+  if (lane == 0) info[b] = bad >= 0 ? bad + 1 : 0;
+}
+
+// adjoint: the diagonal-block step of the blocked gradient on the whole
+// (<= 32 x 32, identity/zero padded) matrix:
+//   P = D^T D_bar; M = sym(tril P); X = D^-1 (substitution by columns);
+//   T = M X; S = X^T T; A_bar = Phi(tril S)
+constexpr int W32P = 33;  // shared pitch (odd: column reads conflict-free)
+__global__ void __launch_bounds__(128) adjoint_w32_kernel(const double* L, const double* Lbar, double* Abar,
+                                                         int n, int64_t batch, int* info) {
+  extern __shared__ double smw[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t b = (int64_t)blockIdx.x * 4 + warp;
+  if (b >= batch) return;
+  double* D = smw + warp * 3 * 32 * W32P;  // D, later T
+  double* M = D + 32 * W32P;               // D_bar, later M
+  double* X = M + 32 * W32P;               // D^-1
+  const double* Lb = L + b * n * n;
+  const double* Wb = Lbar + b * n * n;
+#pragma unroll 4
+  for (int c = 0; c < 32; ++c) {
+    const bool in = lane < n && c < n && c <= lane;
+    D[lane * W32P + c] = in ? Lb[(int64_t)lane * n + c] : (lane >= n && c == lane ? 1.0 : 0.0);
+    M[lane * W32P + c] = in ? Wb[(int64_t)lane * n + c] : 0.0;
+  }
+  const double dii = D[lane * W32P + lane];
+  const unsigned badm = __ballot_sync(0xffffffffu, lane < n && (!(dii > 0.0) || !isfinite(dii)));
+  if (lane == 0) info[b] = badm ? __ffs(badm) : 0;
+  __syncwarp();
+  // P row `lane`, lower part: P[i][j] = sum_k D[k][i] D_bar[k][j]
+  double acc[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    const double dki = D[k * W32P + lane];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = fma(dki, M[k * W32P + j], acc[j]);
+  }
+  // X = D^-1, column `lane`: x_c = 1/D_cc, x_i = -(sum_{k=c}^{i-1} D_ik x_k) / D_ii
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k)
+      if (k >= lane) s = fma(D[i * W32P + k], x[k], s);
+    const double di = D[i * W32P + i];
+    x[i] = (i < lane) ? 0.0 : (i == lane ? 1.0 / di : -s / di);
+  }
+  __syncwarp();
+  // M = sym(tril P): row lane from acc (j <= lane), mirrored entries via shared
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j <= lane) M[lane * W32P + j] = acc[j];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) X[i * W32P + lane] = x[i];
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 32; ++j)
+    if (j > lane) M[lane * W32P + j] = M[j * W32P + lane];
+  __syncwarp();
+  // T = M X, row lane
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    const double mik = M[lane * W32P + k];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = fma(mik, X[k * W32P + j], acc[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) D[lane * W32P + j] = acc[j];  // T over D
+  __syncwarp();
+  // S = X^T T, row lane: S[i][j] = sum_k X[k][i] T[k][j];  A_bar = Phi(tril S)
+#pragma unroll
+  for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < 32; ++k) {
+    const double xki = X[k * W32P + lane];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) acc[j] = fma(xki, D[k * W32P + j], acc[j]);
+  }
+  double* Ab = Abar + b * n * n;
+  if (lane < n) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j)
+      if (j < n) Ab[(int64_t)lane * n + j] = (j < lane) ? acc[j] : (j == lane ? 0.5 * acc[j] : 0.0);
+  }
+}
+
+cudaError_t potrf_batched_w32(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st) {
+  Prof prof_(PROF_POTRF, (double)batch * n * n * n / 3.0, st, 8.0 * batch * n * (n + 1));
+  if (batch == 0) return cudaSuccess;
+  potrf_w32_kernel<<<(unsigned)((batch + 3) / 4), 128, 0, st>>>(A, L, n, batch, info);
+  return cudaGetLastError();
+}
+
+cudaError_t adjoint_batched_w32(const double* L, const double* Lbar, double* Abar, int n, int64_t batch, int* info,
+                                cudaStream_t st) {
+  Prof prof_(PROF_SMALL, (double)batch * 2.0 * n * n * n, st, 24.0 * batch * n * n);
+  if (batch == 0) return cudaSuccess;
+  constexpr int smem = 4 * 3 * 32 * W32P * (int)sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(adjoint_w32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  adjoint_w32_kernel<<<(unsigned)((batch + 3) / 4), 128, smem, st>>>(L, Lbar, Abar, n, batch, info);
+  return cudaGetLastError();
+}
+
 cudaError_t potrf_batched(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st) {
   Prof prof_(PROF_POTRF, (double)batch * n * n * n / 3.0, st, 8.0 * batch * n * (n + 1));
   static bool attr = false;

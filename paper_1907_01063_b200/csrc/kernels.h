@@ -122,6 +122,10 @@ cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cuda
 // L_b = chol(A_b) for b < batch, n x n contiguous each (A may equal L); info[b]
 // (zeroed by the caller) = LAPACK info of matrix b
 cudaError_t potrf_batched(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st);
+// n <= 32: one warp per matrix (info written, no zeroing needed)
+cudaError_t potrf_batched_w32(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st);
+cudaError_t adjoint_batched_w32(const double* L, const double* Lbar, double* Abar, int n, int64_t batch, int* info,
+                                cudaStream_t st);
 // batched.cu: the adjoint of the batched factorization and helpers
 cudaError_t batched_pad(const double* L, const double* Lbar, int n, int64_t batch, double* Lp, double* Wp,
                         cudaStream_t st);

@@ -28,7 +28,8 @@ def relf(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("batch,n", [(1, 1), (3, 2), (7, 5), (257, 64), (33, 100), (20, 128)])
+@pytest.mark.parametrize("batch,n", [(1, 1), (3, 2), (7, 5), (1001, 17), (64, 32), (257, 64), (33, 100),
+                                     (20, 128)])
 def test_cholesky_batched_parity(sc, batch, n):
     A = se_batch(batch, n)
     L, info = sc.cholesky_batched(torch.from_numpy(A).cuda())
@@ -61,7 +62,7 @@ def test_cholesky_batched_integer_exact_in_place_and_failures(sc):
         assert np.array_equal(got[b], L0[b])
 
 
-@pytest.mark.parametrize("batch,n", [(1, 1), (5, 3), (300, 64), (9, 100), (17, 128)])
+@pytest.mark.parametrize("batch,n", [(1, 1), (5, 3), (999, 20), (64, 32), (300, 64), (9, 100), (17, 128)])
 def test_cholesky_adjoint_batched_parity(sc, batch, n):
     A = se_batch(batch, n, seed0=500)
     Ls = np.stack([oracle.cholesky(a) for a in A])
@@ -77,9 +78,11 @@ def test_cholesky_adjoint_batched_parity(sc, batch, n):
     assert relf(Ab[0], single) <= 1e-13
 
 
-def test_cholesky_adjoint_batched_integer_exact_inplace_chunks(sc):
-    # integer-exact banded family, a batch larger than one 4096 chunk, in place
-    n, batch = 16, 4100
+@pytest.mark.parametrize("n", [16, 48])
+def test_cholesky_adjoint_batched_integer_exact_inplace_chunks(sc, n):
+    # integer-exact banded family, a batch larger than one 4096 chunk (n = 48:
+    # the padded path), in place; n = 16 runs one warp per matrix
+    batch = 4100
     L1 = inputs.unit_lower_pm1(n, seed=3, band=2)
     W1 = inputs.int_lbar(n, seed=4)
     want = oracle.cholesky_adjoint(L1, W1)
