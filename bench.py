@@ -44,7 +44,7 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
                0x100: "display_clock_setting"}
 
 
-def config(n: int, world: int, mode: str = "single") -> dict:
+def config(n: int, world: int, mode: str = "single", grid: tuple = (1, 1)) -> dict:
     return {
         "workload": f"SE-kernel GP covariance n={n} (1-D x~U(-10,10), alpha=rho=1, jitter 1e-6): "
                     "SE build + Cholesky + adjoint (BASELINE.json configs[3])",
@@ -55,8 +55,9 @@ def config(n: int, world: int, mode: str = "single") -> dict:
         "l2": "inputs exceed L2 (one n x n FP64 matrix = %.1f GiB vs 126 MB L2); no flush needed" % (8 * n * n / 2 ** 30),
         "parallelism": {"single": "single GPU",
                         "replicas": f"replicas: {world} independent problems, one per GPU",
-                        "dist": f"block-cyclic 256-wide block columns over {world} GPUs (P=1, Q={world}), "
-                                "NCCL broadcasts of panels / C_bar D^-1 / sym(S)"}[mode],
+                        "dist": f"2-D block-cyclic 256x256 tiles over {world} GPUs (P={grid[0]} x Q={grid[1]}), "
+                                "NCCL row/column broadcasts of panels / C_bar D^-1 / L rows / sym(S), "
+                                "column reductions of C_bar^T [B C]"}[mode],
     }
 
 
@@ -200,12 +201,12 @@ def bench_reference(args, rank: int, world: int):
     print(json.dumps(line), flush=True)
 
 
-def setup_dist(sc, world: int, local_rank: int) -> bool:
-    """NCCL communicator of the library; every rank must succeed, else replicas."""
+def setup_dist(sc, world: int, local_rank: int, grid=None) -> bool:
+    """NCCL communicators of the library (P x Q grid); every rank must succeed, else replicas."""
     import torch
     ok = 1
     try:
-        sc.dist_init_from_torch()
+        sc.dist_init_from_torch(None, *(grid or (None, None)))
     except Exception as e:  # noqa: BLE001
         print(f"[bench] dist init failed on this rank: {e}", file=sys.stderr, flush=True)
         ok = 0
@@ -227,28 +228,32 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
     mode = "single"
     if world > 1:
         mode = "replicas"
-        if args.mode in ("auto", "dist") and n % sc.DIST_BLOCK == 0 and setup_dist(sc, world, local_rank):
+        grid = tuple(int(v) for v in args.grid.lower().split("x")) if args.grid else sc.dist_grid(world)
+        if args.mode in ("auto", "dist") and n % sc.DIST_BLOCK == 0 and grid[0] * grid[1] == world \
+                and setup_dist(sc, world, local_rank, grid):
             mode = "dist"
     e2e_fn = None
     if mode == "dist":
-        # one problem of order n, block columns cyclic over the ranks (strong scaling)
+        # one problem of order n, 256 x 256 tiles 2-D block-cyclic over the P x Q grid (strong scaling)
+        P, Q = grid
+        gp, gq = divmod(rank, Q)
         x = torch.from_numpy(inputs.gp_x(n)).to(dev)
-        w = sc.dist_owned_blocks(n, world, rank) * sc.DIST_BLOCK
-        Lbar_loc = sc.dist_scatter(torch.from_numpy(inputs.lbar(n)), world, rank).contiguous().to(dev)
-        K_loc = torch.empty((n, w), dtype=torch.float64, device=dev)
+        hrows, w = sc.dist_local_shape(n, P, Q, gp, gq)
+        Lbar_loc = sc.dist_scatter2(torch.from_numpy(inputs.lbar(n)), P, Q, gp, gq).contiguous().to(dev)
+        K_loc = torch.empty((hrows, w), dtype=torch.float64, device=dev)
         W_loc = torch.empty_like(K_loc)
 
         def step():
-            sc.gp_exp_quad_cov_cols(x, K_loc, world, rank, ALPHA, RHO, JITTER)   # F0 (owned columns)
+            sc.gp_exp_quad_cov_tiles(x, K_loc, P, Q, gp, gq, ALPHA, RHO, JITTER)  # F0 (owned tiles)
             sc.dist_cholesky(K_loc, n)                                          # F1-F4, NCCL panel broadcasts
             W_loc.copy_(Lbar_loc)
             sc.dist_cholesky_adjoint(K_loc, W_loc, n)                           # R0-R5, NCCL broadcasts
 
-        Kh = torch.empty((n, w), dtype=torch.float64).pin_memory()
+        Kh = torch.empty((hrows, w), dtype=torch.float64).pin_memory()
         Lbh = Lbar_loc.cpu().pin_memory()
         Lh = torch.empty_like(Kh).pin_memory()
         Abh = torch.empty_like(Kh).pin_memory()
-        sc.gp_exp_quad_cov_cols(x, K_loc, world, rank, ALPHA, RHO, JITTER)
+        sc.gp_exp_quad_cov_tiles(x, K_loc, P, Q, gp, gq, ALPHA, RHO, JITTER)
         Kh.copy_(K_loc)
 
         def e2e_fn():
@@ -258,8 +263,8 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
             W_loc.copy_(Lbh, non_blocking=True)
             sc.dist_cholesky_adjoint(K_loc, W_loc, n)
             Abh.copy_(W_loc, non_blocking=True)
-        e2e_bytes = (2 * 8 * n * w, 2 * 8 * n * w)
-        e2e_path = "per rank: pinned H2D of its K and L_bar block columns, dist_cholesky + dist_cholesky_adjoint, D2H of L and A_bar"
+        e2e_bytes = (2 * 8 * hrows * w, 2 * 8 * hrows * w)
+        e2e_path = "per rank: pinned H2D of its K and L_bar tiles, dist_cholesky + dist_cholesky_adjoint, D2H of L and A_bar"
     else:
         xs, ls = replica_seeds(rank)
         x = torch.from_numpy(inputs.gp_x(n, seed=xs)).to(dev)
@@ -386,7 +391,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
         "scaling": "strong" if mode == "dist" else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config(n, world, mode),
+        "config": config(n, world, mode, grid if mode == "dist" else (1, 1)),
         "fp64_peak_frac": (jobs * flops / (ms_max / 1e3) / 1e12) / (FP64_PEAK_TFLOPS * world),
         "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": clocks,
@@ -405,6 +410,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--oracle-n", type=int, default=ORACLE_SAMPLE_N)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--grid", default="", help="N>1 dist mode: process grid PxQ (default: 1x2, 2x2, 2x4 ...)")
     ap.add_argument("--mode", choices=["auto", "dist", "replicas"], default="auto",
                     help="N>1: distributed (strong scaling, default) or independent replicas")
     args = ap.parse_args()

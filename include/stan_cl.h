@@ -114,22 +114,36 @@ int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_ba
 
 /*
  * ---- multi-GPU (one process per GPU) ----
- * Layout: block-cyclic by 256-wide block COLUMNS over G ranks (process grid
- * P = 1, Q = G): global block column J (columns J*256 .. J*256+255) is stored on
- * rank J % G as local block column J / G of a row-major n x ld_local array
- * (ld_local >= 256 * number of owned block columns).  n must be a multiple of
- * 256.  Only broadcasts cross NVLink (each factored panel; C_bar D^-1 and
- * sym(S) per adjoint step).  Outputs: the lower triangle of every owned block
- * column is written (+0.0 above the diagonal inside the 256 x 256 diagonal
- * tiles); the part of a block column above its diagonal tile is not touched.
+ * Layout: 2-D block-cyclic by 256 x 256 tiles over a P x Q process grid
+ * (nranks = P * Q; rank r is grid position (p, q) = (r / Q, r % Q)).  Tile
+ * (I, J) (rows I*256.., columns J*256..) lives on rank (I % P, J % Q) as local
+ * tile (I / P, J / Q) of a row-major (R_p * 256) x ld_local array, where R_p
+ * (C_q) is the number of block indices I < n/256 with I % P == p (J % Q == q)
+ * and ld_local >= 256 * C_q.  P = 1 is block-column cyclic (whole columns per
+ * rank).  n must be a multiple of 256.  Only the lower tiles (I >= J) are read
+ * or written; +0.0 is written above the diagonal inside the diagonal tiles.
+ * Per forward step k: the diagonal owner factors L_kk
+ * (column broadcast), process column k % Q solves its panel tiles, each
+ * process row receives its panel rows (row broadcast), each process column
+ * receives the panel tiles of its block columns (column broadcasts, P > 1),
+ * every rank updates its lower trailing tiles.  Per adjoint step
+ * (PAPER.md:298-322): broadcasts of D^-1 (column), C_bar D^-1 (row), L's row
+ * block (column), sym(S) (row), and a column REDUCE (ncclReduce, sum) of the
+ * partial products C_bar^T [B C] to the owners of the block row (P > 1).
  *   stan_cl_dist_get_unique_id  rank 0; the 128-byte NCCL id is shipped to the
  *                               other ranks by the caller (torch.distributed)
- *   stan_cl_dist_init           P must be 1 and Q == nranks; the CUDA device of
- *                               the calling thread is the rank's device
+ *   stan_cl_dist_init           P, Q >= 1, P * Q == nranks; builds the world,
+ *                               row (ncclCommSplit color p) and column (color q)
+ *                               communicators; the CUDA device of the calling
+ *                               thread is the rank's device
  *   stan_cl_dist_cholesky       in place on A_local (nb: 0 or 256)
- *   stan_cl_dist_cholesky_adjoint  L_local read-only; Lbar_to_Abar_local in place
+ *   stan_cl_dist_cholesky_adjoint  L_local read-only; Lbar_to_Abar_local in
+ *                               place; both with leading dimension ld_local
+ * Every rank must make the same sequence of calls (collectives inside).
  * Return values as the single-GPU calls (numerical status all-reduced with max);
- * STAN_CL_ENCCL when NCCL cannot be loaded or fails.
+ * STAN_CL_ENCCL when NCCL cannot be loaded or fails; STAN_CL_EINVAL for a bad
+ * grid, n % 256 != 0, or ld_local too small.  Library-owned scratch: about
+ * (R_p + 1) * 256^2 doubles (+ C_q * 256^2 * (P + 3) for P > 1 / the adjoint).
  */
 int stan_cl_dist_get_unique_id(void* out128);
 int stan_cl_dist_init(int nranks, int rank, const void* id128, int P, int Q);
@@ -137,12 +151,21 @@ int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local);
 int stan_cl_dist_cholesky_adjoint(int64_t n, int nb, const double* L_local, double* Lbar_to_Abar_local,
                                   int64_t ld_local);
 int stan_cl_dist_finalize(void);
-/* the SE covariance's owned block columns for rank q of G (the layout above) */
+/* the SE covariance's tiles for rank (p, q) of a P x Q grid (the layout above;
+ * every local element is written, including tiles above the diagonal) */
+int stan_cl_gp_exp_quad_cov_tiles(int64_t n, const double* x, double alpha, double rho, double jitter,
+                                  double* K_local, int64_t ld_local, int P, int Q, int p, int q);
+/* the 1 x G special case (block columns of rank q) */
 int stan_cl_gp_exp_quad_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter,
                                  double* K_local, int64_t ld_local, int G, int q);
-/* The same distributed algorithms with G simulated ranks in this process on
- * the current device (broadcasts become device copies): the layouts above,
- * one local array per rank.  For testing the multi-GPU path on one GPU. */
+/* The same distributed algorithms with all P * Q ranks simulated in this
+ * process on the current device (broadcasts become device copies, the column
+ * reduce fixed-order additions): one local array per rank, locals[p * Q + q],
+ * all with leading dimension ld_local.  For testing the multi-GPU path on one
+ * GPU.  The *_sim_* forms are the 1 x G grid. */
+int stan_cl_dist_sim2_cholesky(int64_t n, int P, int Q, double* const* A_locals, int64_t ld_local);
+int stan_cl_dist_sim2_cholesky_adjoint(int64_t n, int P, int Q, const double* const* L_locals,
+                                       double* const* W_locals, int64_t ld_local);
 int stan_cl_dist_sim_cholesky(int64_t n, int G, double* const* A_locals, int64_t ld_local);
 int stan_cl_dist_sim_cholesky_adjoint(int64_t n, int G, const double* const* L_locals, double* const* W_locals,
                                       int64_t ld_local);

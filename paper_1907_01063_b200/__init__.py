@@ -69,6 +69,9 @@ SIGNATURES = {
     "stan_cl_dist_sim_cholesky": (_I, [_I64, _I, _P, _I64]),
     "stan_cl_gp_exp_quad_cov_cols": (_I, [_I64, _P, _D, _D, _D, _P, _I64, _I, _I]),
     "stan_cl_dist_sim_cholesky_adjoint": (_I, [_I64, _I, _P, _P, _I64]),
+    "stan_cl_dist_sim2_cholesky": (_I, [_I64, _I, _I, _P, _I64]),
+    "stan_cl_dist_sim2_cholesky_adjoint": (_I, [_I64, _I, _I, _P, _P, _I64]),
+    "stan_cl_gp_exp_quad_cov_tiles": (_I, [_I64, _P, _D, _D, _D, _P, _I64, _I, _I, _I, _I]),
     "stan_cl_version": (_I, []),
 }
 
@@ -301,25 +304,60 @@ DIST_BLOCK = 256
 
 
 def dist_owned_blocks(n: int, G: int, q: int) -> int:
+    """Block indices I < n/256 with I % G == q (local block rows / columns of a grid index)."""
     T = n // DIST_BLOCK
     return (T - q + G - 1) // G if q < T else 0
 
 
-def dist_scatter(A: torch.Tensor, G: int, q: int) -> torch.Tensor:
-    """Rank q's local array (block columns J = q, q+G, ... of A, contiguous)."""
+def dist_grid(G: int) -> tuple[int, int]:
+    """Default P x Q process grid for G ranks: 1x1, 1x2, 2x2, 2x4, ...
+    P <= Q, P the largest divisor of G with P*P <= G."""
+    P = max(d for d in range(1, int(G ** 0.5) + 1) if G % d == 0)
+    return P, G // P
+
+
+def dist_local_shape(n: int, P: int, Q: int, p: int, q: int) -> tuple[int, int]:
+    """(rows, cols) of rank (p, q)'s local array: tiles (I, J), I % P == p, J % Q == q."""
+    return dist_owned_blocks(n, P, p) * DIST_BLOCK, dist_owned_blocks(n, Q, q) * DIST_BLOCK
+
+
+def _tiles(n: int, G: int, g: int) -> list:
+    return list(range(g, n // DIST_BLOCK, G))
+
+
+def dist_scatter2(A: torch.Tensor, P: int, Q: int, p: int, q: int, width: int | None = None) -> torch.Tensor:
+    """Rank (p, q)'s local array of the 2-D block-cyclic layout (contiguous; optional
+    zero-padded width = leading dimension)."""
     n = A.shape[0]
-    cols = [A[:, J * DIST_BLOCK:(J + 1) * DIST_BLOCK] for J in range(q, n // DIST_BLOCK, G)]
-    return torch.cat(cols, dim=1).contiguous() if cols else A.new_empty((n, 0))
+    rows, cols = dist_local_shape(n, P, Q, p, q)
+    out = A.new_zeros((rows, width if width is not None else cols))
+    B = DIST_BLOCK
+    for li, I in enumerate(_tiles(n, P, p)):
+        for lj, J in enumerate(_tiles(n, Q, q)):
+            out[li * B:(li + 1) * B, lj * B:(lj + 1) * B] = A[I * B:(I + 1) * B, J * B:(J + 1) * B]
+    return out
+
+
+def dist_gather2(locals_: list, n: int, P: int, Q: int) -> torch.Tensor:
+    """Inverse of dist_scatter2 over all P*Q ranks (locals_[p*Q + q])."""
+    B = DIST_BLOCK
+    out = locals_[0].new_zeros((n, n))
+    for r, loc in enumerate(locals_):
+        p, q = divmod(r, Q)
+        for li, I in enumerate(_tiles(n, P, p)):
+            for lj, J in enumerate(_tiles(n, Q, q)):
+                out[I * B:(I + 1) * B, J * B:(J + 1) * B] = loc[li * B:(li + 1) * B, lj * B:(lj + 1) * B]
+    return out
+
+
+def dist_scatter(A: torch.Tensor, G: int, q: int) -> torch.Tensor:
+    """Rank q's local array of the 1 x G grid (block columns J = q, q+G, ... of A)."""
+    return dist_scatter2(A, 1, G, 0, q)
 
 
 def dist_gather(locals_: list, n: int) -> torch.Tensor:
     """Inverse of dist_scatter over all ranks."""
-    G = len(locals_)
-    out = locals_[0].new_zeros((n, n))
-    for q, Lq in enumerate(locals_):
-        for i, J in enumerate(range(q, n // DIST_BLOCK, G)):
-            out[:, J * DIST_BLOCK:(J + 1) * DIST_BLOCK] = Lq[:, i * DIST_BLOCK:(i + 1) * DIST_BLOCK]
-    return out
+    return dist_gather2(locals_, n, 1, len(locals_))
 
 
 def _ptr_array(ts):
@@ -327,32 +365,49 @@ def _ptr_array(ts):
     return arr
 
 
-def dist_sim_cholesky(A_locals: list, n: int) -> int:
-    """Distributed forward with len(A_locals) simulated ranks on this device (in place)."""
-    G = len(A_locals)
-    ld = max(t.shape[1] for t in A_locals)
-    assert all(t.shape[1] == ld and t.is_contiguous() for t in A_locals), "equal-width local arrays"
+def _sim_ld(ts) -> int:
+    ld = ts[0].stride(0)
+    assert all(t.stride(0) == ld and t.stride(1) == 1 for t in ts), "equal leading dimensions, row-major"
+    return ld
+
+
+def dist_sim2_cholesky(A_locals: list, n: int, P: int, Q: int) -> int:
+    """Distributed forward on a P x Q grid simulated on this device (A_locals[p*Q + q], in place)."""
+    assert len(A_locals) == P * Q
+    ld = _sim_ld(A_locals)
     with torch.cuda.device(A_locals[0].device):
         _bind_stream(A_locals[0].device)
-        return _check("stan_cl_dist_sim_cholesky",
-                      load().stan_cl_dist_sim_cholesky(n, G, ctypes.cast(_ptr_array(A_locals), ctypes.c_void_p), ld))
+        return _check("stan_cl_dist_sim2_cholesky", load().stan_cl_dist_sim2_cholesky(
+            n, P, Q, ctypes.cast(_ptr_array(A_locals), ctypes.c_void_p), ld))
 
 
-def dist_sim_cholesky_adjoint(L_locals: list, W_locals: list, n: int) -> int:
-    G = len(L_locals)
-    ld = max(t.shape[1] for t in L_locals)
+def dist_sim2_cholesky_adjoint(L_locals: list, W_locals: list, n: int, P: int, Q: int) -> int:
+    assert len(L_locals) == len(W_locals) == P * Q
+    ld = _sim_ld(list(L_locals) + list(W_locals))
     with torch.cuda.device(L_locals[0].device):
         _bind_stream(L_locals[0].device)
-        return _check("stan_cl_dist_sim_cholesky_adjoint", load().stan_cl_dist_sim_cholesky_adjoint(
-            n, G, ctypes.cast(_ptr_array(L_locals), ctypes.c_void_p),
+        return _check("stan_cl_dist_sim2_cholesky_adjoint", load().stan_cl_dist_sim2_cholesky_adjoint(
+            n, P, Q, ctypes.cast(_ptr_array(L_locals), ctypes.c_void_p),
             ctypes.cast(_ptr_array(W_locals), ctypes.c_void_p), ld))
 
 
-def dist_init_from_torch(group=None) -> None:
-    """NCCL communicator for the library from an initialised torch.distributed group:
-    rank 0 creates the id, torch ships it, every rank joins (P = 1, Q = world)."""
+def dist_sim_cholesky(A_locals: list, n: int) -> int:
+    """Distributed forward with len(A_locals) simulated ranks (1 x G grid) on this device."""
+    return dist_sim2_cholesky(A_locals, n, 1, len(A_locals))
+
+
+def dist_sim_cholesky_adjoint(L_locals: list, W_locals: list, n: int) -> int:
+    return dist_sim2_cholesky_adjoint(L_locals, W_locals, n, 1, len(L_locals))
+
+
+def dist_init_from_torch(group=None, P: int | None = None, Q: int | None = None) -> tuple[int, int]:
+    """NCCL communicators for the library from an initialised torch.distributed group:
+    rank 0 creates the id, torch ships it, every rank joins the P x Q grid
+    (default dist_grid(world)); returns (P, Q).  Rank r is grid position (r // Q, r % Q)."""
     import torch.distributed as dist
     rank, world = dist.get_rank(group), dist.get_world_size(group)
+    if P is None or Q is None:
+        P, Q = dist_grid(world)
     try:
         import nvidia.nccl
         libdir = os.path.join(list(nvidia.nccl.__path__)[0], "lib", "libnccl.so.2")
@@ -365,18 +420,26 @@ def dist_init_from_torch(group=None) -> None:
     obj = [bytes(buf)]
     dist.broadcast_object_list(obj, src=0, group=group)
     idb = (ctypes.c_char * 128).from_buffer_copy(obj[0])
-    _check("stan_cl_dist_init", load().stan_cl_dist_init(world, rank, ctypes.cast(idb, ctypes.c_void_p), 1, world))
+    _check("stan_cl_dist_init", load().stan_cl_dist_init(world, rank, ctypes.cast(idb, ctypes.c_void_p), P, Q))
+    return P, Q
+
+
+def gp_exp_quad_cov_tiles(x: torch.Tensor, K_local: torch.Tensor, P: int, Q: int, p: int, q: int,
+                          alpha: float = 1.0, rho: float = 1.0, jitter: float = 0.0) -> torch.Tensor:
+    """Rank (p, q)'s tiles of the SE covariance (2-D block-cyclic), into K_local (rows x ld)."""
+    n = x.shape[0]
+    with torch.cuda.device(x.device):
+        _bind_stream(x.device)
+        _check("stan_cl_gp_exp_quad_cov_tiles", load().stan_cl_gp_exp_quad_cov_tiles(
+            n, x.data_ptr(), float(alpha), float(rho), float(jitter), K_local.data_ptr(), K_local.stride(0),
+            P, Q, p, q))
+    return K_local
 
 
 def gp_exp_quad_cov_cols(x: torch.Tensor, K_local: torch.Tensor, G: int, q: int, alpha: float = 1.0,
                          rho: float = 1.0, jitter: float = 0.0) -> torch.Tensor:
-    """Rank q's owned block columns of the SE covariance, into K_local (n x ld)."""
-    n = x.shape[0]
-    with torch.cuda.device(x.device):
-        _bind_stream(x.device)
-        _check("stan_cl_gp_exp_quad_cov_cols", load().stan_cl_gp_exp_quad_cov_cols(
-            n, x.data_ptr(), float(alpha), float(rho), float(jitter), K_local.data_ptr(), K_local.stride(0), G, q))
-    return K_local
+    """Rank q's owned block columns of the SE covariance (1 x G grid), into K_local (n x ld)."""
+    return gp_exp_quad_cov_tiles(x, K_local, 1, G, 0, q, alpha, rho, jitter)
 
 
 def dist_cholesky(A_local: torch.Tensor, n: int) -> int:
@@ -387,6 +450,7 @@ def dist_cholesky(A_local: torch.Tensor, n: int) -> int:
 
 
 def dist_cholesky_adjoint(L_local: torch.Tensor, W_local: torch.Tensor, n: int) -> int:
+    assert L_local.stride(0) == W_local.stride(0), "L_local and W_local share the leading dimension"
     with torch.cuda.device(L_local.device):
         _bind_stream(L_local.device)
         return _check("stan_cl_dist_cholesky_adjoint", load().stan_cl_dist_cholesky_adjoint(

@@ -19,6 +19,7 @@
 #include <cstring>
 #include <algorithm>
 #include <map>
+#include <numeric>
 #include <tuple>
 #include <mutex>
 #include <vector>
@@ -999,32 +1000,46 @@ int stan_cl_version(void) { return 100; }
 }  // extern "C"
 
 // ============================================================ multi-GPU layer
-// Distributed factorisation and adjoint over G ranks (one process per GPU),
-// block-cyclic by 256-wide block COLUMNS (process grid P = 1, Q = G): block
-// column J lives on rank J % G as local block column J / G of a row-major
-// n x (ncols_local) array.  This is the 2-D block-cyclic layout of
-// SURVEY.md §8(e) with P = 1: for FP64 on NVSwitch the traffic it needs (every
-// rank receives each factored panel once, ~4 n^2 bytes per call) is < 3% of the
-// compute time at n = 65536, and both sweeps then need only BROADCASTS:
-//   forward step k:  owner(k) factors its panel (POTRF + TRSM) -> broadcast the
-//                    panel -> every rank updates its own block columns J > k
-//   adjoint step k:  owner(j) forms C_bar D^-1 -> broadcast -> every rank updates
-//                    its B_bar columns and contracts its own [B C] columns (the
-//                    long K = m dimension is local, so no reduction) -> owner
-//                    runs the symbolic diagonal step -> broadcast sym(S) ->
-//                    every rank updates its R_bar columns.
-// The same code drives (a) NCCL over NVLink (one local rank per process) and
-// (b) a single-process simulation of G ranks on one device (broadcast = device
-// copies), which is what the tests exercise on a one-GPU box.
+// Distributed factorisation and adjoint over a P x Q process grid (one process
+// per GPU), 2-D block-cyclic by 256 x 256 tiles (ScaLAPACK
+// PDPOTRF style): tile (I, J) lives on rank (I % P, J % Q) = global rank
+// (I % P) * Q + J % Q, as local tile (I / P, J / Q) of a row-major
+// (R_p * 256) x (C_q * 256) array (R_p / C_q = number of block rows / columns
+// with I % P == p / J % Q == q).  Only the lower tiles (I >= J) are read or
+// written.  P = 1 is block-column cyclic (every rank holds whole columns).
+//
+//   forward step k
+//     diagonal owner (k%P, k%Q): L_kk = chol(A_kk)   -> column broadcast
+//     process column k%Q: L_Ik = A_Ik L_kk^-T for its rows I > k
+//     row broadcast of those panel rows along every process row
+//     column exchange: rank (p', q) sends the panel tiles L_Jk with J % Q == q
+//       to its process column (P > 1 only)
+//     every rank: A_IJ -= L_Ik L_Jk^T on its lower tiles I >= J > k
+//   adjoint step for block jb
+//     column broadcast of D^-1 (column jb%Q); C_bar D^-1 there
+//     row broadcast of C_bar D^-1; column broadcast of L's row block jb
+//     every rank: B_bar -= C_bar R on its tiles
+//     every rank: partial C_bar^T [B C] over its rows; column reduce to the
+//       owners of block row jb (P > 1)
+//     diagonal owner: symbolic step -> sym(S)
+//     row broadcast of sym(S) along process row jb%P: R_bar -= sym(S) R
+// Collectives: ncclBroadcast / ncclReduce on the row and column communicators
+// (ncclCommSplit of the world communicator), issued by every rank in the same
+// global order.  The same code drives a single-process simulation of the P*Q
+// ranks on one device (broadcast = device copies, reduce = fixed-order adds),
+// which is what the tests exercise on a one-GPU box.
 namespace {
 
-constexpr int64_t DB = 2 * NB;  // distributed block (column panel width)
+constexpr int64_t DB = 2 * NB;  // distributed tile
 
 struct NcclApi {
   void* h = nullptr;
   ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
   ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*commSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   ncclResult_t (*broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
@@ -1040,192 +1055,377 @@ struct NcclApi {
     if (!h) return false;
     getUniqueId = (decltype(getUniqueId))dlsym(h, "ncclGetUniqueId");
     commInitRank = (decltype(commInitRank))dlsym(h, "ncclCommInitRank");
+    commSplit = (decltype(commSplit))dlsym(h, "ncclCommSplit");
     broadcast = (decltype(broadcast))dlsym(h, "ncclBroadcast");
+    reduce = (decltype(reduce))dlsym(h, "ncclReduce");
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
-    return getUniqueId && commInitRank && broadcast && allReduce && commDestroy;
+    return getUniqueId && commInitRank && commSplit && broadcast && reduce && allReduce && commDestroy;
   }
 };
 NcclApi g_nccl;
 
 struct DistState {
-  ncclComm_t comm = nullptr;
-  int G = 0, rank = -1;
+  ncclComm_t comm = nullptr;     // world
+  ncclComm_t rowc = nullptr;     // my process row (Q ranks, rank index = q)
+  ncclComm_t colc = nullptr;     // my process column (P ranks, rank index = p)
+  int G = 0, P = 0, Q = 0, rank = -1;
 };
 DistState g_dist;
 
-// ranks handled by this process: one (NCCL) or all G (simulation)
-struct Rank {
-  int q;                 // global rank
-  const double* L;       // local factor (adjoint) -- or nullptr
-  double* W;             // local working matrix
-  int64_t ld;
-  double* pbuf;          // broadcast landing buffer (n x DB)
-  double* aux;           // per-rank scratch: D^-1 blocks (adjoint), split-K partials ...
-  int* status;
+// number of block indices I in [0, x) with I % P == p (= the local index of the
+// first such I >= x)
+inline int64_t below(int64_t x, int P, int p) { return p < x ? (x - p + P - 1) / P : 0; }
+
+struct Grid {
+  int64_t n, T;
+  int P, Q;
+  int64_t R(int p) const { return below(T, P, p); }  // local block rows of process row p
+  int64_t C(int q) const { return below(T, Q, q); }  // local block columns of process column q
 };
 
-int64_t owned_blocks(int64_t T, int G, int q) { return q < T ? (T - q + G - 1) / G : 0; }
-// number of block columns J < jb owned by rank q (they are local blocks 0 .. cnt-1)
-int64_t owned_below(int64_t jb, int G, int q) { return q < jb ? (jb - q + G - 1) / G : 0; }
+// per-rank device scratch (doubles), laid out by DistPlan
+struct DistPlan {
+  size_t pan, cbuf, stage, dinv, dbuf, lrow, part, z, sbuf, tmp, total;
+};
+DistPlan dist_plan(const Grid& gr, int p, int q, bool adjoint) {
+  DistPlan d{};
+  const size_t t2 = (size_t)DB * DB;
+  size_t o = 0;
+  auto take = [&](size_t cnt) {
+    size_t at = o;
+    o += (cnt + 31) / 32 * 32;  // 256-B aligned
+    return at;
+  };
+  const int64_t R = gr.R(p), C = gr.C(q);
+  d.pan = take((R + 1) * t2);  // [L_kk | panel rows] (forward), C_bar D^-1 rows (adjoint)
+  if (!adjoint) {
+    d.cbuf = take(gr.P > 1 ? C * t2 : 0);
+    d.stage = take(gr.P > 1 ? (size_t)gr.P * (C + 1) * t2 : 0);
+  } else {
+    d.dinv = take(C * t2);
+    d.dbuf = take(t2);
+    d.lrow = take(gr.P > 1 ? C * t2 : 0);
+    size_t part = 0;
+    for (int64_t jb = gr.T - 1; jb >= 0; --jb) {
+      const int64_t mloc = (R - below(jb + 1, gr.P, p)) * DB, w2 = below(jb + 1, gr.Q, q) * DB;
+      if (mloc == 0 || w2 == 0) continue;
+      int s, kps;
+      splitk_choice(mloc, w2, DB, &s, &kps);
+      part = std::max(part, (size_t)s * DB * w2);
+    }
+    d.part = take(part);
+    d.z = take(gr.P > 1 ? C * t2 : 0);
+    d.sbuf = take(t2);
+    d.tmp = take(4 * t2);
+  }
+  d.total = o;
+  return d;
+}
 
-struct Bcast {
+// ranks handled by this process: one (NCCL) or all P*Q (simulation)
+struct Rank {
+  int p, q;
+  const double* L;  // local factor (adjoint) -- or nullptr
+  double* W;        // local working matrix
+  int64_t ld;
+  double* base;     // scratch arena (DistPlan offsets)
+  DistPlan pl;
+  int* status;
+  double* at(size_t off) const { return base + off; }
+};
+
+struct Comm {
   bool sim;
-  // broadcast `count` doubles from ranks[root].buf to every rank's buf (same offset)
-  int operator()(std::vector<Rank>& ranks, int root, double* Rank::*member, size_t count, cudaStream_t st) {
+  int P, Q;
+  Rank* find(std::vector<Rank>& rs, int p, int q) {
+    for (auto& r : rs)
+      if (r.p == p && r.q == q) return &r;
+    return nullptr;
+  }
+  // broadcast `count` doubles within process row p (row = true) or process
+  // column q (row = false) from the member with index `root` (q resp. p);
+  // ptr(rank) names the buffer on each member (the root's holds the data)
+  template <class F>
+  int bcast(std::vector<Rank>& rs, bool row, int idx, int root, F ptr, size_t count, cudaStream_t st) {
+    const int members = row ? Q : P;
+    if (members == 1 || count == 0) return STAN_CL_OK;
     if (sim) {
-      const double* src = ranks[root].*member;
-      for (auto& r : ranks)
-        if (r.q != root) CK(cudaMemcpyAsync(r.*member, src, count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      Rank* src = row ? find(rs, idx, root) : find(rs, root, idx);
+      for (int m = 0; m < members; ++m) {
+        if (m == root) continue;
+        Rank* dst = row ? find(rs, idx, m) : find(rs, m, idx);
+        CK(cudaMemcpyAsync(ptr(*dst), ptr(*src), count * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      }
       return STAN_CL_OK;
     }
-    Rank& me = ranks[0];
-    if (g_nccl.broadcast(me.*member, me.*member, count, ncclFloat64, root, g_dist.comm, st) != ncclSuccess)
+    Rank& me = rs[0];
+    if ((row ? me.p : me.q) != idx) return STAN_CL_OK;
+    double* b = ptr(me);
+    if (g_nccl.broadcast(b, b, count, ncclFloat64, root, row ? g_dist.rowc : g_dist.colc, st) != ncclSuccess)
       return STAN_CL_ENCCL;
+    return STAN_CL_OK;
+  }
+  // sum over process column q into the member with index `root` (fixed order in
+  // the simulation: root, then p = 0, 1, ...)
+  template <class F>
+  int col_reduce(std::vector<Rank>& rs, int q, int root, F ptr, size_t count, cudaStream_t st) {
+    if (P == 1 || count == 0) return STAN_CL_OK;
+    if (sim) {
+      Rank* dst = find(rs, root, q);
+      for (int m = 0; m < P; ++m) {
+        if (m == root) continue;
+        CK(add_block(ptr(*find(rs, m, q)), (int64_t)count, ptr(*dst), (int64_t)count, 1, (int64_t)count, st));
+      }
+      return STAN_CL_OK;
+    }
+    Rank& me = rs[0];
+    if (me.q != q) return STAN_CL_OK;
+    double* b = ptr(me);
+    if (g_nccl.reduce(b, b, count, ncclFloat64, ncclSum, root, g_dist.colc, st) != ncclSuccess) return STAN_CL_ENCCL;
     return STAN_CL_OK;
   }
 };
 
-// local view of rank r for global block column J (owned by r): pointer such
-// that v + row * ld + J*DB addresses element (row, J*DB) of the global matrix
-inline double* col_view(double* base, int64_t J, int G) { return base + (J / G) * DB - J * DB; }
-inline const double* col_view(const double* base, int64_t J, int G) { return base + (J / G) * DB - J * DB; }
+#define RC(x)                   \
+  do {                          \
+    int rc_ = (x);              \
+    if (rc_) return rc_;        \
+  } while (0)
 
-int dist_factor(std::vector<Rank>& ranks, int G, int64_t n, Bcast& bcast) {
+int dist_factor(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
   cudaStream_t st = g.stream;
-  const int64_t T = n / DB;
+  const int64_t T = gr.T, t2 = DB * DB;
+  const int P = gr.P, Q = gr.Q;
+  const int64_t Lc = std::lcm((int64_t)P, (int64_t)Q);
   for (int64_t k = 0; k < T; ++k) {
-    const int o = (int)(k % G);
-    const int64_t c0 = k * DB, m = n - c0;
-    for (auto& r : ranks) {
-      if (r.q != o) continue;
-      double* Wv = col_view(r.W, k, G);
-      int rc = panel(Wv, r.ld, c0, n, DB, r.status, st);  // L11 = chol(A11); L21 = A21 L11^-T
-      if (rc) return rc;
-      CK(copy_block(Wv + c0 * r.ld + c0, r.ld, r.pbuf, DB, m, DB, st));  // rows c0..n of the panel
+    const int pk = (int)(k % P), qk = (int)(k % Q);
+    const int64_t c0 = k * DB;
+    // (a) L_kk = chol(A_kk) on the diagonal owner, in place, then into pan[0]
+    for (auto& r : rs) {
+      if (r.p != pk || r.q != qk) continue;
+      double* tile = r.W + (k / P) * DB * r.ld + (k / Q) * DB;
+      RC(panel(tile - c0 * r.ld - c0, r.ld, c0, c0 + DB, DB, r.status, st));  // view: rows [c0, c0 + DB)
+      CK(copy_block(tile, r.ld, r.at(r.pl.pan), DB, DB, DB, st));
     }
-    int rc = bcast(ranks, o, &Rank::pbuf, (size_t)m * DB, st);
-    if (rc) return rc;
-    for (auto& r : ranks) {  // trailing update of the rank's own block columns J > k
-      for (int64_t J = k + 1 + ((r.q - (k + 1)) % G + G) % G; J < T; J += G) {
-        const double* P = r.pbuf + (J * DB - c0) * DB;  // panel rows J*DB..n
-        double* C = col_view(r.W, J, G) + J * DB * r.ld + J * DB;
-        CK(gemm_full(true, true, (int)(n - J * DB), (int)DB, (int)DB, -1.0, 1, P, DB, P, DB, C, r.ld, r.status, st,
-                     /*lower_only=*/1, PROF_SYRK));
-      }
+    RC(cm.bcast(rs, false, qk, pk, [](Rank& r) { return r.at(r.pl.pan); }, (size_t)t2, st));
+    // (b) process column qk: L_Ik = A_Ik L_kk^-T for the local rows I > k
+    //     (two 128-wide substitutions with the cross update, as the forward panel)
+    for (auto& r : rs) {
+      if (r.q != qk) continue;
+      const int64_t li0 = below(k + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB;
+      if (mloc == 0) continue;
+      double* pan = r.at(r.pl.pan);
+      double* A = r.W + li0 * DB * r.ld + (k / Q) * DB;
+      CK(copy_block(A, r.ld, pan + t2, DB, mloc, DB, st));
+      CK(trsm_panel(pan, DB, 0, DB, DB + mloc, r.status, st));
+      CK(gemm_full(true, true, (int)mloc, NB, NB, -1.0, 1, pan + t2, DB, pan + NB * DB, DB, pan + t2 + NB, DB,
+                   r.status, st, 0, PROF_LOOKAHEAD));
+      CK(trsm_panel(pan, DB, NB, DB, DB + mloc, r.status, st));
+      CK(copy_block(pan + t2, DB, A, r.ld, mloc, DB, st));
     }
-  }
-  for (auto& r : ranks) {  // strict upper of the local diagonal tiles
-    for (int64_t J = r.q; J < T; J += G) CK(zero_tile_upper(col_view(r.W, J, G), r.ld, J * DB, (int)DB, st));
-  }
-  return STAN_CL_OK;
-}
-
-int dist_adjoint(std::vector<Rank>& ranks, int G, int64_t n, Bcast& bcast) {
-  cudaStream_t st = g.stream;
-  const int64_t T = n / DB;
-  // per-rank aux layout: D^-1 of the owned blocks | Ctmp (n x DB) | Ssym | T1..T3 | split-K partials
-  auto dinv = [&](Rank& r, int64_t J) { return r.aux + (J / G) * DB * DB; };
-  const int64_t nb_own_max = (T + G - 1) / G;
-  auto tmp = [&](Rank& r, int i) { return r.aux + nb_own_max * DB * DB + (int64_t)i * DB * DB; };  // 0..3
-  auto part = [&](Rank& r) { return r.aux + nb_own_max * DB * DB + 4 * DB * DB; };
-  for (auto& r : ranks) {
-    for (int64_t J = r.q; J < T; J += G) {
-      // block_inverses addresses block J at Dinv + J*DB*DB: shift so it lands at dinv(r, J)
-      int rc = block_inverses(col_view(r.L, J, G), r.ld, DB, J, 1, dinv(r, J) - J * DB * DB, tmp(r, 0), r.status, st);
-      if (rc) return rc;
+    // (c) row broadcast of the panel rows along every process row
+    for (int p = 0; p < P; ++p) {
+      const int64_t mloc = (gr.R(p) - below(k + 1, P, p)) * DB;
+      RC(cm.bcast(rs, true, p, qk, [](Rank& r) { return r.at(r.pl.pan) + DB * DB; }, (size_t)mloc * DB, st));
     }
-  }
-  for (int64_t k = n; k > 0; k -= DB) {
-    const int64_t j = k - DB, m = n - k, jb = j / DB;
-    const int o = (int)(jb % G);
-    if (m > 0) {
-      for (auto& r : ranks) {  // C_adj = C_adj D^-1 (owner), into pbuf; written back to A_bar
-        if (r.q != o) continue;
-        double* Cb = col_view(r.W, jb, G) + k * r.ld + j;
-        CK(gemm_full(true, false, (int)m, (int)DB, (int)DB, 1.0, 0, Cb, r.ld, dinv(r, jb), DB, r.pbuf, DB, r.status,
-                     st, 0, PROF_TRMM));
-        CK(copy_block(r.pbuf, DB, Cb, r.ld, m, DB, st));
-      }
-      int rc = bcast(ranks, o, &Rank::pbuf, (size_t)m * DB, st);
-      if (rc) return rc;
-      for (auto& r : ranks) {
-        const int64_t nlt = owned_below(jb, G, r.q);          // local blocks with J < jb
-        const int64_t nle = nlt + (r.q == o ? 1 : 0);          // ... and J == jb
-        if (nlt > 0)  // B_adj -= C_adj R  on the rank's own columns
-          CK(gemm_full(true, false, (int)m, (int)(nlt * DB), (int)DB, -1.0, 1, r.pbuf, DB, r.L + j * r.ld, r.ld,
-                       r.W + k * r.ld, r.ld, r.status, st));
-        if (nle > 0) {  // [R_adj D_adj] -= C_adj^T [B C], K = m local
-          int splits, kps;
-          splitk_choice(m, nle * DB, DB, &splits, &kps);
-          CK(gemm_splitk_tn((int)DB, (int)(nle * DB), (int)m, splits, kps, r.pbuf, DB, r.L + k * r.ld, r.ld,
-                            part(r), r.status, st));
-          CK(splitk_reduce_sub(part(r), splits, (int)DB, (int)(nle * DB), r.W + j * r.ld, r.ld, r.status, st));
+    // (d) column exchange (P > 1): rank (p', q) sends the tiles L_Jk, J > k,
+    //     J % P == p', J % Q == q (J = J0 + t * lcm(P, Q)) to its process column
+    if (P > 1) {
+      for (int q = 0; q < Q; ++q) {
+        for (int pp = 0; pp < P; ++pp) {
+          int64_t J0 = -1;
+          for (int64_t J = k + 1; J < std::min(T, k + 1 + Lc); ++J)
+            if (J % P == pp && J % Q == q) {
+              J0 = J;
+              break;
+            }
+          if (J0 < 0) continue;
+          const int64_t cnt = (T - 1 - J0) / Lc + 1;
+          Rank* root = cm.sim ? cm.find(rs, pp, q) : (rs[0].p == pp && rs[0].q == q ? &rs[0] : nullptr);
+          const size_t soff = (size_t)pp * (gr.C(q) + 1) * t2;
+          if (root) {
+            const int64_t li0 = below(k + 1, P, pp);
+            CK(copy_tiles(root->at(root->pl.pan) + t2, J0 / P - li0, Lc / P, root->at(root->pl.stage) + soff, 0, 1,
+                          cnt, t2, st));
+          }
+          RC(cm.bcast(rs, false, q, pp, [soff](Rank& r) { return r.at(r.pl.stage) + soff; }, (size_t)cnt * t2,
+                      st));
+          for (auto& r : rs) {
+            if (r.q != q || r.p == pp) continue;
+            CK(copy_tiles(r.at(r.pl.stage) + soff, 0, 1, r.at(r.pl.cbuf), J0 / Q, Lc / Q, cnt, t2, st));
+          }
         }
       }
     }
-    for (auto& r : ranks) {  // symbolic diagonal step on the owner
-      if (r.q != o) continue;
-      const double* D = col_view(r.L, jb, G) + j * r.ld + j;
-      double* Dbar = col_view(r.W, jb, G) + j * r.ld + j;
-      const double* Di = dinv(r, jb);
-      CK(gemm_small((int)DB, true, true, false, D, r.ld, Dbar, r.ld, tmp(r, 1), DB, r.status, st, 1.0, 1, 0, 0, 0,
-                    /*c_sym=*/true));
-      CK(gemm_small((int)DB, true, false, false, Di, DB, tmp(r, 1), DB, tmp(r, 2), DB, r.status, st));
-      CK(gemm_small((int)DB, false, false, false, tmp(r, 2), DB, Di, DB, tmp(r, 3), DB, r.status, st));
-      CK(phi_sym(tmp(r, 3), r.pbuf, Dbar, r.ld, r.status, st, (int)DB));  // sym(S) -> pbuf
+    // (e) trailing update of the local lower tiles I >= J > k
+    for (auto& r : rs) {
+      const int64_t li0 = below(k + 1, P, r.p), R = gr.R(r.p);
+      const double* pan = r.at(r.pl.pan) + t2;
+      for (int64_t lj = below(k + 1, Q, r.q); lj < gr.C(r.q); ++lj) {
+        const int64_t J = lj * Q + r.q, li_s = below(J, P, r.p);
+        if (li_s >= R) continue;
+        const double* Ljk = (J % P == r.p) ? pan + (J / P - li0) * t2 : r.at(r.pl.cbuf) + lj * t2;
+        CK(gemm_full(true, true, (int)((R - li_s) * DB), (int)DB, (int)DB, -1.0, 1, pan + (li_s - li0) * t2, DB,
+                     Ljk, DB, r.W + li_s * DB * r.ld + lj * DB, r.ld, r.status, st,
+                     /*lower_only=*/(li_s * P + r.p == J) ? 1 : 0, PROF_SYRK));
+      }
     }
-    int rc = bcast(ranks, o, &Rank::pbuf, (size_t)DB * DB, st);
-    if (rc) return rc;
-    for (auto& r : ranks) {  // R_adj -= sym(S) R on the rank's own columns
-      const int64_t nlt = owned_below(jb, G, r.q);
-      if (nlt > 0)
-        CK(gemm_full(true, false, (int)DB, (int)(nlt * DB), (int)DB, -1.0, 1, r.pbuf, DB, r.L + j * r.ld, r.ld,
-                     r.W + j * r.ld, r.ld, r.status, st));
+  }
+  for (auto& r : rs)  // strict upper of the local diagonal tiles
+    for (int64_t J = 0; J < T; ++J)
+      if (J % P == r.p && J % Q == r.q) {
+        double* tile = r.W + (J / P) * DB * r.ld + (J / Q) * DB;
+        CK(zero_tile_upper(tile, r.ld, 0, (int)DB, st));
+      }
+  return STAN_CL_OK;
+}
+
+int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
+  cudaStream_t st = g.stream;
+  const int64_t T = gr.T, t2 = DB * DB;
+  const int P = gr.P, Q = gr.Q;
+  auto ltile = [&](const Rank& r, const double* M, int64_t I, int64_t J) {  // local tile (I, J) of M
+    return M + (I / P) * DB * r.ld + (J / Q) * DB;
+  };
+  // D^-1 of the owned diagonal tiles (slot J / Q); they depend only on L
+  for (auto& r : rs)
+    for (int64_t J = 0; J < T; ++J) {
+      if (J % P != r.p || J % Q != r.q) continue;
+      const double* D = ltile(r, r.L, J, J);
+      double* dst = r.at(r.pl.dinv) + (J / Q) * t2;
+      RC(block_inverses(D - J * DB * r.ld - J * DB, r.ld, DB, J, 1, dst - J * t2, r.at(r.pl.tmp), r.status, st));
+    }
+  for (int64_t jb = T - 1; jb >= 0; --jb) {
+    const int pj = (int)(jb % P), qj = (int)(jb % Q);
+    auto dinv_of = [&](Rank& r) { return r.p == pj ? r.at(r.pl.dinv) + (jb / Q) * t2 : r.at(r.pl.dbuf); };
+    if (jb < T - 1) {
+      // R1: C_bar <- C_bar D^-1 on process column qj (D^-1 broadcast down it)
+      RC(cm.bcast(rs, false, qj, pj, dinv_of, (size_t)t2, st));
+      for (auto& r : rs) {
+        if (r.q != qj) continue;
+        const int64_t li0 = below(jb + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB;
+        if (mloc == 0) continue;
+        double* Cb = r.W + li0 * DB * r.ld + (jb / Q) * DB;
+        CK(gemm_full(true, false, (int)mloc, (int)DB, (int)DB, 1.0, 0, Cb, r.ld, dinv_of(r), DB, r.at(r.pl.pan), DB,
+                     r.status, st, 0, PROF_TRMM));
+        CK(copy_block(r.at(r.pl.pan), DB, Cb, r.ld, mloc, DB, st));
+      }
+      for (int p = 0; p < P; ++p) {
+        const int64_t mloc = (gr.R(p) - below(jb + 1, P, p)) * DB;
+        RC(cm.bcast(rs, true, p, qj, [](Rank& r) { return r.at(r.pl.pan); }, (size_t)mloc * DB, st));
+      }
+      // L's row block jb (columns J < jb) down every process column (P > 1)
+      if (P > 1) {
+        for (int q = 0; q < Q; ++q) {
+          const int64_t w = below(jb, Q, q) * DB;
+          if (w == 0) continue;
+          for (auto& r : rs)
+            if (r.p == pj && r.q == q)
+              CK(copy_block(r.L + (jb / P) * DB * r.ld, r.ld, r.at(r.pl.lrow), w, DB, w, st));
+          RC(cm.bcast(rs, false, q, pj, [](Rank& r) { return r.at(r.pl.lrow); }, (size_t)DB * w, st));
+        }
+      }
+      // R3: B_bar -= C_bar R on the local tiles I > jb > J
+      for (auto& r : rs) {
+        const int64_t li0 = below(jb + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB, w = below(jb, Q, r.q) * DB;
+        if (mloc == 0 || w == 0) continue;
+        const double* Rr = P > 1 ? r.at(r.pl.lrow) : r.L + jb * DB * r.ld;
+        const int64_t ldr = P > 1 ? w : r.ld;
+        CK(gemm_full(true, false, (int)mloc, (int)w, (int)DB, -1.0, 1, r.at(r.pl.pan), DB, Rr, ldr,
+                     r.W + li0 * DB * r.ld, r.ld, r.status, st));
+      }
+      // R2: [R_bar D_bar] -= C_bar^T [B C]: local split-K partials over the rows
+      //     I > jb, reduced down each process column to the owner of row block jb
+      //     (large-k product PAPER.md:172-174)
+      for (auto& r : rs) {
+        const int64_t li0 = below(jb + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB, w2 = below(jb + 1, Q, r.q) * DB;
+        if (w2 == 0) continue;
+        double* dst = P > 1 ? r.at(r.pl.z) : r.W + jb * DB * r.ld;
+        const int64_t ldd = P > 1 ? w2 : r.ld;
+        if (P > 1) CK(cudaMemsetAsync(dst, 0, (size_t)DB * w2 * sizeof(double), st));
+        if (mloc == 0) continue;
+        int splits, kps;
+        splitk_choice(mloc, w2, DB, &splits, &kps);
+        CK(gemm_splitk_tn((int)DB, (int)w2, (int)mloc, splits, kps, r.at(r.pl.pan), DB, r.L + li0 * DB * r.ld, r.ld,
+                          r.at(r.pl.part), r.status, st));
+        CK(splitk_reduce_sub(r.at(r.pl.part), splits, (int)DB, (int)w2, dst, ldd, r.status, st));
+      }
+      if (P > 1) {
+        for (int q = 0; q < Q; ++q) {
+          const int64_t w2 = below(jb + 1, Q, q) * DB;
+          if (w2 == 0) continue;
+          RC(cm.col_reduce(rs, q, pj, [](Rank& r) { return r.at(r.pl.z); }, (size_t)DB * w2, st));
+          for (auto& r : rs)
+            if (r.p == pj && r.q == q)
+              CK(add_block(r.at(r.pl.z), w2, r.W + (jb / P) * DB * r.ld, r.ld, DB, w2, st));
+        }
+      }
+    }
+    // R4: symbolic diagonal step on the owner -> sym(S) in sbuf
+    for (auto& r : rs) {
+      if (r.p != pj || r.q != qj) continue;
+      const double* D = ltile(r, r.L, jb, jb);
+      double* Dbar = r.W + (jb / P) * DB * r.ld + (jb / Q) * DB;
+      const double* Di = r.at(r.pl.dinv) + (jb / Q) * t2;
+      double* T1 = r.at(r.pl.tmp);
+      CK(gemm_small((int)DB, true, true, false, D, r.ld, Dbar, r.ld, T1, DB, r.status, st, 1.0, 1, 0, 0, 0,
+                    /*c_sym=*/true));
+      CK(gemm_small((int)DB, true, false, false, Di, DB, T1, DB, T1 + t2, DB, r.status, st));
+      CK(gemm_small((int)DB, false, false, false, T1 + t2, DB, Di, DB, T1 + 2 * t2, DB, r.status, st));
+      CK(phi_sym(T1 + 2 * t2, r.at(r.pl.sbuf), Dbar, r.ld, r.status, st, (int)DB));
+    }
+    // R5: R_bar -= sym(S) R on process row pj
+    RC(cm.bcast(rs, true, pj, qj, [](Rank& r) { return r.at(r.pl.sbuf); }, (size_t)t2, st));
+    for (auto& r : rs) {
+      if (r.p != pj) continue;
+      const int64_t w = below(jb, Q, r.q) * DB;
+      if (w == 0) continue;
+      CK(gemm_full(true, false, (int)DB, (int)w, (int)DB, -1.0, 1, r.at(r.pl.sbuf), DB, r.L + (jb / P) * DB * r.ld,
+                   r.ld, r.W + (jb / P) * DB * r.ld, r.ld, r.status, st));
     }
   }
   return STAN_CL_OK;
 }
 
-// per-rank device scratch for a problem of order n over G ranks
-size_t dist_aux_doubles(int64_t n, int G) {
-  const int64_t T = n / DB, own = (T + G - 1) / G;
-  int64_t part = 0;
-  for (int64_t k = n; k > 0; k -= DB) {
-    const int64_t m = n - k;
-    if (!m) continue;
-    int s, kps;
-    splitk_choice(m, own * DB, DB, &s, &kps);
-    part = std::max(part, (int64_t)s * DB * own * DB);
+// nloc ranks in this process: all P*Q (sim) or the one at (p0, q0)
+int dist_run(bool adjoint, int64_t n, int P, int Q, bool sim, int p0, int q0, const double* const* Ls,
+             double* const* Ws, int64_t ld) {
+  if (n == 0) return STAN_CL_OK;
+  if (n < 0 || n % DB != 0 || P < 1 || Q < 1 || ld < 1) return STAN_CL_EINVAL;
+  const Grid gr{n, n / DB, P, Q};
+  const int nloc = sim ? P * Q : 1;
+  std::vector<DistPlan> plans;
+  size_t total = 0;
+  for (int i = 0; i < nloc; ++i) {
+    const int p = sim ? i / Q : p0, q = sim ? i % Q : q0;
+    const bool owns = gr.R(p) > 0 && gr.C(q) > 0;  // a rank of a grid larger than the tile count may own none
+    if (owns && (!Ws[i] || (adjoint && !Ls[i]))) return STAN_CL_EINVAL;
+    if (gr.C(q) > 0 && ld < gr.C(q) * DB) return STAN_CL_EINVAL;
+    plans.push_back(dist_plan(gr, p, q, adjoint));
+    total += plans.back().total;
   }
-  return (size_t)(own * DB * DB + 4 * DB * DB + part);
-}
-
-int dist_run(bool adjoint, int64_t n, int G, int nloc, int q0, const double* const* Ls, double* const* Ws,
-             int64_t ld, bool sim) {
-  if (n <= 0 || n % DB != 0 || G < 1 || ld < 1) return n == 0 ? STAN_CL_OK : STAN_CL_EINVAL;
-  const int64_t T = n / DB;
-  const size_t aux = adjoint ? dist_aux_doubles(n, G) : 0;
-  const size_t per = (size_t)n * DB + aux;  // pbuf + aux
   double* buf = nullptr;
-  int rc = ensure_mat(0, per * nloc * sizeof(double), &buf);
+  int rc = ensure_mat(0, std::max<size_t>(total, 1) * sizeof(double), &buf);
   if (rc) return rc;
   rc = ensure_ws(al(sizeof(int) * 64) + NB * NB * sizeof(double));
   if (rc) return rc;
   int* status = (int*)g.ws;
   CK(cudaMemsetAsync(status, 0, sizeof(int), g.stream));
-  std::vector<Rank> ranks;
+  std::vector<Rank> rs;
+  size_t off = 0;
   for (int i = 0; i < nloc; ++i) {
-    const int q = q0 + i;
-    if (ld < owned_blocks(T, G, q) * DB) return STAN_CL_EINVAL;
-    ranks.push_back(Rank{q, adjoint ? Ls[i] : nullptr, Ws[i], ld, buf + i * per, buf + i * per + n * DB, status});
+    const int p = sim ? i / Q : p0, q = sim ? i % Q : q0;
+    rs.push_back(Rank{p, q, adjoint ? Ls[i] : nullptr, Ws[i], ld, buf + off, plans[i], status});
+    off += plans[i].total;
   }
-  if (adjoint) {  // A_bar <- tril(L_bar), locally: strict upper of the local diagonal tiles
-    for (auto& r : ranks)
-      for (int64_t J = r.q; J < T; J += G) CK(zero_tile_upper(col_view(r.W, J, G), r.ld, J * DB, (int)DB, g.stream));
-  }
-  Bcast bc{sim};
-  return adjoint ? dist_adjoint(ranks, G, n, bc) : dist_factor(ranks, G, n, bc);
+  if (adjoint)  // A_bar <- tril(L_bar): strict upper of the local diagonal tiles
+    for (auto& r : rs)
+      for (int64_t J = 0; J < gr.T; ++J)
+        if (J % P == r.p && J % Q == r.q)
+          CK(zero_tile_upper(r.W + (J / P) * DB * r.ld + (J / Q) * DB, r.ld, 0, (int)DB, g.stream));
+  Comm cm{sim, P, Q};
+  return adjoint ? dist_adjoint(rs, gr, cm) : dist_factor(rs, gr, cm);
 }
 
 }  // namespace
@@ -1242,7 +1442,8 @@ int stan_cl_dist_get_unique_id(void* out128) {
 }
 
 int stan_cl_dist_init(int nranks, int rank, const void* id128, int P, int Q) {
-  if (nranks < 1 || rank < 0 || rank >= nranks || !id128 || P != 1 || Q != nranks) return STAN_CL_EINVAL;
+  if (nranks < 1 || rank < 0 || rank >= nranks || !id128 || P < 1 || Q < 1 || P * Q != nranks)
+    return STAN_CL_EINVAL;
   if (!g_nccl.load()) return STAN_CL_ENCCL;
   if (g_dist.comm) return STAN_CL_EINVAL;
   ncclUniqueId id;
@@ -1251,15 +1452,25 @@ int stan_cl_dist_init(int nranks, int rank, const void* id128, int P, int Q) {
     g_dist.comm = nullptr;
     return STAN_CL_ENCCL;
   }
+  const int p = rank / Q, q = rank % Q;
+  // row communicator: same p, ordered by q; column communicator: same q, ordered by p
+  if (g_nccl.commSplit(g_dist.comm, p, q, &g_dist.rowc, nullptr) != ncclSuccess ||
+      g_nccl.commSplit(g_dist.comm, q, p, &g_dist.colc, nullptr) != ncclSuccess) {
+    if (g_dist.rowc) g_nccl.commDestroy(g_dist.rowc);
+    g_nccl.commDestroy(g_dist.comm);
+    g_dist = DistState{};
+    return STAN_CL_ENCCL;
+  }
   g_dist.G = nranks;
+  g_dist.P = P;
+  g_dist.Q = Q;
   g_dist.rank = rank;
   return STAN_CL_OK;
 }
 
 static int dist_status_allreduce(int rc) {
   if (rc) return rc;
-  // the first failing row anywhere (status words are 0 or row+1; max is fine for
-  // the "did anything fail" question, the owner's value is the row)
+  // "did anything fail": status words are 0 or row+1; the max is a failing row
   int* status = (int*)g.ws;
   if (g_nccl.allReduce(status, status, 1, ncclInt32, ncclMax, g_dist.comm, g.stream) != ncclSuccess)
     return STAN_CL_ENCCL;
@@ -1269,7 +1480,8 @@ static int dist_status_allreduce(int rc) {
 int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local) {
   if (!g_dist.comm || (nb != 0 && nb != (int)DB)) return STAN_CL_EINVAL;
   double* Ws[1] = {A_local};
-  int rc = dist_run(false, n, g_dist.G, 1, g_dist.rank, nullptr, Ws, ld_local, false);
+  const int p = g_dist.rank / g_dist.Q, q = g_dist.rank % g_dist.Q;
+  int rc = dist_run(false, n, g_dist.P, g_dist.Q, false, p, q, nullptr, Ws, ld_local);
   return n == 0 ? rc : dist_status_allreduce(rc);
 }
 
@@ -1278,38 +1490,55 @@ int stan_cl_dist_cholesky_adjoint(int64_t n, int nb, const double* L_local, doub
   if (!g_dist.comm || (nb != 0 && nb != (int)DB)) return STAN_CL_EINVAL;
   const double* Ls[1] = {L_local};
   double* Ws[1] = {Lbar_to_Abar_local};
-  int rc = dist_run(true, n, g_dist.G, 1, g_dist.rank, Ls, Ws, ld_local, false);
+  const int p = g_dist.rank / g_dist.Q, q = g_dist.rank % g_dist.Q;
+  int rc = dist_run(true, n, g_dist.P, g_dist.Q, false, p, q, Ls, Ws, ld_local);
   return n == 0 ? rc : dist_status_allreduce(rc);
 }
 
 int stan_cl_dist_finalize(void) {
+  if (g_dist.rowc) g_nccl.commDestroy(g_dist.rowc);
+  if (g_dist.colc) g_nccl.commDestroy(g_dist.colc);
   if (g_dist.comm) g_nccl.commDestroy(g_dist.comm);
   g_dist = DistState{};
   return STAN_CL_OK;
 }
 
-int stan_cl_gp_exp_quad_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter,
-                                 double* K_local, int64_t ld_local, int G, int q) {
-  if (n < 0 || G < 1 || q < 0 || q >= G || n % DB != 0) return STAN_CL_EINVAL;
+int stan_cl_gp_exp_quad_cov_tiles(int64_t n, const double* x, double alpha, double rho, double jitter,
+                                  double* K_local, int64_t ld_local, int P, int Q, int p, int q) {
+  if (n < 0 || P < 1 || Q < 1 || p < 0 || p >= P || q < 0 || q >= Q || n % DB != 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!x || !K_local) return STAN_CL_EINVAL;
   if (!(rho != 0.0) || !(rho - rho == 0.0)) return STAN_CL_EINVAL;
-  if (ld_local < owned_blocks(n / DB, G, q) * DB) return STAN_CL_EINVAL;
-  CK(se_cov_cols(n, x, alpha, rho, jitter, K_local, ld_local, G, q, g.stream));
+  if (ld_local < below(n / DB, Q, q) * DB) return STAN_CL_EINVAL;
+  CK(se_cov_tiles(n, x, alpha, rho, jitter, K_local, ld_local, P, Q, p, q, g.stream));
   return STAN_CL_OK;
 }
 
-int stan_cl_dist_sim_cholesky(int64_t n, int G, double* const* A_locals, int64_t ld_local) {
-  if (!A_locals || G < 1) return STAN_CL_EINVAL;
-  int rc = dist_run(false, n, G, G, 0, nullptr, A_locals, ld_local, true);
+int stan_cl_gp_exp_quad_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter,
+                                 double* K_local, int64_t ld_local, int G, int q) {
+  return stan_cl_gp_exp_quad_cov_tiles(n, x, alpha, rho, jitter, K_local, ld_local, 1, G, 0, q);
+}
+
+int stan_cl_dist_sim2_cholesky(int64_t n, int P, int Q, double* const* A_locals, int64_t ld_local) {
+  if (!A_locals || P < 1 || Q < 1) return STAN_CL_EINVAL;
+  int rc = dist_run(false, n, P, Q, true, 0, 0, nullptr, A_locals, ld_local);
   return (rc || n == 0) ? rc : read_status();
+}
+
+int stan_cl_dist_sim2_cholesky_adjoint(int64_t n, int P, int Q, const double* const* L_locals,
+                                       double* const* W_locals, int64_t ld_local) {
+  if (!L_locals || !W_locals || P < 1 || Q < 1) return STAN_CL_EINVAL;
+  int rc = dist_run(true, n, P, Q, true, 0, 0, L_locals, W_locals, ld_local);
+  return (rc || n == 0) ? rc : read_status();
+}
+
+int stan_cl_dist_sim_cholesky(int64_t n, int G, double* const* A_locals, int64_t ld_local) {
+  return stan_cl_dist_sim2_cholesky(n, 1, G, A_locals, ld_local);
 }
 
 int stan_cl_dist_sim_cholesky_adjoint(int64_t n, int G, const double* const* L_locals, double* const* W_locals,
                                       int64_t ld_local) {
-  if (!L_locals || !W_locals || G < 1) return STAN_CL_EINVAL;
-  int rc = dist_run(true, n, G, G, 0, L_locals, W_locals, ld_local, true);
-  return (rc || n == 0) ? rc : read_status();
+  return stan_cl_dist_sim2_cholesky_adjoint(n, 1, G, L_locals, W_locals, ld_local);
 }
 
 }  // extern "C"

@@ -138,30 +138,84 @@ cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double 
 
 // the owned 256-wide block columns J = q, q+G, ... of K, stored contiguously
 // (local column lc*256 + c  <->  global column (lc*G + q)*256 + c)
-__global__ void se_cov_cols_kernel(int64_t n, const double* __restrict__ x, double sq_alpha,
-                                   double neg_half_inv_rho2, double jitter, double* __restrict__ K,
-                                   int64_t ld, int64_t ncols, int G, int q) {
-  const long long total = (long long)n * ncols;
+// 2-D block-cyclic layout: rank (p, q) of a P x Q grid holds
+// the 256 x 256 tiles (I, J) with I % P == p, J % Q == q as local tile
+// (I / P, J / Q) of a row-major (rows x ncols) array.  Every local element is
+// written (tiles above the diagonal too: the builder is cheap and the result
+// is then the full symmetric K restricted to the rank's tiles).
+__global__ void se_cov_tiles_kernel(int64_t nrows, const double* __restrict__ x, double sq_alpha,
+                                    double neg_half_inv_rho2, double jitter, double* __restrict__ K,
+                                    int64_t ld, int64_t ncols, int P, int p, int Q, int q) {
+  const long long total = (long long)nrows * ncols;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
        idx += (long long)gridDim.x * blockDim.x) {
-    const long long i = idx / ncols, lcol = idx - i * ncols;
-    const long long j = ((lcol >> 8) * G + q) * 256 + (lcol & 255);
+    const long long lrow = idx / ncols, lcol = idx - lrow * ncols;
+    const long long i = ((lrow >> 8) * P + p) * 256 + (lrow & 255);
+    const long long j = ((lcol >> 8) * Q + q) * 256 + (lcol & 255);
     const double d = x[i] - x[j];
     const double e = __dmul_rn(__dmul_rn(d, d), neg_half_inv_rho2);
     double v = __dmul_rn(sq_alpha, exp(e));
     if (i == j) v = __dadd_rn(v, jitter);
-    K[i * ld + lcol] = v;
+    K[lrow * ld + lcol] = v;
   }
+}
+
+cudaError_t se_cov_tiles(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
+                         int64_t ld, int P, int Q, int p, int q, cudaStream_t st) {
+  const int64_t T = n / 256;
+  const int64_t nrows = (p < T ? (T - p + P - 1) / P : 0) * 256, ncols = (q < T ? (T - q + Q - 1) / Q : 0) * 256;
+  if (nrows == 0 || ncols == 0) return cudaSuccess;
+  Prof prof_(PROF_SE, 0.0, st, 8.0 * nrows * ncols + 8.0 * (nrows + ncols));
+  se_cov_tiles_kernel<<<grid_for((long long)nrows * ncols, 256), 256, 0, st>>>(
+      nrows, x, alpha * alpha, -0.5 / (rho * rho), jitter, K, ld, ncols, P, p, Q, q);
+  return cudaGetLastError();
 }
 
 cudaError_t se_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
                         int64_t ld, int G, int q, cudaStream_t st) {
-  const int64_t T = n / 256, own = q < T ? (T - q + G - 1) / G : 0;
-  const int64_t ncols = own * 256;
-  if (n == 0 || ncols == 0) return cudaSuccess;
-  Prof prof_(PROF_SE, 0.0, st, 8.0 * n * ncols + 8.0 * n);
-  se_cov_cols_kernel<<<grid_for((long long)n * ncols, 256), 256, 0, st>>>(n, x, alpha * alpha, -0.5 / (rho * rho),
-                                                                          jitter, K, ld, ncols, G, q);
+  return se_cov_tiles(n, x, alpha, rho, jitter, K, ld, 1, G, 0, q, st);
+}
+
+// dst tile (d0 + ds*t) <- src tile (s0 + ss*t), t < cnt; tiles of `elems` doubles
+// stored contiguously (elems even, 16-B aligned)
+__global__ void copy_tiles_kernel(const double* __restrict__ src, int64_t s0, int64_t ss, double* __restrict__ dst,
+                                  int64_t d0, int64_t ds, int64_t elems) {
+  const int64_t t = blockIdx.y;
+  const double2* s = reinterpret_cast<const double2*>(src + (s0 + ss * t) * elems);
+  double2* d = reinterpret_cast<double2*>(dst + (d0 + ds * t) * elems);
+  for (int64_t h = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; h < elems / 2; h += (int64_t)gridDim.x * blockDim.x)
+    d[h] = s[h];
+}
+
+cudaError_t copy_tiles(const double* src, int64_t s0, int64_t ss, double* dst, int64_t d0, int64_t ds, int64_t cnt,
+                       int64_t elems, cudaStream_t st) {
+  if (cnt <= 0 || elems <= 0) return cudaSuccess;
+  Prof prof_(PROF_MISC, 0.0, st, 16.0 * cnt * elems);
+  copy_tiles_kernel<<<dim3(32, (unsigned)cnt), 256, 0, st>>>(src, s0, ss, dst, d0, ds, elems);
+  return cudaGetLastError();
+}
+
+// dst[rows x cols] (ldd) += src[rows x cols] (lds); cols even, 16-B aligned rows
+__global__ void add_block_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
+                                 int64_t ldd, int64_t rows, int64_t cols) {
+  const long long half = rows * cols / 2;
+  for (long long h = blockIdx.x * (long long)blockDim.x + threadIdx.x; h < half;
+       h += (long long)gridDim.x * blockDim.x) {
+    const long long e = 2 * h, r = e / cols, c = e - r * cols;
+    double2 a = *reinterpret_cast<const double2*>(src + r * lds + c);
+    double2* d = reinterpret_cast<double2*>(dst + r * ldd + c);
+    double2 b = *d;
+    b.x = __dadd_rn(b.x, a.x);
+    b.y = __dadd_rn(b.y, a.y);
+    *d = b;
+  }
+}
+
+cudaError_t add_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+                      cudaStream_t st) {
+  if (rows == 0 || cols == 0) return cudaSuccess;
+  Prof prof_(PROF_MISC, 0.0, st, 24.0 * rows * cols);
+  add_block_kernel<<<grid_for(rows * cols / 2, 256), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
   return cudaGetLastError();
 }
 

@@ -48,7 +48,18 @@ cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double 
 cudaError_t se_cov_cols(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
                         int64_t ld, int G, int q, cudaStream_t st);
 
+// tiles (I, J), I % P == p, J % Q == q, of K for rank (p, q) of a P x Q grid
+// (2-D block-cyclic, 256 x 256 tiles; local tile (I / P, J / Q))
+cudaError_t se_cov_tiles(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
+                         int64_t ld, int P, int Q, int p, int q, cudaStream_t st);
+
 // ---- layout helpers (K11) ----
+// dst tile (d0 + ds*t) <- src tile (s0 + ss*t) for t < cnt (contiguous tiles of `elems` doubles)
+cudaError_t copy_tiles(const double* src, int64_t s0, int64_t ss, double* dst, int64_t d0, int64_t ds, int64_t cnt,
+                       int64_t elems, cudaStream_t st);
+// dst[rows x cols] (ldd) += src (lds); cols even, 16-B aligned rows
+cudaError_t add_block(const double* src, int64_t lds, double* dst, int64_t ldd, int64_t rows, int64_t cols,
+                      cudaStream_t st);
 // dst[N x N] (ldd) <- lower(src[n x n], lds) with +0.0 strict upper; rows/cols >= n
 // become diag_pad * I (diag_pad = 1 for L/A, 0 for adjoints).  N >= n.
 cudaError_t copy_lower_pad(const double* src, int64_t n, int64_t lds, double* dst, int64_t N,

@@ -56,3 +56,23 @@ def test_max_over_ranks_and_replica_seeds():
 def test_single_rank_passthrough():
     import bench
     assert bench.max_over_ranks(3.5, 1) == 3.5
+
+
+def test_grid_layout_roundtrip():
+    """2-D block-cyclic host layout: default grids, local shapes,
+    scatter/gather round trip, and that every tile lands on rank (I % P, J % Q)."""
+    import paper_1907_01063_b200 as sc
+    assert [sc.dist_grid(g) for g in (1, 2, 4, 8, 6, 3)] == [(1, 1), (1, 2), (2, 2), (2, 4), (2, 3), (1, 3)]
+    B = sc.DIST_BLOCK
+    for n, P, Q in [(1792, 2, 2), (2304, 2, 4), (768, 4, 1), (1280, 3, 2)]:
+        T = n // B
+        A = torch.arange(n * n, dtype=torch.float64).reshape(n, n)
+        locs = [sc.dist_scatter2(A, P, Q, r // Q, r % Q) for r in range(P * Q)]
+        assert sum(l.numel() for l in locs) == n * n
+        for r, l in enumerate(locs):
+            p, q = divmod(r, Q)
+            assert tuple(l.shape) == sc.dist_local_shape(n, P, Q, p, q)
+            for li, I in enumerate(range(p, T, P)):
+                for lj, J in enumerate(range(q, T, Q)):
+                    assert l[li * B, lj * B] == A[I * B, J * B]
+        assert torch.equal(sc.dist_gather2(locs, n, P, Q), A)

@@ -7,6 +7,7 @@ transport itself is exercised by test_nccl_ranks when >= 2 GPUs are visible.
 """
 from __future__ import annotations
 
+import ctypes
 import os
 import socket
 
@@ -111,7 +112,76 @@ def test_dist_not_pd_and_errors(sc):
     t = torch.zeros(300, 512, dtype=torch.float64, device="cuda")
     assert lib.stan_cl_dist_cholesky(300, 0, t.data_ptr(), 512) == -1      # no communicator
     assert lib.stan_cl_dist_init(2, 0, None, 1, 2) == -1                    # no id
-    assert lib.stan_cl_dist_init(2, 0, t.data_ptr(), 2, 1) == -1            # P != 1
+    idb = (ctypes.c_char * 128)()
+    assert lib.stan_cl_dist_init(2, 0, ctypes.cast(idb, ctypes.c_void_p), 2, 2) == -1   # P*Q != nranks
+    assert lib.stan_cl_dist_init(2, 0, ctypes.cast(idb, ctypes.c_void_p), 0, 2) == -1   # P < 1
+
+
+# ---- 2-D block-cyclic grids (P > 1): row/column broadcasts, column reductions
+GRIDS = [(1280, 2, 1), (1792, 2, 2), (1280, 3, 2), (2304, 2, 4), (1536, 2, 3), (768, 4, 1)]
+
+
+def scatter2(sc, A: np.ndarray, P: int, Q: int):
+    n = A.shape[0]
+    At = torch.from_numpy(np.ascontiguousarray(A)).cuda()
+    width = max(sc.dist_local_shape(n, P, Q, 0, q)[1] for q in range(Q))
+    return [sc.dist_scatter2(At, P, Q, r // Q, r % Q, width).contiguous() for r in range(P * Q)]
+
+
+@pytest.mark.parametrize("n,P,Q", GRIDS)
+def test_dist_sim2_cholesky(sc, n, P, Q):
+    K = se(n)
+    locs = scatter2(sc, K, P, Q)
+    assert sc.dist_sim2_cholesky(locs, n, P, Q) == 0
+    got = sc.dist_gather2(locs, n, P, Q).cpu().numpy()
+    check_lower_and_tiles(got, oracle.cholesky(K), 1e-11)
+    L0 = inputs.unit_lower_pm1(n, seed=n + P * Q)       # integer-exact family: bit for bit
+    locs = scatter2(sc, inputs.gram_exact(L0), P, Q)
+    assert sc.dist_sim2_cholesky(locs, n, P, Q) == 0
+    assert np.array_equal(np.tril(sc.dist_gather2(locs, n, P, Q).cpu().numpy()), L0)
+
+
+@pytest.mark.parametrize("n,P,Q", GRIDS)
+def test_dist_sim2_adjoint(sc, n, P, Q):
+    L = oracle.cholesky(se(n))
+    W = inputs.lbar(n)
+    Ls, Ws = scatter2(sc, L, P, Q), scatter2(sc, W, P, Q)
+    assert sc.dist_sim2_cholesky_adjoint(Ls, Ws, n, P, Q) == 0
+    check_lower_and_tiles(sc.dist_gather2(Ws, n, P, Q).cpu().numpy(), oracle.cholesky_adjoint(L, W), 1e-9)
+    Li = inputs.unit_lower_pm1(n, seed=3, band=2)       # integer-exact adjoint family: bit for bit
+    Wi = inputs.int_lbar(n, seed=4)
+    Ls, Ws = scatter2(sc, Li, P, Q), scatter2(sc, Wi, P, Q)
+    assert sc.dist_sim2_cholesky_adjoint(Ls, Ws, n, P, Q) == 0
+    assert np.array_equal(np.tril(sc.dist_gather2(Ws, n, P, Q).cpu().numpy()), oracle.cholesky_adjoint(Li, Wi))
+
+
+def test_dist_sim2_matches_single_gpu_layout(sc):
+    """P = 1 of the 2-D code is the block-column layout: same bits as dist_sim on 1 x G."""
+    n = 1280
+    K = se(n)
+    a = scatter2(sc, K, 1, 3)
+    b = scatter_padded(sc, K, 3)
+    assert sc.dist_sim2_cholesky(a, n, 1, 3) == 0 and sc.dist_sim_cholesky(b, n) == 0
+    assert torch.equal(sc.dist_gather2(a, n, 1, 3), sc.dist_gather(b, n))
+
+
+@pytest.mark.parametrize("n,P,Q", [(1280, 2, 2), (1536, 3, 2)])
+def test_se_cov_tiles(sc, n, P, Q):
+    x = torch.from_numpy(inputs.gp_x(n)).cuda()
+    K = sc.gp_exp_quad_cov(x, 1.3, 0.7, 1e-6)
+    for r in range(P * Q):
+        p, q = divmod(r, Q)
+        rows, cols = sc.dist_local_shape(n, P, Q, p, q)
+        loc = torch.empty((rows, cols), dtype=torch.float64, device="cuda")
+        sc.gp_exp_quad_cov_tiles(x, loc, P, Q, p, q, 1.3, 0.7, 1e-6)
+        assert torch.equal(loc, sc.dist_scatter2(K, P, Q, p, q))
+
+
+def test_dist_sim2_not_pd(sc):
+    n, P, Q = 1280, 2, 2
+    A = inputs.toeplitz(n)
+    A[1000, 1000] = -1e12
+    assert sc.dist_sim2_cholesky(scatter2(sc, A, P, Q), n, P, Q) == 1001
 
 
 def _free_port():
