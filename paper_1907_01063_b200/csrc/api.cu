@@ -155,6 +155,9 @@ int ensure_ws(size_t bytes) {
     return STAN_CL_ENOMEM;
   }
   g.ws_cap = bytes;
+  // the int header (status word, grid-barrier counters of the fused diagonal
+  // step) starts at zero; the kernels leave the counters at zero
+  CK(cudaMemset(g.ws, 0, sizeof(int) * 64));
   return STAN_CL_OK;
 }
 
@@ -423,13 +426,11 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
     }
     // D_adj = transpose(D) * D_adj; copy_lower_tri_to_upper_tri
     // (only the lower tiles of P = D^T D_adj are formed, stored mirrored)
-    CK(gemm_small((int)B, true, true, false, D, ld, Dbar, ld, T1, B, status, st, 1.0, 1, 0, 0, 0, /*c_sym=*/true));
     // D = transpose(lower_triangular_inverse(D)); D_adj = D * transpose(D * D_adj)
     // computed as S = D^-T sym(P) D^-1
-    CK(gemm_small((int)B, true, false, false, Db, B, T1, B, T2, B, status, st));
-    CK(gemm_small((int)B, false, false, false, T2, B, Db, B, T3, B, status, st));
     // copy_lower_tri_to_upper_tri; diagonal * 0.5; set_zeros_in_upper_tri
-    CK(phi_sym(T3, T4, Dbar, ld, status, st, (int)B));
+    // -- all in one launch (three DMMA products separated by grid barriers)
+    CK(adj_diag_fused((int)B, D, ld, Dbar, ld, Db, T1, T2, T3, T4, (unsigned*)status + 16, status, st));
     // R_adj = R_adj - D_adj * R
     if (j > 0)
       CK(gemm_full(true, false, (int)B, (int)j, (int)B, -1.0, 1, T4, B, R, ld, Wm + j * ld, ld, status, st));
@@ -1369,11 +1370,8 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
       double* Dbar = r.W + (jb / P) * DB * r.ld + (jb / Q) * DB;
       const double* Di = r.at(r.pl.dinv) + (jb / Q) * t2;
       double* T1 = r.at(r.pl.tmp);
-      CK(gemm_small((int)DB, true, true, false, D, r.ld, Dbar, r.ld, T1, DB, r.status, st, 1.0, 1, 0, 0, 0,
-                    /*c_sym=*/true));
-      CK(gemm_small((int)DB, true, false, false, Di, DB, T1, DB, T1 + t2, DB, r.status, st));
-      CK(gemm_small((int)DB, false, false, false, T1 + t2, DB, Di, DB, T1 + 2 * t2, DB, r.status, st));
-      CK(phi_sym(T1 + 2 * t2, r.at(r.pl.sbuf), Dbar, r.ld, r.status, st, (int)DB));
+      CK(adj_diag_fused((int)DB, D, r.ld, Dbar, r.ld, Di, T1, T1 + t2, T1 + 2 * t2, r.at(r.pl.sbuf),
+                        (unsigned*)r.status + 16, r.status, st));
     }
     // R5: R_bar -= sym(S) R on process row pj
     RC(cm.bcast(rs, true, pj, qj, [](Rank& r) { return r.at(r.pl.sbuf); }, (size_t)t2, st));

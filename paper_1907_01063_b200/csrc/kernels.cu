@@ -111,18 +111,44 @@ static inline int grid_for(long long work, int threads, int cap = 148 * 16) {
 }
 
 // ----------------------------------------------------------------------- F0
-__global__ void se_cov_kernel(int64_t n, const double* __restrict__ x, double sq_alpha,
-                              double neg_half_inv_rho2, double jitter, double* __restrict__ K) {
-  const long long total = (long long)n * n;
-  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < total;
-       idx += (long long)gridDim.x * blockDim.x) {
-    const long long i = idx / n, j = idx - i * n;
-    const double d = x[i] - x[j];
-    // same association as the definition: (d*d)*c, then alpha^2 * exp(.), + jitter on i == j
-    const double e = __dmul_rn(__dmul_rn(d, d), neg_half_inv_rho2);
-    double v = __dmul_rn(sq_alpha, exp(e));
-    if (i == j) v = __dadd_rn(v, jitter);
-    K[idx] = v;
+// K is symmetric bit for bit (x_j - x_i = -(x_i - x_j) exactly, so the squares
+// agree): each CTA evaluates one 64 x 64 tile (I, J), I >= J, once, writes it,
+// and writes its transpose through shared memory as tile (J, I).  Half the
+// exp() evaluations of the elementwise form and no 64-bit index division;
+// both stores are coalesced 256-B rows.  Diagonal tiles are evaluated in full.
+constexpr int SE_T = 64;
+__global__ void __launch_bounds__(256) se_cov_kernel(int64_t n, const double* __restrict__ x, double sq_alpha,
+                                                     double neg_half_inv_rho2, double jitter,
+                                                     double* __restrict__ K) {
+  const int ti = blockIdx.y, tj = blockIdx.x;
+  if (tj > ti) return;
+  __shared__ double t[SE_T][SE_T + 1];
+  __shared__ double xi[SE_T], xj[SE_T];
+  const int tid = threadIdx.x, tx = tid & (SE_T - 1), ty = tid >> 6;
+  const int64_t i0 = (int64_t)ti * SE_T, j0 = (int64_t)tj * SE_T;
+  if (tid < SE_T) xi[tid] = (i0 + tid < n) ? x[i0 + tid] : 0.0;
+  else if (tid < 2 * SE_T) xj[tid - SE_T] = (j0 + tid - SE_T < n) ? x[j0 + tid - SE_T] : 0.0;
+  __syncthreads();
+#pragma unroll 4
+  for (int r = ty; r < SE_T; r += 4) {
+    const int64_t i = i0 + r, j = j0 + tx;
+    double v = 0.0;
+    if (i < n && j < n) {
+      const double d = xi[r] - xj[tx];
+      // same association as the definition: (d*d)*c, then alpha^2 * exp(.), + jitter on i == j
+      const double e = __dmul_rn(__dmul_rn(d, d), neg_half_inv_rho2);
+      v = __dmul_rn(sq_alpha, exp(e));
+      if (i == j) v = __dadd_rn(v, jitter);
+      K[i * n + j] = v;
+    }
+    t[r][tx] = v;
+  }
+  if (ti == tj) return;
+  __syncthreads();
+#pragma unroll 4
+  for (int r = ty; r < SE_T; r += 4) {
+    const int64_t row = j0 + r, col = i0 + tx;
+    if (row < n && col < n) K[row * n + col] = t[tx][r];
   }
 }
 
@@ -132,12 +158,11 @@ cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double 
   if (n == 0) return cudaSuccess;
   const double sq_alpha = alpha * alpha;
   const double c = -0.5 / (rho * rho);
-  se_cov_kernel<<<grid_for((long long)n * n, 256), 256, 0, st>>>(n, x, sq_alpha, c, jitter, K);
+  const unsigned T = (unsigned)((n + SE_T - 1) / SE_T);
+  se_cov_kernel<<<dim3(T, T), 256, 0, st>>>(n, x, sq_alpha, c, jitter, K);
   return cudaGetLastError();
 }
 
-// the owned 256-wide block columns J = q, q+G, ... of K, stored contiguously
-// (local column lc*256 + c  <->  global column (lc*G + q)*256 + c)
 // 2-D block-cyclic layout: rank (p, q) of a P x Q grid holds
 // the 256 x 256 tiles (I, J) with I % P == p, J % Q == q as local tile
 // (I / P, J / Q) of a row-major (rows x ncols) array.  Every local element is
@@ -978,20 +1003,16 @@ constexpr int G128_SMEM = (32 * G128_AP + NB * G128_BP) * (int)sizeof(double);
 // the lower triangle of A's storage is read; B_SYM: B read as sym(tril(B)).
 // 128 threads per 32 x 32 output tile; K staged through shared memory in
 // 128-deep chunks whose 64 global loads per thread are all issued before use.
+// One 32 x 32 output tile (m0, n0) of the product (device function: the
+// batched kernel below and the fused diagonal step use it).  Operands are read
+// through L2 (ld.global.cg): in the fused kernel they were written by other
+// CTAs of the same launch.
 template <int S, bool A_T, bool A_TRIL, bool B_SYM, bool C_SYM>
-__global__ void __launch_bounds__(128) gemmS_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
-                                                    const double* __restrict__ B, int64_t ldb, int64_t sB,
-                                                    double* __restrict__ C, int64_t ldc, int64_t sC,
-                                                    double sign, const int* status) {
-  if (*status != 0) return;
-  extern __shared__ double sm[];
+__device__ __forceinline__ void gemmS_tile(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                                           int64_t ldb, double* __restrict__ C, int64_t ldc, double sign, int m0,
+                                           int n0, double* sm) {
   double* As = sm;                 // [32][G128_AP]   As[m][k - k0]
   double* Bs = sm + 32 * G128_AP;  // [128][G128_BP]  Bs[k - k0][n]
-  A += (long long)blockIdx.z * sA;
-  B += (long long)blockIdx.z * sB;
-  C += (long long)blockIdx.z * sC;
-  const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
-  if (C_SYM && m0 < n0) return;  // strictly upper tile: written as the mirror of (n0, m0)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
   double acc[2][2][2] = {};
@@ -1002,14 +1023,14 @@ __global__ void __launch_bounds__(128) gemmS_kernel(const double* __restrict__ A
       const int idx = tid + q * 128;
       if (A_T) {
         const int k = k0 + (idx >> 5), m = m0 + (idx & 31);
-        va[q] = (A_TRIL && m > k) ? 0.0 : __ldg(A + (long long)k * lda + m);
+        va[q] = (A_TRIL && m > k) ? 0.0 : __ldcg(A + (long long)k * lda + m);
       } else {
         const int m = m0 + (idx >> 7), k = k0 + (idx & (NB - 1));
-        va[q] = (A_TRIL && k > m) ? 0.0 : __ldg(A + (long long)m * lda + k);
+        va[q] = (A_TRIL && k > m) ? 0.0 : __ldcg(A + (long long)m * lda + k);
       }
       const int k = k0 + (idx >> 5), gn = n0 + (idx & 31);
-      if (B_SYM) vb[q] = (k >= gn) ? __ldg(B + (long long)k * ldb + gn) : __ldg(B + (long long)gn * ldb + k);
-      else vb[q] = __ldg(B + (long long)k * ldb + gn);
+      if (B_SYM) vb[q] = (k >= gn) ? __ldcg(B + (long long)k * ldb + gn) : __ldcg(B + (long long)gn * ldb + k);
+      else vb[q] = __ldcg(B + (long long)k * ldb + gn);
     }
     if (k0) __syncthreads();
 #pragma unroll
@@ -1050,6 +1071,20 @@ __global__ void __launch_bounds__(128) gemmS_kernel(const double* __restrict__ A
         }
       }
     }
+}
+
+
+template <int S, bool A_T, bool A_TRIL, bool B_SYM, bool C_SYM>
+__global__ void __launch_bounds__(128) gemmS_kernel(const double* __restrict__ A, int64_t lda, int64_t sA,
+                                                    const double* __restrict__ B, int64_t ldb, int64_t sB,
+                                                    double* __restrict__ C, int64_t ldc, int64_t sC,
+                                                    double sign, const int* status) {
+  if (*status != 0) return;
+  extern __shared__ double sm[];
+  const int m0 = blockIdx.y * 32, n0 = blockIdx.x * 32;
+  if (C_SYM && m0 < n0) return;  // strictly upper tile: written as the mirror of (n0, m0)
+  gemmS_tile<S, A_T, A_TRIL, B_SYM, C_SYM>(A + (long long)blockIdx.z * sA, lda, B + (long long)blockIdx.z * sB, ldb,
+                                           C + (long long)blockIdx.z * sC, ldc, sign, m0, n0, sm);
 }
 
 template <int S, bool A_T, bool A_TRIL, bool B_SYM, bool C_SYM>
@@ -1101,6 +1136,87 @@ cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, co
                     cudaStream_t st, int n) {
   Prof prof_(PROF_MISC, 0.0, st, 24.0 * n * n);
   phi_sym_kernel<<<64, 256, 0, st>>>(S, Ssym, Dbar, ldd, n, status);
+  return cudaGetLastError();
+}
+
+// ---- R4 fused: the whole symbolic diagonal step in ONE launch ---------------
+//   P = sym(tril(D^T D_bar)); T = D^-T P; S = T D^-1;
+// Ssym = mirror(tril S); D_bar = Phi(S).  (S/32)^2 CTAs, one 32 x 32 tile of
+// each product per CTA, the three products separated by grid-wide barriers (a
+// counter in global memory, left at zero by each launch for the next; all
+// CTAs are co-resident: 64 CTAs of 128 threads).  Same tile arithmetic as the three gemmS launches +
+// phi_sym it replaces, so the result is bit-identical; it saves two launches
+// and their drain/fill per block step.
+__device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+template <int S>
+__global__ void __launch_bounds__(128) adj_diag_kernel(const double* __restrict__ D, int64_t ldl,
+                                                       double* __restrict__ Dbar, int64_t ldw,
+                                                       const double* __restrict__ Di, double* __restrict__ T1,
+                                                       double* __restrict__ T2, double* __restrict__ T3,
+                                                       double* __restrict__ Ssym, unsigned* ctr,
+                                                       const int* status) {
+  if (*status != 0) return;  // uniform: no kernel writes status concurrently with this one
+  extern __shared__ double sm[];
+  constexpr int TT = S / 32;
+  const unsigned nb = gridDim.x;
+  const int m0 = (blockIdx.x / TT) * 32, n0 = (blockIdx.x % TT) * 32;
+  if (m0 >= n0) gemmS_tile<S, true, true, false, true>(D, ldl, Dbar, ldw, T1, S, 1.0, m0, n0, sm);
+  grid_barrier(ctr, nb);
+  gemmS_tile<S, true, false, false, false>(Di, S, T1, S, T2, S, 1.0, m0, n0, sm);
+  grid_barrier(ctr, 2 * nb);
+  gemmS_tile<S, false, false, false, false>(T2, S, Di, S, T3, S, 1.0, m0, n0, sm);
+  grid_barrier(ctr, 3 * nb);
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < S * S; idx += nb * blockDim.x) {
+    const int a = idx / S, b = idx - a * S;
+    const double low = (a >= b) ? __ldcg(T3 + a * S + b) : __ldcg(T3 + b * S + a);
+    Ssym[idx] = low;
+    Dbar[(long long)a * ldw + b] = (a > b) ? low : (a == b ? 0.5 * low : 0.0);
+  }
+  // the last CTA out re-arms the barrier for the next launch (every CTA has
+  // passed all three barriers once ctr[1] reaches nb), so no memset is needed
+  if (threadIdx.x == 0 && atomicAdd(ctr + 1, 1u) == nb - 1) {
+    ctr[0] = 0;
+    ctr[1] = 0;
+    __threadfence();
+  }
+}
+
+cudaError_t adj_diag_fused(int S, const double* D, int64_t ldl, double* Dbar, int64_t ldw, const double* Di,
+                           double* T1, double* T2, double* T3, double* Ssym, unsigned* ctr, const int* status,
+                           cudaStream_t st) {
+  Prof prof_(PROF_SMALL, 6.0 * S * S * S, st, 8.0 * 10 * S * S);
+  cudaError_t e = cudaSuccess;
+  if (S == 256) {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(adj_diag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, G128_SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    adj_diag_kernel<256><<<64, 128, G128_SMEM, st>>>(D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
+  } else if (S == 128) {
+    static bool attr = false;
+    if (!attr) {
+      e = cudaFuncSetAttribute(adj_diag_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, G128_SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    adj_diag_kernel<128><<<16, 128, G128_SMEM, st>>>(D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
+  } else {
+    return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 

@@ -126,6 +126,14 @@ cudaError_t gemm_small(int S, bool a_t, bool a_tril, bool b_sym, const double* A
 // S (n x n, ld n): Ssym = mirror(tril(S)) -> ws; Dbar = Phi(S) = tril(S) with halved diagonal
 cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, const int* status,
                     cudaStream_t st, int n = 128);
+// the symbolic diagonal step fused (S = 128 or 256):
+// T1 = sym(tril(D^T D_bar)), T2 = D^-T T1, T3 = T2 D^-1 (S x S scratch each,
+// ld S), Ssym = mirror(tril T3), D_bar = Phi(T3); one launch with grid-wide
+// barriers on ctr[0..1] (device scratch that must be zero before the first
+// call; every launch leaves it zero)
+cudaError_t adj_diag_fused(int S, const double* D, int64_t ldl, double* Dbar, int64_t ldw, const double* Di,
+                           double* T1, double* T2, double* T3, double* Ssym, unsigned* ctr, const int* status,
+                           cudaStream_t st);
 // status = first base+k+1 with !(L[k][k] > 0 && finite), k < n
 cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st, int64_t base = 0);
 
