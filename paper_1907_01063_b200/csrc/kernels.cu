@@ -374,28 +374,45 @@ constexpr int TP = NB + 1;  // pitch of shared 128 x 128 staging tiles (doubles)
 constexpr int POTRF_SMEM = NB * TP * (int)sizeof(double);
 
 // column J of the warp factorization; templated so every register index is
-// static (a runtime-bounded loop would send row[] to local memory)
+// static (a runtime-bounded loop would send row[] to local memory).  Software
+// pipelined: (d, sq, y) = column J's pivot and its correctly rounded square
+// root / reciprocal, computed one step ahead.  The next pivot is formed on lane
+// J+1 from its own registers (l_{J+1,J} is its row[J]: the same fma as the
+// generic update on that lane, so bit-identical), shuffled, and its sqrt/rcp
+// chain is issued before this column's rank-1 update, whose independent
+// LDS/FMAs fill the chain's latency.  col is double-buffered (64 doubles), so
+// one __syncwarp per column suffices.
 template <int J>
-__device__ __forceinline__ void potrf_wstep(double (&row)[32], int lane, double* rc, double* col, int& bad) {
-  const double d = __shfl_sync(0xffffffffu, row[J], J);
+__device__ __forceinline__ void potrf_wstep(double (&row)[32], int lane, double* rc, double* col, int& bad,
+                                            double d, double sq, double y) {
   bad = (bad < 0 && !(d > 0.0)) ? J : bad;  // warp-uniform
-  double sq, y;
-  scaled_sqrt_rcp(d, sq, y);
   if (lane == J) {
     row[J] = sq;
     rc[J] = y;
   } else {
     row[J] = div_pos(row[J], sq, y);
   }
-  col[lane] = row[J];
+  double* cb = col + 32 * (J & 1);
+  cb[lane] = row[J];
+  double dn = 0.0, sqn = 0.0, yn = 0.0;
+  if constexpr (J + 1 < 32) dn = __shfl_sync(0xffffffffu, fma(-row[J], row[J], row[J + 1]), J + 1);
   __syncwarp();
+  if constexpr (J + 1 < 32) scaled_sqrt_rcp(dn, sqn, yn);
 #pragma unroll
   for (int c = J + 1; c < 32; ++c) {
-    const double lc = col[c];
+    const double lc = cb[c];
     if (lane >= c) row[c] = fma(-row[J], lc, row[c]);
   }
-  __syncwarp();
-  if constexpr (J + 1 < 32) potrf_wstep<J + 1>(row, lane, rc, col, bad);
+  if constexpr (J + 1 < 32) potrf_wstep<J + 1>(row, lane, rc, col, bad, dn, sqn, yn);
+  else __syncwarp();
+}
+
+// start the pipelined warp factorization (col: 64 doubles of shared memory)
+__device__ __forceinline__ void potrf_wstart(double (&row)[32], int lane, double* rc, double* col, int& bad) {
+  const double d0 = __shfl_sync(0xffffffffu, row[0], 0);
+  double sq0, y0;
+  scaled_sqrt_rcp(d0, sq0, y0);
+  potrf_wstep<0>(row, lane, rc, col, bad, d0, sq0, y0);
 }
 
 // warp 0: factor the 32 x 32 diagonal block at (c0, c0) of S in place;
@@ -406,7 +423,7 @@ __device__ __forceinline__ int potrf_wblock(double* S, int c0, int lane, double*
 #pragma unroll
   for (int c = 0; c < 32; ++c) row[c] = (c <= lane) ? Sr[c] : 0.0;
   int bad = -1;
-  potrf_wstep<0>(row, lane, rc + c0, col, bad);
+  potrf_wstart(row, lane, rc + c0, col, bad);
 #pragma unroll
   for (int c = 0; c < 32; ++c)
     if (c <= lane) Sr[c] = row[c];
@@ -420,7 +437,7 @@ __device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, 
                                                 int nv, int* status, int64_t info_base) {
   extern __shared__ double S[];
   __shared__ double rc[NB];   // 1 / L[j][j]
-  __shared__ double colb[32];
+  __shared__ double colb[64];
   __shared__ int fail_j;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const double* base = src;
@@ -559,7 +576,7 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
 // factorization of the diagonal-tile kernel (same arithmetic)
 __global__ void __launch_bounds__(128) potrf_w32_kernel(const double* A, double* L, int n, int64_t batch,
                                                        int* info) {
-  __shared__ double col[4][32], rcs[4][32];
+  __shared__ double col[4][64], rcs[4][32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * 4 + warp;
   if (b >= batch) return;  // warp-uniform
@@ -569,7 +586,7 @@ __global__ void __launch_bounds__(128) potrf_w32_kernel(const double* A, double*
   for (int c = 0; c < 32; ++c)
     row[c] = (lane < n) ? ((c <= lane && c < n) ? Ab[(int64_t)lane * n + c] : 0.0) : (c == lane ? 1.0 : 0.0);
   int bad = -1;
-  potrf_wstep<0>(row, lane, rcs[warp], col[warp], bad);
+  potrf_wstart(row, lane, rcs[warp], col[warp], bad);
   double* Lb = L + b * n * n;
   if (lane < n) {
 #pragma unroll
