@@ -84,6 +84,38 @@ __device__ __forceinline__ double div_pos(double x, double b, double y) {
   return fma(fma(-q, b, x), y, q);
 }
 
+// ---- programmatic dependent launch (PDL) ----------------------------------
+// The dependent kernels of the panel chain and of the adjoint block step are
+// launched with cudaLaunchAttributeProgrammaticStreamSerialization (launch_pdl):
+// their CTAs may be scheduled while the stream predecessor drains, which hides
+// the launch latency at each kernel boundary.  Every kernel launched that way
+// calls pdl_wait() before touching global memory (it returns once the
+// predecessor grid has completed and its writes are visible), then
+// pdl_trigger() so its own successor can be scheduled.  Without the launch
+// attribute both are no-ops.  STAN_CL_PDL=0 disables the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_enter() {
+  pdl_wait();
+  pdl_trigger();
+}
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 // Device-side status word shared by the kernels of one call: 0 = fine,
 // k > 0 = first failing pivot row + 1 (LAPACK info).  Kernels that see a
 // nonzero word exit early (the result is unspecified on failure).

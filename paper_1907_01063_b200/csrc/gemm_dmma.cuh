@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_CTAS) gemm_dmma_kernel(Ge
   constexpr int MI = CF::MI, NI = CF::NI, BK = CF::BK;
   using TA = Tile<BM, A_KMAJ, BK>;
   using TB = Tile<BN, B_KMAJ, BK>;
+  pdl_enter();
   if (p.status && *p.status != 0) return;
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
@@ -290,7 +291,7 @@ cudaError_t launch_gemm(const GemmArgs& p, int splits, cudaStream_t st) {
     grid = dim3(p.N / CF::BN, p.M / CF::BM, MODE == MODE_SPLITK ? splits : 1);
   }
   if (grid.x == 0 || grid.y == 0) return cudaSuccess;
-  kern<<<grid, CF::THREADS, smem, st>>>(p);
+  return launch_pdl(kern, grid, CF::THREADS, smem, st, p);
   return cudaGetLastError();
 }
 

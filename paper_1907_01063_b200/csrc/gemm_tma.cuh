@@ -191,6 +191,7 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
   using SA = Slab<BM, A_KMAJ, BKS>;
   using SB = Slab<BN, B_KMAJ, BKS>;
   using SM = Smem<CF, A_KMAJ, B_KMAJ>;
+  pdl_enter();
   if (p.status && *p.status != 0) return;
   if ((int)blockIdx.x >= nitems) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -390,8 +391,7 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reser
   // reserve_sms: SMs left free for kernels on other streams
   const int nsm = (tma_num_sms() - (reserve_sms > 0 && reserve_sms < tma_num_sms() ? reserve_sms : 0)) * CF::MINB;
   const int grid = nitems < nsm ? nitems : nsm;
-  kern<<<grid, CF::NCONS + 32, SM::TOTAL, st>>>(ma, mb, p, nitems, map);
-  return cudaGetLastError();
+  return launch_pdl(kern, grid, CF::NCONS + 32, SM::TOTAL, st, ma, mb, p, nitems, map);
 }
 
 }  // namespace stancl

@@ -103,6 +103,14 @@ void prof_read(int kind, double* ms, double* flops, long long* count, double* by
   if (bytes) *bytes = g_prof.bytes[kind];
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("STAN_CL_PDL");
+    return !e || atoi(e) != 0;
+  }();
+  return on;
+}
+
 static inline int grid_for(long long work, int threads, int cap = 148 * 16) {
   long long b = (work + threads - 1) / threads;
   if (b < 1) b = 1;
@@ -330,6 +338,7 @@ cudaError_t init_pad(double* W, int64_t n, int64_t N, double diag_pad, cudaStrea
 // dst[rows x cols] (ldd) <- src (lds); cols even, 16-B aligned rows
 __global__ void copy_block_kernel(const double* __restrict__ src, int64_t lds, double* __restrict__ dst,
                                   int64_t ldd, int64_t rows, int64_t cols) {
+  pdl_enter();
   const long long half = rows * cols / 2;
   for (long long h = blockIdx.x * (long long)blockDim.x + threadIdx.x; h < half;
        h += (long long)gridDim.x * blockDim.x) {
@@ -342,8 +351,7 @@ cudaError_t copy_block(const double* src, int64_t lds, double* dst, int64_t ldd,
                        cudaStream_t st) {
   if (rows == 0 || cols == 0) return cudaSuccess;
   Prof prof_(PROF_MISC, 0.0, st, 16.0 * rows * cols);
-  copy_block_kernel<<<grid_for(rows * cols / 2, 256), 256, 0, st>>>(src, lds, dst, ldd, rows, cols);
-  return cudaGetLastError();
+  return launch_pdl(copy_block_kernel, grid_for(rows * cols / 2, 256), 256, 0, st, src, lds, dst, ldd, rows, cols);
 }
 
 cudaError_t zero_upper(double* A, int64_t n, int64_t ld, cudaStream_t st) {
@@ -547,6 +555,7 @@ __device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, 
 
 __global__ void __launch_bounds__(256, 1) potrf_tile_kernel(double* W, int64_t ld, int64_t k0,
                                                             int* status) {
+  pdl_enter();
   if (*status != 0) return;
   double* base = W + k0 * ld + k0;
   potrf_tile_body(base, ld, base, ld, NB, status, k0);
@@ -567,8 +576,7 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  potrf_tile_kernel<<<1, 256, POTRF_SMEM, st>>>(W, ld, k0, status);
-  return cudaGetLastError();
+  return launch_pdl(potrf_tile_kernel, 1, 256, POTRF_SMEM, st, W, ld, k0, status);
 }
 
 // ---- NEXT-4, n <= 32: one WARP per matrix, everything in registers/shared ----
@@ -736,6 +744,7 @@ constexpr int TRSM_TP = TRSM_W + 1;
 
 __global__ void __launch_bounds__(256, 2) trsm_panel_kernel(double* W, int64_t ld, int64_t k0,
                                                             int64_t r0, const int* status) {
+  pdl_enter();
   if (*status != 0) return;
   __shared__ double LT[TRSM_W * TRSM_TP];
   __shared__ double dg[TRSM_W], rdg[TRSM_W];  // L_jj and RN(1 / L_jj)
@@ -780,8 +789,7 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
   if (r1 <= r0) return cudaSuccess;
   Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st, 16.0 * (r1 - r0) * NB + 4.0 * NB * NB);
   const int blocks = (int)((r1 - r0) / TRSM_ROWS);
-  trsm_panel_kernel<<<blocks, 256, 0, st>>>(W, ld, k0, r0, status);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(trsm_panel_kernel, blocks, 256, 0, st, W, ld, k0, r0, status);
   if (e != cudaSuccess) return e;
   // Ac -= Xa Lb^T: A = Xa (rows x 64, k-major), B = Lb (64 x 64, n x k), C = Ac
   double* Xa = W + r0 * ld + k0;
@@ -789,7 +797,8 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
   GemmArgs p{Xa, ld, Lb, ld, Xa + TRSM_W, ld, (int)(r1 - r0), TRSM_W, TRSM_W, TRSM_W, -1.0, 1, 0, status, 0};
   e = launch_gemm<gemm::CfgW8, true, true, MODE_FULL>(p, 1, st);
   if (e != cudaSuccess) return e;
-  trsm_panel_kernel<<<blocks, 256, 0, st>>>(W, ld, k0 + TRSM_W, r0, status);
+  e = launch_pdl(trsm_panel_kernel, blocks, 256, 0, st, W, ld, k0 + TRSM_W, r0, status);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -920,6 +929,7 @@ cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const doubl
 
 __global__ void splitk_reduce_sub_kernel(const double* __restrict__ P, int splits, int M, int N,
                                          double* __restrict__ dst, int64_t ldd, const int* status) {
+  pdl_enter();
   if (*status != 0) return;
   const long long half = (long long)M * N / 2;
   const long long plane = (long long)M * N;
@@ -945,9 +955,8 @@ cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double*
                               const int* status, cudaStream_t st) {
   Prof prof_(PROF_MISC, 0.0, st, 8.0 * (splits + 2.0) * M * N);
   if (M == 0 || N == 0) return cudaSuccess;
-  splitk_reduce_sub_kernel<<<grid_for((long long)M * N / 2, 256), 256, 0, st>>>(P, splits, M, N, dst,
-                                                                                ldd, status);
-  return cudaGetLastError();
+  return launch_pdl(splitk_reduce_sub_kernel, grid_for((long long)M * N / 2, 256), 256, 0, st, P, splits, M, N, dst,
+                    ldd, status);
 }
 
 // ------------------------------------------------------------- R1/R4 helpers
@@ -1184,6 +1193,7 @@ __global__ void __launch_bounds__(128) adj_diag_kernel(const double* __restrict_
                                                        double* __restrict__ T2, double* __restrict__ T3,
                                                        double* __restrict__ Ssym, unsigned* ctr,
                                                        const int* status) {
+  pdl_enter();
   if (*status != 0) return;  // uniform: no kernel writes status concurrently with this one
   extern __shared__ double sm[];
   constexpr int TT = S / 32;
@@ -1222,7 +1232,8 @@ cudaError_t adj_diag_fused(int S, const double* D, int64_t ldl, double* Dbar, in
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    adj_diag_kernel<256><<<64, 128, G128_SMEM, st>>>(D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
+    e = launch_pdl(adj_diag_kernel<256>, 64, 128, G128_SMEM, st, D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
+    if (e != cudaSuccess) return e;
   } else if (S == 128) {
     static bool attr = false;
     if (!attr) {
@@ -1230,7 +1241,8 @@ cudaError_t adj_diag_fused(int S, const double* D, int64_t ldl, double* Dbar, in
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    adj_diag_kernel<128><<<16, 128, G128_SMEM, st>>>(D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
+    e = launch_pdl(adj_diag_kernel<128>, 16, 128, G128_SMEM, st, D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
+    if (e != cudaSuccess) return e;
   } else {
     return cudaErrorInvalidValue;
   }
