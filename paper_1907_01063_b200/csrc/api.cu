@@ -64,6 +64,13 @@ int cuda_fail(cudaError_t e, const char* where) {
   } while (0)
 
 inline int64_t round_up(int64_t n, int64_t b) { return (n + b - 1) / b * b; }
+
+// no programmatic dependent launch inside the host-streamed entry points
+// (kernels.h pdl_allow: measured 185 -> 202 ms per e2e step with it on)
+struct PdlOff {
+  PdlOff() { pdl_allow(false); }
+  ~PdlOff() { pdl_allow(true); }
+};
 inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
 
 bool ranges_overlap(const void* a, const void* b, size_t bytes) {
@@ -823,6 +830,7 @@ int cholesky_host_enqueue(int64_t n, const double* A, double* L) {
 }
 
 int stan_cl_cholesky_host(int64_t n, const double* A, double* L) {
+  PdlOff pdl_off_;
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!A || !L) return STAN_CL_EINVAL;
@@ -878,6 +886,7 @@ int adjoint_host_enqueue(int64_t n, const double* L, const double* L_bar, double
 }
 
 int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar) {
+  PdlOff pdl_off_;
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
@@ -1088,6 +1097,7 @@ struct Grid {
 // per-rank device scratch (doubles), laid out by DistPlan
 struct DistPlan {
   size_t pan, cbuf, stage, dinv, dbuf, lrow, part, z, sbuf, tmp, total;
+  size_t pan_sz = 0, cbuf_sz = 0, stage_sz = 0;  // forward: two sets (lookahead double buffering)
 };
 DistPlan dist_plan(const Grid& gr, int p, int q, bool adjoint) {
   DistPlan d{};
@@ -1099,11 +1109,16 @@ DistPlan dist_plan(const Grid& gr, int p, int q, bool adjoint) {
     return at;
   };
   const int64_t R = gr.R(p), C = gr.C(q);
-  d.pan = take((R + 1) * t2);  // [L_kk | panel rows] (forward), C_bar D^-1 rows (adjoint)
-  if (!adjoint) {
-    d.cbuf = take(gr.P > 1 ? C * t2 : 0);
-    d.stage = take(gr.P > 1 ? (size_t)gr.P * (C + 1) * t2 : 0);
+  auto a32 = [](size_t c) { return (c + 31) / 32 * 32; };
+  if (!adjoint) {  // two buffer sets: panel k+1 is formed while panel k is consumed
+    d.pan_sz = a32((R + 1) * t2);  // [L_kk | panel rows]
+    d.cbuf_sz = a32(gr.P > 1 ? C * t2 : 0);
+    d.stage_sz = a32(gr.P > 1 ? (size_t)gr.P * (C + 1) * t2 : 0);
+    d.pan = take(2 * d.pan_sz);
+    d.cbuf = take(2 * d.cbuf_sz);
+    d.stage = take(2 * d.stage_sz);
   } else {
+    d.pan = take((R + 1) * t2);  // C_bar D^-1 rows
     d.dinv = take(C * t2);
     d.dbuf = take(t2);
     d.lrow = take(gr.P > 1 ? C * t2 : 0);
@@ -1134,6 +1149,9 @@ struct Rank {
   DistPlan pl;
   int* status;
   double* at(size_t off) const { return base + off; }
+  double* pan(int b) const { return base + pl.pan + b * pl.pan_sz; }
+  double* cbuf(int b) const { return base + pl.cbuf + b * pl.cbuf_sz; }
+  double* stage(int b) const { return base + pl.stage + b * pl.stage_sz; }
 };
 
 struct Comm {
@@ -1194,90 +1212,128 @@ struct Comm {
     if (rc_) return rc_;        \
   } while (0)
 
-int dist_factor(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
-  cudaStream_t st = g.stream;
+// forward phases (a)-(d) of step k into buffer set b, on stream st
+int dist_panel(std::vector<Rank>& rs, const Grid& gr, Comm& cm, int64_t k, int b, cudaStream_t st) {
   const int64_t T = gr.T, t2 = DB * DB;
   const int P = gr.P, Q = gr.Q;
   const int64_t Lc = std::lcm((int64_t)P, (int64_t)Q);
-  for (int64_t k = 0; k < T; ++k) {
-    const int pk = (int)(k % P), qk = (int)(k % Q);
-    const int64_t c0 = k * DB;
-    // (a) L_kk = chol(A_kk) on the diagonal owner, in place, then into pan[0]
-    for (auto& r : rs) {
-      if (r.p != pk || r.q != qk) continue;
-      double* tile = r.W + (k / P) * DB * r.ld + (k / Q) * DB;
-      RC(panel(tile - c0 * r.ld - c0, r.ld, c0, c0 + DB, DB, r.status, st));  // view: rows [c0, c0 + DB)
-      CK(copy_block(tile, r.ld, r.at(r.pl.pan), DB, DB, DB, st));
-    }
-    RC(cm.bcast(rs, false, qk, pk, [](Rank& r) { return r.at(r.pl.pan); }, (size_t)t2, st));
-    // (b) process column qk: L_Ik = A_Ik L_kk^-T for the local rows I > k
-    //     (two 128-wide substitutions with the cross update, as the forward panel)
-    for (auto& r : rs) {
-      if (r.q != qk) continue;
-      const int64_t li0 = below(k + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB;
-      if (mloc == 0) continue;
-      double* pan = r.at(r.pl.pan);
-      double* A = r.W + li0 * DB * r.ld + (k / Q) * DB;
-      CK(copy_block(A, r.ld, pan + t2, DB, mloc, DB, st));
-      CK(trsm_panel(pan, DB, 0, DB, DB + mloc, r.status, st));
-      CK(gemm_full(true, true, (int)mloc, NB, NB, -1.0, 1, pan + t2, DB, pan + NB * DB, DB, pan + t2 + NB, DB,
-                   r.status, st, 0, PROF_LOOKAHEAD));
-      CK(trsm_panel(pan, DB, NB, DB, DB + mloc, r.status, st));
-      CK(copy_block(pan + t2, DB, A, r.ld, mloc, DB, st));
-    }
-    // (c) row broadcast of the panel rows along every process row
-    for (int p = 0; p < P; ++p) {
-      const int64_t mloc = (gr.R(p) - below(k + 1, P, p)) * DB;
-      RC(cm.bcast(rs, true, p, qk, [](Rank& r) { return r.at(r.pl.pan) + DB * DB; }, (size_t)mloc * DB, st));
-    }
-    // (d) column exchange (P > 1): rank (p', q) sends the tiles L_Jk, J > k,
-    //     J % P == p', J % Q == q (J = J0 + t * lcm(P, Q)) to its process column
-    if (P > 1) {
-      for (int q = 0; q < Q; ++q) {
-        for (int pp = 0; pp < P; ++pp) {
-          int64_t J0 = -1;
-          for (int64_t J = k + 1; J < std::min(T, k + 1 + Lc); ++J)
-            if (J % P == pp && J % Q == q) {
-              J0 = J;
-              break;
-            }
-          if (J0 < 0) continue;
-          const int64_t cnt = (T - 1 - J0) / Lc + 1;
-          Rank* root = cm.sim ? cm.find(rs, pp, q) : (rs[0].p == pp && rs[0].q == q ? &rs[0] : nullptr);
-          const size_t soff = (size_t)pp * (gr.C(q) + 1) * t2;
-          if (root) {
-            const int64_t li0 = below(k + 1, P, pp);
-            CK(copy_tiles(root->at(root->pl.pan) + t2, J0 / P - li0, Lc / P, root->at(root->pl.stage) + soff, 0, 1,
-                          cnt, t2, st));
+  const int pk = (int)(k % P), qk = (int)(k % Q);
+  const int64_t c0 = k * DB;
+  // (a) L_kk = chol(A_kk) on the diagonal owner, in place, then into pan[0]
+  for (auto& r : rs) {
+    if (r.p != pk || r.q != qk) continue;
+    double* tile = r.W + (k / P) * DB * r.ld + (k / Q) * DB;
+    RC(panel(tile - c0 * r.ld - c0, r.ld, c0, c0 + DB, DB, r.status, st));  // view: rows [c0, c0 + DB)
+    CK(copy_block(tile, r.ld, r.pan(b), DB, DB, DB, st));
+  }
+  RC(cm.bcast(rs, false, qk, pk, [b](Rank& r) { return r.pan(b); }, (size_t)t2, st));
+  // (b) process column qk: L_Ik = A_Ik L_kk^-T for the local rows I > k
+  //     (two 128-wide substitutions with the cross update, as the forward panel)
+  for (auto& r : rs) {
+    if (r.q != qk) continue;
+    const int64_t li0 = below(k + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB;
+    if (mloc == 0) continue;
+    double* pan = r.pan(b);
+    double* A = r.W + li0 * DB * r.ld + (k / Q) * DB;
+    CK(copy_block(A, r.ld, pan + t2, DB, mloc, DB, st));
+    CK(trsm_panel(pan, DB, 0, DB, DB + mloc, r.status, st));
+    CK(gemm_full(true, true, (int)mloc, NB, NB, -1.0, 1, pan + t2, DB, pan + NB * DB, DB, pan + t2 + NB, DB,
+                 r.status, st, 0, PROF_LOOKAHEAD, /*allow_persistent=*/false));
+    CK(trsm_panel(pan, DB, NB, DB, DB + mloc, r.status, st));
+    CK(copy_block(pan + t2, DB, A, r.ld, mloc, DB, st));
+  }
+  // (c) row broadcast of the panel rows along every process row
+  for (int p = 0; p < P; ++p) {
+    const int64_t mloc = (gr.R(p) - below(k + 1, P, p)) * DB;
+    RC(cm.bcast(rs, true, p, qk, [b](Rank& r) { return r.pan(b) + DB * DB; }, (size_t)mloc * DB, st));
+  }
+  // (d) column exchange (P > 1): rank (p', q) sends the tiles L_Jk, J > k,
+  //     J % P == p', J % Q == q (J = J0 + t * lcm(P, Q)) to its process column
+  if (P > 1) {
+    for (int q = 0; q < Q; ++q) {
+      for (int pp = 0; pp < P; ++pp) {
+        int64_t J0 = -1;
+        for (int64_t J = k + 1; J < std::min(T, k + 1 + Lc); ++J)
+          if (J % P == pp && J % Q == q) {
+            J0 = J;
+            break;
           }
-          RC(cm.bcast(rs, false, q, pp, [soff](Rank& r) { return r.at(r.pl.stage) + soff; }, (size_t)cnt * t2,
-                      st));
-          for (auto& r : rs) {
-            if (r.q != q || r.p == pp) continue;
-            CK(copy_tiles(r.at(r.pl.stage) + soff, 0, 1, r.at(r.pl.cbuf), J0 / Q, Lc / Q, cnt, t2, st));
-          }
+        if (J0 < 0) continue;
+        const int64_t cnt = (T - 1 - J0) / Lc + 1;
+        Rank* root = cm.sim ? cm.find(rs, pp, q) : (rs[0].p == pp && rs[0].q == q ? &rs[0] : nullptr);
+        const size_t soff = (size_t)pp * (gr.C(q) + 1) * t2;
+        if (root) {
+          const int64_t li0 = below(k + 1, P, pp);
+          CK(copy_tiles(root->pan(b) + t2, J0 / P - li0, Lc / P, root->stage(b) + soff, 0, 1, cnt, t2, st));
+        }
+        RC(cm.bcast(rs, false, q, pp, [soff, b](Rank& r) { return r.stage(b) + soff; }, (size_t)cnt * t2, st));
+        for (auto& r : rs) {
+          if (r.q != q || r.p == pp) continue;
+          CK(copy_tiles(r.stage(b) + soff, 0, 1, r.cbuf(b), J0 / Q, Lc / Q, cnt, t2, st));
         }
       }
     }
-    // (e) trailing update of the local lower tiles I >= J > k
-    for (auto& r : rs) {
-      const int64_t li0 = below(k + 1, P, r.p), R = gr.R(r.p);
-      const double* pan = r.at(r.pl.pan) + t2;
-      for (int64_t lj = below(k + 1, Q, r.q); lj < gr.C(r.q); ++lj) {
-        const int64_t J = lj * Q + r.q, li_s = below(J, P, r.p);
-        if (li_s >= R) continue;
-        const double* Ljk = (J % P == r.p) ? pan + (J / P - li0) * t2 : r.at(r.pl.cbuf) + lj * t2;
-        CK(gemm_full(true, true, (int)((R - li_s) * DB), (int)DB, (int)DB, -1.0, 1, pan + (li_s - li0) * t2, DB,
-                     Ljk, DB, r.W + li_s * DB * r.ld + lj * DB, r.ld, r.status, st,
-                     /*lower_only=*/(li_s * P + r.p == J) ? 1 : 0, PROF_SYRK));
-      }
+  }
+  return STAN_CL_OK;
+}
+
+// forward phase (e) of step k (buffer set b): A_IJ -= L_Ik L_Jk^T on the local
+// lower tiles I >= J with J in [Jlo, Jhi)
+int dist_update(std::vector<Rank>& rs, const Grid& gr, int64_t k, int b, int64_t Jlo, int64_t Jhi, cudaStream_t st,
+                int reserve) {
+  const int64_t t2 = DB * DB;
+  const int P = gr.P, Q = gr.Q;
+  for (auto& r : rs) {
+    const int64_t li0 = below(k + 1, P, r.p), R = gr.R(r.p);
+    const double* pan = r.pan(b) + t2;
+    for (int64_t lj = below(Jlo, Q, r.q); lj < below(Jhi, Q, r.q); ++lj) {
+      const int64_t J = lj * Q + r.q, li_s = below(J, P, r.p);
+      if (li_s >= R) continue;
+      const double* Ljk = (J % P == r.p) ? pan + (J / P - li0) * t2 : r.cbuf(b) + lj * t2;
+      CK(gemm_full(true, true, (int)((R - li_s) * DB), (int)DB, (int)DB, -1.0, 1, pan + (li_s - li0) * t2, DB,
+                   Ljk, DB, r.W + li_s * DB * r.ld + lj * DB, r.ld, r.status, st,
+                   /*lower_only=*/(li_s * P + r.p == J) ? 1 : 0, PROF_SYRK, true, reserve));
     }
   }
+  return STAN_CL_OK;
+}
+
+// Right-looking distributed forward with one step of lookahead: the panel of
+// step k+1 (diagonal factorization, panel solve, row broadcasts, column
+// exchange) runs on the high-priority side stream while the main stream
+// applies the rest of step k's trailing update, which leaves SMs free for the
+// panel kernels and the NCCL kernels.  Buffer sets alternate by step parity.
+//   main: wait panel k; update block column k+1 (the ranks of column (k+1)%Q)
+//   side: wait that; panel k+1
+//   main: update block columns > k+1
+int dist_factor(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
+  cudaStream_t main = g.stream;
+  const int64_t T = gr.T;
+  RC(ensure_side(2 * T + 2));
+  cudaStream_t side = g.side;
+  cudaEvent_t* ev = g.events.data();  // ev[0]: start; ev[1 + 2k]: panel k done; ev[2 + 2k]: column k+1 updated
+  constexpr int kReserve = 16;        // SMs the bulk update leaves to the panel / NCCL kernels
+  CK(cudaEventRecord(ev[0], main));
+  CK(cudaStreamWaitEvent(side, ev[0], 0));
+  RC(dist_panel(rs, gr, cm, 0, 0, side));
+  CK(cudaEventRecord(ev[1], side));
+  for (int64_t k = 0; k < T; ++k) {
+    const int b = (int)(k & 1);
+    CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
+    if (k + 1 == T) break;
+    RC(dist_update(rs, gr, k, b, k + 1, k + 2, main, 0));
+    CK(cudaEventRecord(ev[2 + 2 * k], main));
+    CK(cudaStreamWaitEvent(side, ev[2 + 2 * k], 0));
+    RC(dist_panel(rs, gr, cm, k + 1, b ^ 1, side));
+    CK(cudaEventRecord(ev[1 + 2 * (k + 1)], side));
+    RC(dist_update(rs, gr, k, b, k + 2, T, main, kReserve));
+  }
+  const int P = gr.P, Q = gr.Q;
   for (auto& r : rs)  // strict upper of the local diagonal tiles
     for (int64_t J = 0; J < T; ++J)
       if (J % P == r.p && J % Q == r.q) {
         double* tile = r.W + (J / P) * DB * r.ld + (J / Q) * DB;
-        CK(zero_tile_upper(tile, r.ld, 0, (int)DB, st));
+        CK(zero_tile_upper(tile, r.ld, 0, (int)DB, main));
       }
   return STAN_CL_OK;
 }

@@ -103,12 +103,14 @@ void prof_read(int kind, double* ms, double* flops, long long* count, double* by
   if (bytes) *bytes = g_prof.bytes[kind];
 }
 
+static bool g_pdl_allowed = true;
+void pdl_allow(bool on) { g_pdl_allowed = on; }
 bool pdl_enabled() {
   static const bool on = [] {
     const char* e = getenv("STAN_CL_PDL");
     return !e || atoi(e) != 0;
   }();
-  return on;
+  return on && g_pdl_allowed;
 }
 
 static inline int grid_for(long long work, int threads, int cap = 148 * 16) {
@@ -858,12 +860,12 @@ const CfgSel& cfgsel() {
   return s;
 }
 
-cudaError_t gemm_full_persist(bool a_kmaj, bool b_kmaj, const GemmArgs& p, cudaStream_t st) {
+cudaError_t gemm_full_persist(bool a_kmaj, bool b_kmaj, const GemmArgs& p, cudaStream_t st, int reserve = 0) {
   using CF = tg::CfgT32;
-  if (a_kmaj && b_kmaj) return launch_tma<CF, true, true, MODE_FULL>(p, 1, st);
-  if (a_kmaj && !b_kmaj) return launch_tma<CF, true, false, MODE_FULL>(p, 1, st);
-  if (!a_kmaj && b_kmaj) return launch_tma<CF, false, true, MODE_FULL>(p, 1, st);
-  return launch_tma<CF, false, false, MODE_FULL>(p, 1, st);
+  if (a_kmaj && b_kmaj) return launch_tma<CF, true, true, MODE_FULL>(p, 1, st, reserve);
+  if (a_kmaj && !b_kmaj) return launch_tma<CF, true, false, MODE_FULL>(p, 1, st, reserve);
+  if (!a_kmaj && b_kmaj) return launch_tma<CF, false, true, MODE_FULL>(p, 1, st, reserve);
+  return launch_tma<CF, false, false, MODE_FULL>(p, 1, st, reserve);
 }
 
 template <class CF>
@@ -878,7 +880,7 @@ cudaError_t gemm_full_cfg(bool a_kmaj, bool b_kmaj, const GemmArgs& p, cudaStrea
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st, int lower_only, int prof_kind,
-                      bool allow_persistent) {
+                      bool allow_persistent, int reserve_sms) {
   if (M == 0 || N == 0) return cudaSuccess;
   Prof prof_(prof_kind, 2.0 * M * N * K, st, (beta ? 16.0 : 8.0) * M * N + 8.0 * ((double)M * K + (double)N * K));
   GemmArgs p{A, lda, B, ldb, C, ldc, M, N, K, K, sign, beta, lower_only, status, cfgsel().pingpong};
@@ -889,7 +891,7 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
     if (N != gemm::CfgBig::BN) return cudaErrorInvalidValue;
     return gemm_full_cfg<gemm::CfgBig>(a_kmaj, b_kmaj, p, st);
   }
-  if (cfgsel().tma_gemm && allow_persistent) return gemm_full_persist(a_kmaj, b_kmaj, p, st);
+  if (cfgsel().tma_gemm && allow_persistent) return gemm_full_persist(a_kmaj, b_kmaj, p, st, reserve_sms);
   switch (cfgsel().gemm) {
     case CFG_BIG: return gemm_full_cfg<gemm::CfgBig>(a_kmaj, b_kmaj, p, st);
     case CFG_W8: return gemm_full_cfg<gemm::CfgW8>(a_kmaj, b_kmaj, p, st);

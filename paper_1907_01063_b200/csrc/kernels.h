@@ -35,6 +35,10 @@ struct Prof {
   cudaStream_t st_;
   cudaEvent_t e0_ = nullptr, e1_ = nullptr;
 };
+// programmatic dependent launch on/off for the calls that follow (common.cuh;
+// the host-streamed entry points turn it off: early-resident dependent CTAs
+// would hold SMs the copy-stream kernels of the streamed transfers need)
+void pdl_allow(bool on);
 void prof_enable(unsigned mask);  // bit k enables class k
 bool prof_active();
 void prof_reset();
@@ -89,11 +93,12 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
 //   a_kmaj: A is M x K row-major (else K x M);  b_kmaj: B is N x K (else K x N)
 // lower_only: store only r >= c (relative to C); prof_kind: profiling class;
 // allow_persistent = false keeps the one-tile-per-CTA kernel (for work issued on
-// the lookahead side stream, which must not hold SMs the trailing update needs)
+// the lookahead side stream, which must not hold SMs the trailing update needs);
+// reserve_sms: the persistent kernel leaves that many SMs free for other streams
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st, int lower_only = 0,
-                      int prof_kind = 1, bool allow_persistent = true);
+                      int prof_kind = 1, bool allow_persistent = true, int reserve_sms = 0);
 // lower tiles of square C[M x M] -= A A'^T style: C -= A B^T, A, B both k-major (SYRK)
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                           double* C, int64_t ldc, const int* status, cudaStream_t st);
