@@ -408,11 +408,11 @@ __device__ __forceinline__ void potrf_wstep(double (&row)[32], int lane, double*
   if constexpr (J + 1 < 32) dn = __shfl_sync(0xffffffffu, fma(-row[J], row[J], row[J + 1]), J + 1);
   __syncwarp();
   if constexpr (J + 1 < 32) scaled_sqrt_rcp(dn, sqn, yn);
+  // unpredicated: entries above the diagonal (c > lane) also take the update,
+  // but they are never read as pivots, columns or results (only c <= lane is
+  // written back), and a predicated fma compiles to fma + 2 selects + 2 moves
 #pragma unroll
-  for (int c = J + 1; c < 32; ++c) {
-    const double lc = cb[c];
-    if (lane >= c) row[c] = fma(-row[J], lc, row[c]);
-  }
+  for (int c = J + 1; c < 32; ++c) row[c] = fma(-row[J], cb[c], row[c]);
   if constexpr (J + 1 < 32) potrf_wstep<J + 1>(row, lane, rc, col, bad, dn, sqn, yn);
   else __syncwarp();
 }
