@@ -440,6 +440,62 @@ __device__ __forceinline__ int potrf_wblock(double* S, int c0, int lane, double*
   return bad;
 }
 
+// optional phase timers (tools/potrf_lab.cu defines STANCL_POTRF_TIMERS and
+// provides `__device__ long long g_ptimer[8]`): thread 0 accumulates clock64
+// deltas per phase; compiled out of the library
+#ifdef STANCL_POTRF_TIMERS
+#define PT_MARK(slot)                                   \
+  do {                                                  \
+    if (threadIdx.x == 0) {                             \
+      const long long now_ = clock64();                 \
+      g_ptimer[slot] += now_ - pt_last_;                \
+      pt_last_ = now_;                                  \
+    }                                                   \
+  } while (0)
+#else
+#define PT_MARK(slot) \
+  do {                \
+  } while (0)
+#endif
+
+// phase (c) of one 32-column block, templated on its column offset so the
+// trailing extent R is static (runtime-bounded predicates compile to
+// select/move pairs): S[i][k] -= sum_j X[i][j] X[k][j], r0 <= k <= i
+template <int C0>
+__device__ __forceinline__ void potrf_syrk_block(double* S, int tid) {
+  constexpr int c0 = C0, r0 = c0 + 32, R = NB - r0;
+  constexpr int AMAX = R / 16;  // row / column groups of 16 present (6, 4, 2)
+  const int ti = tid >> 4, tj = tid & 15;
+  double acc[AMAX][AMAX];
+#pragma unroll
+  for (int a = 0; a < AMAX; ++a)
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      const int i = ti + 16 * a, k = tj + 16 * b;
+      acc[a][b] = (k <= i) ? S[(r0 + i) * TP + r0 + k] : 0.0;
+    }
+#pragma unroll 4
+  for (int j = 0; j < 32; ++j) {
+    double xi[AMAX], xk[AMAX];
+#pragma unroll
+    for (int a = 0; a < AMAX; ++a) {
+      xi[a] = S[(r0 + ti + 16 * a) * TP + c0 + j];
+      xk[a] = S[(r0 + tj + 16 * a) * TP + c0 + j];
+    }
+#pragma unroll
+    for (int a = 0; a < AMAX; ++a)
+#pragma unroll
+      for (int b = 0; b <= a; ++b) acc[a][b] = fma(-xi[a], xk[b], acc[a][b]);
+  }
+#pragma unroll
+  for (int a = 0; a < AMAX; ++a)
+#pragma unroll
+    for (int b = 0; b <= a; ++b) {
+      const int i = ti + 16 * a, k = tj + 16 * b;
+      if (k <= i) S[(r0 + i) * TP + r0 + k] = acc[a][b];
+    }
+}
+
 // One tile: src (lds) -> dst (ldd), the leading nv x nv block (nv <= 128) is the
 // matrix; the rest of the 128 x 128 tile is identity padding (pivots 1, never
 // fails).  On failure status <- info_base + j + 1 (first failing column j).
@@ -450,6 +506,9 @@ __device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, 
   __shared__ double colb[64];
   __shared__ int fail_j;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+#ifdef STANCL_POTRF_TIMERS
+  long long pt_last_ = clock64();
+#endif
   const double* base = src;
   if (nv < NB) {
     for (int idx = tid; idx < NB * NB; idx += 256) {
@@ -457,13 +516,23 @@ __device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, 
       if (c <= r) S[r * TP + c] = (r < nv) ? base[(long long)r * lds + c] : (r == c ? 1.0 : 0.0);
     }
   } else if ((((uintptr_t)base & 15) == 0) && ((lds & 1) == 0)) {
-#pragma unroll 4
-    for (int idx = tid; idx < NB * NB / 2; idx += 256) {
-      const int r = idx >> 6, c = (idx & 63) << 1;
-      if (c <= r) {
-        const double2 v = *reinterpret_cast<const double2*>(base + (long long)r * lds + c);
-        S[r * TP + c] = v.x;
-        S[r * TP + c + 1] = v.y;
+    // 16 loads in flight per thread (the tile arrives from L2 right after the
+    // lookahead update: latency-bound, not bandwidth-bound)
+#pragma unroll
+    for (int it0 = 0; it0 < NB * NB / 2 / 256; it0 += 16) {
+      double2 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = tid + (it0 + u) * 256, r = idx >> 6, c = (idx & 63) << 1;
+        v[u] = (c <= r) ? *reinterpret_cast<const double2*>(base + (long long)r * lds + c) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const int idx = tid + (it0 + u) * 256, r = idx >> 6, c = (idx & 63) << 1;
+        if (c <= r) {
+          S[r * TP + c] = v[u].x;
+          S[r * TP + c + 1] = v[u].y;
+        }
       }
     }
   } else {
@@ -474,6 +543,8 @@ __device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, 
   }
   if (tid == 0) fail_j = -1;
   __syncthreads();
+  PT_MARK(0);
+#pragma unroll 1
   for (int c0 = 0; c0 < NB; c0 += 32) {
     // (a) the 32 x 32 diagonal block, warp 0
     if (warp == 0) {
@@ -481,6 +552,7 @@ __device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, 
       if (lane == 0 && bad >= 0) fail_j = c0 + bad;
     }
     __syncthreads();
+    PT_MARK(1);
     const int r0 = c0 + 32, R = NB - r0;
     if (fail_j >= 0 || R == 0) break;
     // (b) rows r0.. of block column c0: X <- X L^-T, ascending j
@@ -499,40 +571,13 @@ __device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, 
       for (int c = 0; c < 32; ++c) Sx[c] = x[c];
     }
     __syncthreads();
-    // (c) trailing lower part: S[i][k] -= sum_j X[i][j] X[k][j], r0 <= k <= i
-    {
-      const int ti = tid >> 4, tj = tid & 15;
-      double acc[6][6];
-#pragma unroll
-      for (int a = 0; a < 6; ++a)
-#pragma unroll
-        for (int b = 0; b < 6; ++b) {
-          const int i = ti + 16 * a, k = tj + 16 * b;
-          acc[a][b] = (i < R && k <= i) ? S[(r0 + i) * TP + r0 + k] : 0.0;
-        }
-#pragma unroll 4
-      for (int j = 0; j < 32; ++j) {
-        double xi[6], xk[6];
-#pragma unroll
-        for (int a = 0; a < 6; ++a) {
-          xi[a] = (16 * a < R) ? S[(r0 + ti + 16 * a) * TP + c0 + j] : 0.0;
-          xk[a] = (16 * a < R) ? S[(r0 + tj + 16 * a) * TP + c0 + j] : 0.0;
-        }
-#pragma unroll
-        for (int a = 0; a < 6; ++a)
-#pragma unroll
-          for (int b = 0; b <= a; ++b)
-            if (16 * a < R) acc[a][b] = fma(-xi[a], xk[b], acc[a][b]);
-      }
-#pragma unroll
-      for (int a = 0; a < 6; ++a)
-#pragma unroll
-        for (int b = 0; b <= a; ++b) {
-          const int i = ti + 16 * a, k = tj + 16 * b;
-          if (i < R && k <= i) S[(r0 + i) * TP + r0 + k] = acc[a][b];
-        }
-    }
+    PT_MARK(2);
+    // (c) trailing lower part (static extent per block)
+    if (c0 == 0) potrf_syrk_block<0>(S, tid);
+    else if (c0 == 32) potrf_syrk_block<32>(S, tid);
+    else potrf_syrk_block<64>(S, tid);
     __syncthreads();
+    PT_MARK(3);
   }
   if (nv < NB) {
     for (int idx = tid; idx < nv * nv; idx += 256) {
@@ -552,6 +597,7 @@ __device__ __forceinline__ void potrf_tile_body(const double* src, int64_t lds, 
       dst[(long long)r * ldd + c] = (c <= r) ? S[r * TP + c] : 0.0;
     }
   }
+  PT_MARK(4);
   if (tid == 0 && fail_j >= 0) atomicCAS(status, 0, (int)(info_base + fail_j + 1));
 }
 

@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cmath>
 #include <vector>
+#define STANCL_POTRF_TIMERS 1
+namespace stancl { __device__ long long g_ptimer[8]; }
 #include "../paper_1907_01063_b200/csrc/kernels.cu"
 using namespace stancl;
 
@@ -314,6 +316,14 @@ int main() {
     if (v) for (int i = 0; i < n * n; ++i) ndiff += a[i] != b[i];
     printf("%-34s %8.2f us/launch  differ from v0: %lld  err %s\n", names[v], (ms - tc) * 1000.0 / R, ndiff,
            cudaGetErrorString(cudaGetLastError()));
+    if (v == 7) {
+      long long pt[8] = {0};
+      cudaMemcpyToSymbol(g_ptimer, pt, sizeof(pt));
+      cudaMemset(status, 0, 4);
+      restore<<<16, 256>>>(work, orig, n * n); run(7); cudaDeviceSynchronize();
+      cudaMemcpyFromSymbol(pt, g_ptimer, sizeof(pt));
+      printf("   production phases (cycles): load %lld  warp-diag %lld  trsm %lld  syrk %lld  store %lld\n", pt[0], pt[1], pt[2], pt[3], pt[4]);
+    }
     if (v == 2 || v == 4 || v == 6) {
       cudaMemcpyFromSymbol(ph, g_phase, sizeof(ph));
       printf("   phases (cycles): load %lld  warp-diag %lld  trsm %lld  syrk %lld  store %lld\n", ph[0], ph[1], ph[2], ph[3], ph[4]);
