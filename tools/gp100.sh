@@ -1,0 +1,4 @@
+# fused 128-wide TRSM: parity, timing vs the split form
+timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
+STAN_CL_TRSM_SPLIT=1 timeout 300 python tools/quick_time.py 1024 4096 8192 16384
+timeout 300 python tools/quick_time.py 1024 4096 8192 16384
