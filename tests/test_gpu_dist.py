@@ -213,6 +213,50 @@ def _nccl_worker(rank, world, port, n, q):
         dist.destroy_process_group()
 
 
+def _nccl_single_worker(port, n, q):
+    """world_size 1: the real NCCL path (dlopen, ncclCommInitRank, two ncclCommSplit,
+    the status all-reduce, finalize) on one device, forward + adjoint."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+    import paper_1907_01063_b200 as sc
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        grid = sc.dist_init_from_torch()
+        K = torch.from_numpy(se(n)).cuda()
+        loc = sc.dist_scatter2(K, 1, 1, 0, 0).contiguous()
+        rc = sc.dist_cholesky(loc, n)
+        L = loc.cpu().numpy()
+        W = torch.from_numpy(inputs.lbar(n)).cuda().contiguous()
+        rca = sc.dist_cholesky_adjoint(loc, W, n)
+        A = sc.load().stan_cl_dist_init(1, 0, None, 1, 1)        # already initialised / bad id
+        q.put((grid, rc, rca, L, W.cpu().numpy(), A))
+    except Exception as e:  # noqa: BLE001
+        q.put(("error", repr(e)))
+    finally:
+        sc.load().stan_cl_dist_finalize()
+        dist.destroy_process_group()
+
+
+def test_nccl_single_rank(sc):
+    import torch.multiprocessing as mp
+    n = 768
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_single_worker, args=(_free_port(), n, q))
+    p.start()
+    res = q.get(timeout=300)
+    p.join(timeout=60)
+    assert res[0] != "error", res
+    grid, rc, rca, L, Ab, again = res
+    assert grid == (1, 1) and rc == 0 and rca == 0 and again == -1
+    K = se(n)
+    check_lower_and_tiles(L, oracle.cholesky(K), 1e-11)
+    check_lower_and_tiles(Ab, oracle.cholesky_adjoint(L, inputs.lbar(n)), 1e-9)
+
+
 @pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
 def test_nccl_ranks(sc):
     import torch.multiprocessing as mp
