@@ -1098,6 +1098,7 @@ struct Grid {
 struct DistPlan {
   size_t pan, cbuf, stage, dinv, dbuf, lrow, part, z, sbuf, tmp, total;
   size_t pan_sz = 0, cbuf_sz = 0, stage_sz = 0;  // forward: two sets (lookahead double buffering)
+  size_t lrow_sz = 0;                             // adjoint: pan and lrow doubled likewise
 };
 DistPlan dist_plan(const Grid& gr, int p, int q, bool adjoint) {
   DistPlan d{};
@@ -1118,10 +1119,12 @@ DistPlan dist_plan(const Grid& gr, int p, int q, bool adjoint) {
     d.cbuf = take(2 * d.cbuf_sz);
     d.stage = take(2 * d.stage_sz);
   } else {
-    d.pan = take((R + 1) * t2);  // C_bar D^-1 rows
+    d.pan_sz = a32((R + 1) * t2);  // C_bar D^-1 rows (two sets: the side stream still reads step jb+1's)
+    d.lrow_sz = a32(gr.P > 1 ? C * t2 : 0);
+    d.pan = take(2 * d.pan_sz);
     d.dinv = take(C * t2);
     d.dbuf = take(t2);
-    d.lrow = take(gr.P > 1 ? C * t2 : 0);
+    d.lrow = take(2 * d.lrow_sz);
     size_t part = 0;
     for (int64_t jb = gr.T - 1; jb >= 0; --jb) {
       const int64_t mloc = (R - below(jb + 1, gr.P, p)) * DB, w2 = below(jb + 1, gr.Q, q) * DB;
@@ -1152,6 +1155,7 @@ struct Rank {
   double* pan(int b) const { return base + pl.pan + b * pl.pan_sz; }
   double* cbuf(int b) const { return base + pl.cbuf + b * pl.cbuf_sz; }
   double* stage(int b) const { return base + pl.stage + b * pl.stage_sz; }
+  double* lrow(int b) const { return base + pl.lrow + b * pl.lrow_sz; }
 };
 
 struct Comm {
@@ -1338,10 +1342,49 @@ int dist_factor(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
   return STAN_CL_OK;
 }
 
+// B_bar -= C_bar R on the local tiles I > jb with global block column J in
+// [Jlo, Jhi) (C_bar D^-1 rows in pan(b); R = L's row block jb: local for P = 1,
+// else the broadcast copy lrow(b))
+int dist_r3(std::vector<Rank>& rs, const Grid& gr, int64_t jb, int b, int64_t Jlo, int64_t Jhi, cudaStream_t st,
+            int reserve) {
+  const int P = gr.P, Q = gr.Q;
+  for (auto& r : rs) {
+    const int64_t li0 = below(jb + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB;
+    const int64_t lj0 = below(std::max<int64_t>(Jlo, 0), Q, r.q), lj1 = below(std::min(Jhi, jb), Q, r.q);
+    if (mloc == 0 || lj1 <= lj0) continue;
+    const int64_t w = below(jb, Q, r.q) * DB;  // width of the R row block held / broadcast
+    const double* Rr = P > 1 ? r.lrow(b) : r.L + jb * DB * r.ld;
+    const int64_t ldr = P > 1 ? w : r.ld;
+    CK(gemm_full(true, false, (int)mloc, (int)((lj1 - lj0) * DB), (int)DB, -1.0, 1, r.pan(b), DB, Rr + lj0 * DB, ldr,
+                 r.W + li0 * DB * r.ld + lj0 * DB, r.ld, r.status, st, 0, PROF_GEMM, true, reserve));
+  }
+  return STAN_CL_OK;
+}
+
+// Reverse sweep over 256-wide blocks with lookahead: the
+// bulk of each step's B_bar update (the largest GEMM) runs on the side stream
+// while the main stream goes on with the latency-bound chain (split-K product
+// and its column reduce, the symbolic diagonal step, sym(S) broadcast, R_bar
+// update, the next step's D^-1 / C_bar D^-1 broadcasts).  Per step jb (buffer
+// set b = jb & 1):
+//   main: [wait side done with set b (step jb+2)] D^-1 bcast; C_bar D^-1 -> pan(b);
+//         row bcast; L row bcast -> lrow(b); [wait side's column jb-1 update of
+//         step jb+1] B_bar(:, jb-1) -= ...; event A
+//   side: wait A; B_bar(:, jb-2) -= ... ; event P1; B_bar(:, < jb-2) -= ...; event R(b)
+//   main: split-K partials, column reduce, symbolic step, sym(S) bcast, R_bar update
+// The column the next step's C_bar needs (jb-1) is updated on the main stream,
+// the one after it (jb-2) first on the side stream, so no two updates of the same
+// tiles are ever in flight together.
 int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
   cudaStream_t st = g.stream;
   const int64_t T = gr.T, t2 = DB * DB;
   const int P = gr.P, Q = gr.Q;
+  RC(ensure_side(8));
+  cudaStream_t side = g.side;
+  cudaEvent_t* ev = g.events.data();  // 0: start; 1, 2: side done with set 0 / 1; 3: column jb-2 done; 4: main ready
+  constexpr int kReserve = 16;        // SMs the side-stream bulk update leaves to the main-stream chain / NCCL
+  for (int i = 0; i < 4; ++i) CK(cudaEventRecord(ev[i], st));
+  CK(cudaStreamWaitEvent(side, ev[0], 0));
   auto ltile = [&](const Rank& r, const double* M, int64_t I, int64_t J) {  // local tile (I, J) of M
     return M + (I / P) * DB * r.ld + (J / Q) * DB;
   };
@@ -1355,8 +1398,10 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
     }
   for (int64_t jb = T - 1; jb >= 0; --jb) {
     const int pj = (int)(jb % P), qj = (int)(jb % Q);
+    const int b = (int)(jb & 1);
     auto dinv_of = [&](Rank& r) { return r.p == pj ? r.at(r.pl.dinv) + (jb / Q) * t2 : r.at(r.pl.dbuf); };
     if (jb < T - 1) {
+      CK(cudaStreamWaitEvent(st, ev[1 + b], 0));  // the side stream is done with pan(b) / lrow(b) of step jb+2
       // R1: C_bar <- C_bar D^-1 on process column qj (D^-1 broadcast down it)
       RC(cm.bcast(rs, false, qj, pj, dinv_of, (size_t)t2, st));
       for (auto& r : rs) {
@@ -1364,13 +1409,13 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
         const int64_t li0 = below(jb + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB;
         if (mloc == 0) continue;
         double* Cb = r.W + li0 * DB * r.ld + (jb / Q) * DB;
-        CK(gemm_full(true, false, (int)mloc, (int)DB, (int)DB, 1.0, 0, Cb, r.ld, dinv_of(r), DB, r.at(r.pl.pan), DB,
+        CK(gemm_full(true, false, (int)mloc, (int)DB, (int)DB, 1.0, 0, Cb, r.ld, dinv_of(r), DB, r.pan(b), DB,
                      r.status, st, 0, PROF_TRMM));
-        CK(copy_block(r.at(r.pl.pan), DB, Cb, r.ld, mloc, DB, st));
+        CK(copy_block(r.pan(b), DB, Cb, r.ld, mloc, DB, st));
       }
       for (int p = 0; p < P; ++p) {
         const int64_t mloc = (gr.R(p) - below(jb + 1, P, p)) * DB;
-        RC(cm.bcast(rs, true, p, qj, [](Rank& r) { return r.at(r.pl.pan); }, (size_t)mloc * DB, st));
+        RC(cm.bcast(rs, true, p, qj, [b](Rank& r) { return r.pan(b); }, (size_t)mloc * DB, st));
       }
       // L's row block jb (columns J < jb) down every process column (P > 1)
       if (P > 1) {
@@ -1378,20 +1423,20 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
           const int64_t w = below(jb, Q, q) * DB;
           if (w == 0) continue;
           for (auto& r : rs)
-            if (r.p == pj && r.q == q)
-              CK(copy_block(r.L + (jb / P) * DB * r.ld, r.ld, r.at(r.pl.lrow), w, DB, w, st));
-          RC(cm.bcast(rs, false, q, pj, [](Rank& r) { return r.at(r.pl.lrow); }, (size_t)DB * w, st));
+            if (r.p == pj && r.q == q) CK(copy_block(r.L + (jb / P) * DB * r.ld, r.ld, r.lrow(b), w, DB, w, st));
+          RC(cm.bcast(rs, false, q, pj, [b](Rank& r) { return r.lrow(b); }, (size_t)DB * w, st));
         }
       }
-      // R3: B_bar -= C_bar R on the local tiles I > jb > J
-      for (auto& r : rs) {
-        const int64_t li0 = below(jb + 1, P, r.p), mloc = (gr.R(r.p) - li0) * DB, w = below(jb, Q, r.q) * DB;
-        if (mloc == 0 || w == 0) continue;
-        const double* Rr = P > 1 ? r.at(r.pl.lrow) : r.L + jb * DB * r.ld;
-        const int64_t ldr = P > 1 ? w : r.ld;
-        CK(gemm_full(true, false, (int)mloc, (int)w, (int)DB, -1.0, 1, r.at(r.pl.pan), DB, Rr, ldr,
-                     r.W + li0 * DB * r.ld, r.ld, r.status, st));
-      }
+      // R3 on column jb-1 here (the next step's C_bar), after the side stream's
+      // update of that column from step jb+1; the rest on the side stream
+      CK(cudaStreamWaitEvent(st, ev[3], 0));
+      RC(dist_r3(rs, gr, jb, b, jb - 1, jb, st, 0));
+      CK(cudaEventRecord(ev[4], st));
+      CK(cudaStreamWaitEvent(side, ev[4], 0));
+      RC(dist_r3(rs, gr, jb, b, jb - 2, jb - 1, side, 0));
+      CK(cudaEventRecord(ev[3], side));
+      RC(dist_r3(rs, gr, jb, b, 0, jb - 2, side, kReserve));
+      CK(cudaEventRecord(ev[1 + b], side));
       // R2: [R_bar D_bar] -= C_bar^T [B C]: local split-K partials over the rows
       //     I > jb, reduced down each process column to the owner of row block jb
       //     (large-k product PAPER.md:172-174)
@@ -1404,7 +1449,7 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
         if (mloc == 0) continue;
         int splits, kps;
         splitk_choice(mloc, w2, DB, &splits, &kps);
-        CK(gemm_splitk_tn((int)DB, (int)w2, (int)mloc, splits, kps, r.at(r.pl.pan), DB, r.L + li0 * DB * r.ld, r.ld,
+        CK(gemm_splitk_tn((int)DB, (int)w2, (int)mloc, splits, kps, r.pan(b), DB, r.L + li0 * DB * r.ld, r.ld,
                           r.at(r.pl.part), r.status, st));
         CK(splitk_reduce_sub(r.at(r.pl.part), splits, (int)DB, (int)w2, dst, ldd, r.status, st));
       }
@@ -1439,6 +1484,9 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
                    r.ld, r.W + (jb / P) * DB * r.ld, r.ld, r.status, st));
     }
   }
+  // join: the last side-stream updates
+  CK(cudaStreamWaitEvent(st, ev[1], 0));
+  CK(cudaStreamWaitEvent(st, ev[2], 0));
   return STAN_CL_OK;
 }
 
