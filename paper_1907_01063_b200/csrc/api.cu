@@ -1113,7 +1113,7 @@ DistPlan dist_plan(const Grid& gr, int p, int q, bool adjoint) {
   auto a32 = [](size_t c) { return (c + 31) / 32 * 32; };
   if (!adjoint) {  // two buffer sets: panel k+1 is formed while panel k is consumed
     d.pan_sz = a32((R + 1) * t2);  // [L_kk | panel rows]
-    d.cbuf_sz = a32(gr.P > 1 ? C * t2 : 0);
+    d.cbuf_sz = a32(C * t2);  // L_Jk of every local block column (one GEMM per step)
     d.stage_sz = a32(gr.P > 1 ? (size_t)gr.P * (C + 1) * t2 : 0);
     d.pan = take(2 * d.pan_sz);
     d.cbuf = take(2 * d.cbuf_sz);
@@ -1251,6 +1251,19 @@ int dist_panel(std::vector<Rank>& rs, const Grid& gr, Comm& cm, int64_t k, int b
     const int64_t mloc = (gr.R(p) - below(k + 1, P, p)) * DB;
     RC(cm.bcast(rs, true, p, qk, [b](Rank& r) { return r.pan(b) + DB * DB; }, (size_t)mloc * DB, st));
   }
+  // (d0) own tiles: L_Jk with J % P == p, J % Q == q, J > k from the panel rows into
+  //      the column buffer (slot J / Q), so the trailing update is one GEMM per step
+  for (auto& r : rs) {
+    int64_t J0 = -1;
+    for (int64_t J = k + 1; J < std::min(T, k + 1 + Lc); ++J)
+      if (J % P == r.p && J % Q == r.q) {
+        J0 = J;
+        break;
+      }
+    if (J0 < 0) continue;
+    const int64_t cnt = (T - 1 - J0) / Lc + 1, li0 = below(k + 1, P, r.p);
+    CK(copy_tiles(r.pan(b) + t2, J0 / P - li0, Lc / P, r.cbuf(b), J0 / Q, Lc / Q, cnt, t2, st));
+  }
   // (d) column exchange (P > 1): rank (p', q) sends the tiles L_Jk, J > k,
   //     J % P == p', J % Q == q (J = J0 + t * lcm(P, Q)) to its process column
   if (P > 1) {
@@ -1282,22 +1295,21 @@ int dist_panel(std::vector<Rank>& rs, const Grid& gr, Comm& cm, int64_t k, int b
 }
 
 // forward phase (e) of step k (buffer set b): A_IJ -= L_Ik L_Jk^T on the local
-// lower tiles I >= J with J in [Jlo, Jhi)
+// lower tiles I >= J with J in [Jlo, Jhi): one block-cyclic-masked GEMM per rank
+// (rows from the first local block row that reaches the first column's diagonal)
 int dist_update(std::vector<Rank>& rs, const Grid& gr, int64_t k, int b, int64_t Jlo, int64_t Jhi, cudaStream_t st,
                 int reserve) {
   const int64_t t2 = DB * DB;
   const int P = gr.P, Q = gr.Q;
   for (auto& r : rs) {
     const int64_t li0 = below(k + 1, P, r.p), R = gr.R(r.p);
-    const double* pan = r.pan(b) + t2;
-    for (int64_t lj = below(Jlo, Q, r.q); lj < below(Jhi, Q, r.q); ++lj) {
-      const int64_t J = lj * Q + r.q, li_s = below(J, P, r.p);
-      if (li_s >= R) continue;
-      const double* Ljk = (J % P == r.p) ? pan + (J / P - li0) * t2 : r.cbuf(b) + lj * t2;
-      CK(gemm_full(true, true, (int)((R - li_s) * DB), (int)DB, (int)DB, -1.0, 1, pan + (li_s - li0) * t2, DB,
-                   Ljk, DB, r.W + li_s * DB * r.ld + lj * DB, r.ld, r.status, st,
-                   /*lower_only=*/(li_s * P + r.p == J) ? 1 : 0, PROF_SYRK, true, reserve));
-    }
+    const int64_t lj_lo = below(Jlo, Q, r.q), lj_hi = below(Jhi, Q, r.q);
+    if (lj_hi <= lj_lo) continue;
+    const int64_t li_f = below(lj_lo * Q + r.q, P, r.p);  // first local block row with I >= J of column lj_lo
+    if (li_f >= R) continue;
+    CK(gemm_cyclic_lower((int)((R - li_f) * DB), (int)((lj_hi - lj_lo) * DB), (int)DB, r.pan(b) + t2 + (li_f - li0) * t2,
+                         DB, r.cbuf(b) + lj_lo * t2, DB, r.W + li_f * DB * r.ld + lj_lo * DB, r.ld, P, r.p, Q, r.q,
+                         (int)li_f, (int)lj_lo, r.status, st, reserve));
   }
   return STAN_CL_OK;
 }

@@ -47,6 +47,12 @@ struct GemmArgs {
   int lower_only;   // MODE_FULL: mask stores to r >= c
   const int* status;  // optional: skip work if *status != 0
   int pingpong;     // serialise the MMA main loops of co-resident CTAs (per-SM token)
+  // TMA kernel, MODE_FULL, BM = 128, BN = 64: block-cyclic lower mask (the
+  // distributed forward's trailing update, rank (cy_p, cy_q) of a cy_P x cy_Q grid).
+  // C is a rectangle of 256 x 256 blocks whose local block (i, j) is global tile
+  // (I, J) = ((cy_li + i) cy_P + cy_p, (cy_lj + j) cy_Q + cy_q): tiles with I < J are
+  // skipped (no loads, no stores), I == J blocks keep their lower part only.
+  int cyc = 0, cy_P = 1, cy_p = 0, cy_Q = 1, cy_q = 0, cy_li = 0, cy_lj = 0;
 };
 
 // Per-SM MMA token ("ping-pong" between the CTAs resident on one SM): a CTA

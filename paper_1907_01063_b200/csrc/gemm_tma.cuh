@@ -141,6 +141,33 @@ __device__ __forceinline__ double frag(const double* s, int rc, int k) {
 template <class CF, int MODE>
 struct TItemMap {
   int ntn, ntiles, ktiles_full;
+  // block-cyclic lower mask (GemmArgs::cyc): is the item computed, and the
+  // diagonal offset d of its block (elements kept iff r >= c + d) if masked
+  __device__ __forceinline__ bool valid(const GemmArgs& p, int item, bool& masked, int& d) const {
+    masked = false;
+    d = 0;
+    if constexpr (MODE != MODE_FULL) {
+      return true;
+    } else {
+      if (!p.cyc) return true;
+      const int tm = item / ntn, tn = item - (item / ntn) * ntn;
+      const int bi = tm / (256 / CF::BM), bj = tn / (256 / CF::BN);
+      const long long I = (long long)(p.cy_li + bi) * p.cy_P + p.cy_p, J = (long long)(p.cy_lj + bj) * p.cy_Q + p.cy_q;
+      if (I < J) return false;
+      if (I > J) return true;
+      d = (bi - bj) * 256;
+      const int rr0 = (tm % (256 / CF::BM)) * CF::BM, cc0 = (tn % (256 / CF::BN)) * CF::BN;
+      if (rr0 + CF::BM - 1 < cc0) return false;  // wholly above the block diagonal
+      masked = true;
+      return true;
+    }
+  }
+  __device__ __forceinline__ int next_valid(const GemmArgs& p, int item, int stride, int nitems) const {
+    bool m;
+    int d;
+    while (item < nitems && !valid(p, item, m, d)) item += stride;
+    return item;
+  }
   __device__ __forceinline__ void get(const GemmArgs& p, int item, int& m0, int& n0, int& kbeg, int& ns,
                                       int& z) const {
     int tm, tn, tile = item;
@@ -223,7 +250,8 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
       if (B_KMAJ) prefetch_tmap(&tmB);
     }
     int it = 0;
-    for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    for (int item = map.next_valid(p, blockIdx.x, gridDim.x, nitems); item < nitems;
+         item = map.next_valid(p, item + gridDim.x, gridDim.x, nitems)) {
       int m0, n0, kbeg, ns, z;
       map.get(p, item, m0, n0, kbeg, ns, z);
       for (int s = 0; s < ns; ++s, ++it) {
@@ -256,14 +284,17 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
     cp_async_commit();
   };
   int m0, n0, kbeg, ns, z;
-  map.get(p, blockIdx.x, m0, n0, kbeg, ns, z);
+  const int first = map.next_valid(p, blockIdx.x, gridDim.x, nitems);
+  if (first >= nitems) return;
+  map.get(p, first, m0, n0, kbeg, ns, z);
   if (CF::CPREF && need_c) load_c(m0, n0);
   int kap[4];
 #pragma unroll
   for (int s = 0; s < 4; ++s) kap[s] = kappa(s, t);
   int it = 0;
   double acc[MI][NI][2];
-  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+  for (int item = first; item < nitems;) {
+    const int nxt_item = map.next_valid(p, item + gridDim.x, gridDim.x, nitems);
     if (need_c && CF::CPREF) {
       cp_async_wait<0>();
 #pragma unroll
@@ -314,7 +345,7 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
         // prefetch the next item's C into the private slots only now: the DMMAs
         // above consumed acc (loaded from these slots), and asm-volatile order
         // keeps this cp.async behind them, so the refill cannot overtake the read
-        const int nxt = item + gridDim.x;
+        const int nxt = nxt_item;
         if (nxt < nitems) {
           int m1, n1, kb1, ns1, z1;
           map.get(p, nxt, m1, n1, kb1, ns1, z1);
@@ -332,8 +363,11 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
       Cout = p.C;
       ldo = p.ldc;
     }
-    const bool mask = (MODE == MODE_LOWER) || (MODE == MODE_FULL && p.lower_only);
-    const bool crosses = mask && (n0 + BN - 1 > m0);
+    bool cmask;
+    int dd;
+    map.valid(p, item, cmask, dd);  // block-cyclic diagonal block: keep r >= c + dd
+    const bool mask = (MODE == MODE_LOWER) || (MODE == MODE_FULL && (p.lower_only || cmask));
+    const bool crosses = mask && (n0 + BN - 1 + dd > m0);
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
@@ -342,14 +376,14 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
         double* dst = Cout + (long long)r * ldo + c;
         const double v0 = xor_sign(acc[i][j][0], smask), v1 = xor_sign(acc[i][j][1], smask);
         if (crosses) {
-          if (r >= c) dst[0] = v0;
-          if (r >= c + 1) dst[1] = v1;
+          if (r >= c + dd) dst[0] = v0;
+          if (r >= c + 1 + dd) dst[1] = v1;
         } else {
           *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
         }
       }
-    const int nxt = item + gridDim.x;
-    if (nxt < nitems) map.get(p, nxt, m0, n0, kbeg, ns, z);
+    if (nxt_item < nitems) map.get(p, nxt_item, m0, n0, kbeg, ns, z);
+    item = nxt_item;
   }
 }
 

@@ -946,6 +946,24 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
   }
 }
 
+cudaError_t gemm_cyclic_lower(int M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                              double* C, int64_t ldc, int P, int p, int Q, int q, int li0, int lj0, const int* status,
+                              cudaStream_t st, int reserve_sms) {
+  if (M == 0 || N == 0) return cudaSuccess;
+  if (M % 256 || N % 256) return cudaErrorInvalidValue;
+  // algorithmic work: the lower tiles only (about half the rectangle on a square grid)
+  Prof prof_(PROF_SYRK, 2.0 * M * N * K, st, 16.0 * M * N + 8.0 * ((double)M * K + (double)N * K));
+  GemmArgs g{A, lda, B, ldb, C, ldc, M, N, K, K, -1.0, 1, 0, status, cfgsel().pingpong};
+  g.cyc = 1;
+  g.cy_P = P;
+  g.cy_p = p;
+  g.cy_Q = Q;
+  g.cy_q = q;
+  g.cy_li = li0;
+  g.cy_lj = lj0;
+  return launch_tma<tg::CfgT32, true, true, MODE_FULL>(g, 1, st, reserve_sms);
+}
+
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                           double* C, int64_t ldc, const int* status, cudaStream_t st) {
   if (M == 0) return cudaSuccess;

@@ -99,6 +99,13 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st, int lower_only = 0,
                       int prof_kind = 1, bool allow_persistent = true, int reserve_sms = 0);
+// C[M x N] -= A B^T (A M x K, B N x K, both k-major) on the block-cyclic lower
+// tiles of rank (p, q) of a P x Q grid: C's 256 x 256 block (i, j) is global tile
+// ((li0 + i) P + p, (lj0 + j) Q + q); blocks above the diagonal are skipped and
+// diagonal blocks keep their lower part (the distributed trailing update)
+cudaError_t gemm_cyclic_lower(int M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
+                              double* C, int64_t ldc, int P, int p, int Q, int q, int li0, int lj0, const int* status,
+                              cudaStream_t st, int reserve_sms = 0);
 // lower tiles of square C[M x M] -= A A'^T style: C -= A B^T, A, B both k-major (SYRK)
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                           double* C, int64_t ldc, const int* status, cudaStream_t st);
