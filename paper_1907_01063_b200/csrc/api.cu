@@ -358,21 +358,24 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
 // inverses by substitution (tri_inverse_batched); for B = 256 the off-diagonal
 // block of [[D11, 0], [D21, D22]]^-1 is -D22^-1 D21 D11^-1 (two batched 128^3
 // products).  Blocks [b0, b0 + nb) of size B; Dinv holds N/B blocks of B x B.
+// tile_stride (optional): element distance between consecutive blocks (default
+// the next diagonal block, B ld + B; the distributed adjoint passes the stride
+// between a rank's owned diagonal tiles), results contiguous from Dinv + b0 B^2.
 int block_inverses(const double* Lw, int64_t ld, int64_t B, int64_t b0, int64_t nb, double* Dinv, double* scratch,
-                   int* status, cudaStream_t st) {
+                   int* status, cudaStream_t st, int64_t tile_stride = 0) {
   const double* Lb = Lw + b0 * B * ld + b0 * B;
   double* Db = Dinv + b0 * B * B;
   if (B == NB) {
-    CK(tri_inverse_batched(Lb, ld, (int)nb, Db, status, st));
+    CK(tri_inverse_batched(Lb, ld, (int)nb, Db, status, st, 0, 0, 1, tile_stride));
     return STAN_CL_OK;
   }
   // B = 256: the 2*nb diagonal 128-inverses straight into the 256 layout, then
   // T = D21 X11 and X21 = -X22 T, both batched over the nb blocks
   CK(cudaMemsetAsync(Db, 0, (size_t)nb * B * B * sizeof(double), st));
-  CK(tri_inverse_batched(Lb, ld, (int)(2 * nb), Db, status, st, B, B * B, 2));
+  CK(tri_inverse_batched(Lb, ld, (int)(2 * nb), Db, status, st, B, B * B, 2, tile_stride));
   const double* D21 = Lb + NB * ld;  // rows 128.., cols 0..128 of the first block
   CK(gemm_small(NB, false, false, false, D21, ld, Db, B, scratch, NB, status, st, 1.0, (int)nb,
-                B * ld + B, B * B, (int64_t)NB * NB));
+                tile_stride ? tile_stride : B * ld + B, B * B, (int64_t)NB * NB));
   CK(gemm_small(NB, false, false, false, Db + NB * B + NB, B, scratch, NB, Db + NB * B, B, status, st, -1.0,
                 (int)nb, B * B, (int64_t)NB * NB, B * B));
   return STAN_CL_OK;
@@ -1136,7 +1139,7 @@ DistPlan dist_plan(const Grid& gr, int p, int q, bool adjoint) {
     d.part = take(part);
     d.z = take(gr.P > 1 ? C * t2 : 0);
     d.sbuf = take(t2);
-    d.tmp = take(4 * t2);
+    d.tmp = take(std::max<size_t>(4 * t2, (size_t)C * NB * NB));  // also the batched D^-1 scratch (NB^2 per tile)
   }
   d.total = o;
   return d;
@@ -1392,26 +1395,41 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
   const int64_t T = gr.T, t2 = DB * DB;
   const int P = gr.P, Q = gr.Q;
   RC(ensure_side(8));
-  cudaStream_t side = g.side;
+  // one rank: no collectives to hide, and the two streams' persistent GEMMs only
+  // compete for SMs (measured 108 vs 95 ms at n = 16384 on a 1 x 1 grid), so the
+  // bulk update then stays in stream order
+  const bool overlap = P * Q > 1;
+  cudaStream_t side = overlap ? g.side : st;
   cudaEvent_t* ev = g.events.data();  // 0: start; 1, 2: side done with set 0 / 1; 3: column jb-2 done; 4: main ready
-  constexpr int kReserve = 16;        // SMs the side-stream bulk update leaves to the main-stream chain / NCCL
+  const int kReserve = overlap ? 16 : 0;  // SMs the side-stream bulk update leaves to the main-stream chain / NCCL
   for (int i = 0; i < 4; ++i) CK(cudaEventRecord(ev[i], st));
   CK(cudaStreamWaitEvent(side, ev[0], 0));
   auto ltile = [&](const Rank& r, const double* M, int64_t I, int64_t J) {  // local tile (I, J) of M
     return M + (I / P) * DB * r.ld + (J / Q) * DB;
   };
-  // D^-1 of the owned diagonal tiles (slot J / Q); they depend only on L
-  for (auto& r : rs)
-    for (int64_t J = 0; J < T; ++J) {
-      if (J % P != r.p || J % Q != r.q) continue;
-      const double* D = ltile(r, r.L, J, J);
-      double* dst = r.at(r.pl.dinv) + (J / Q) * t2;
-      RC(block_inverses(D - J * DB * r.ld - J * DB, r.ld, DB, J, 1, dst - J * t2, r.at(r.pl.tmp), r.status, st));
-    }
+  // D^-1 of the owned diagonal tiles J = J0 + t lcm(P, Q) (slot t), one batched
+  // call per rank (consecutive owned tiles are a constant local stride apart);
+  // they depend only on L
+  const int64_t Lc = std::lcm((int64_t)P, (int64_t)Q);
+  auto first_diag = [&](const Rank& r) -> int64_t {
+    for (int64_t J = 0; J < std::min(T, Lc); ++J)
+      if (J % P == r.p && J % Q == r.q) return J;
+    return -1;
+  };
+  for (auto& r : rs) {
+    const int64_t J0 = first_diag(r);
+    if (J0 < 0) continue;
+    const int64_t cnt = (T - 1 - J0) / Lc + 1;
+    const int64_t stride = (Lc / P) * DB * r.ld + (Lc / Q) * DB;
+    const double* D = ltile(r, r.L, J0, J0);
+    RC(block_inverses(D, r.ld, DB, 0, cnt, r.at(r.pl.dinv), r.at(r.pl.tmp), r.status, st, stride));
+  }
   for (int64_t jb = T - 1; jb >= 0; --jb) {
     const int pj = (int)(jb % P), qj = (int)(jb % Q);
     const int b = (int)(jb & 1);
-    auto dinv_of = [&](Rank& r) { return r.p == pj ? r.at(r.pl.dinv) + (jb / Q) * t2 : r.at(r.pl.dbuf); };
+    auto dinv_of = [&](Rank& r) {
+      return r.p == pj ? r.at(r.pl.dinv) + ((jb - first_diag(r)) / Lc) * t2 : r.at(r.pl.dbuf);
+    };
     if (jb < T - 1) {
       CK(cudaStreamWaitEvent(st, ev[1 + b], 0));  // the side stream is done with pan(b) / lrow(b) of step jb+2
       // R1: C_bar <- C_bar D^-1 on process column qj (D^-1 broadcast down it)
@@ -1441,14 +1459,18 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
       }
       // R3 on column jb-1 here (the next step's C_bar), after the side stream's
       // update of that column from step jb+1; the rest on the side stream
-      CK(cudaStreamWaitEvent(st, ev[3], 0));
-      RC(dist_r3(rs, gr, jb, b, jb - 1, jb, st, 0));
-      CK(cudaEventRecord(ev[4], st));
-      CK(cudaStreamWaitEvent(side, ev[4], 0));
-      RC(dist_r3(rs, gr, jb, b, jb - 2, jb - 1, side, 0));
-      CK(cudaEventRecord(ev[3], side));
-      RC(dist_r3(rs, gr, jb, b, 0, jb - 2, side, kReserve));
-      CK(cudaEventRecord(ev[1 + b], side));
+      if (overlap) {
+        CK(cudaStreamWaitEvent(st, ev[3], 0));
+        RC(dist_r3(rs, gr, jb, b, jb - 1, jb, st, 0));
+        CK(cudaEventRecord(ev[4], st));
+        CK(cudaStreamWaitEvent(side, ev[4], 0));
+        RC(dist_r3(rs, gr, jb, b, jb - 2, jb - 1, side, 0));
+        CK(cudaEventRecord(ev[3], side));
+        RC(dist_r3(rs, gr, jb, b, 0, jb - 2, side, kReserve));
+        CK(cudaEventRecord(ev[1 + b], side));
+      } else {
+        RC(dist_r3(rs, gr, jb, b, 0, jb, st, 0));  // one launch, in stream order
+      }
       // R2: [R_bar D_bar] -= C_bar^T [B C]: local split-K partials over the rows
       //     I > jb, reduced down each process column to the owner of row block jb
       //     (large-k product PAPER.md:172-174)
@@ -1481,7 +1503,7 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
       if (r.p != pj || r.q != qj) continue;
       const double* D = ltile(r, r.L, jb, jb);
       double* Dbar = r.W + (jb / P) * DB * r.ld + (jb / Q) * DB;
-      const double* Di = r.at(r.pl.dinv) + (jb / Q) * t2;
+      const double* Di = r.at(r.pl.dinv) + ((jb - first_diag(r)) / Lc) * t2;
       double* T1 = r.at(r.pl.tmp);
       CK(adj_diag_fused((int)DB, D, r.ld, Dbar, r.ld, Di, T1, T1 + t2, T1 + 2 * t2, r.at(r.pl.sbuf),
                         (unsigned*)r.status + 16, r.status, st));

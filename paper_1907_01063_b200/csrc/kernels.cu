@@ -1041,8 +1041,10 @@ __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, in
   double* D = sm;               // packed lower: D[i][k] at i(i+1)/2 + k
   double* X = sm + TRI_PACKED;  // X[c][i] = (D^-1)[i][c]  (column c of the inverse, contiguous)
   const int b = blockIdx.x, c = threadIdx.x;
-  // block b: the b-th diagonal block of L, or (istride > 0) the tile at b * istride
-  const double* src = istride > 0 ? L + (long long)b * istride : L + (long long)b * NB * ld + (long long)b * NB;
+  // block b: the b-th diagonal block of L, or (istride > 0) diagonal half b % per
+  // of the tile at (b / per) * istride
+  const double* src = istride > 0 ? L + (long long)(b / per) * istride + (long long)(b % per) * (NB * ld + NB)
+                                  : L + (long long)b * NB * ld + (long long)b * NB;
   for (int idx = c; idx < NB * NB; idx += NB) {
     const int i = idx >> 7, k = idx & (NB - 1);
     if (k <= i) D[i * (i + 1) / 2 + k] = src[(long long)i * ld + k];
