@@ -1331,7 +1331,8 @@ int dist_factor(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
   RC(ensure_side(2 * T + 2));
   cudaStream_t side = g.side;
   cudaEvent_t* ev = g.events.data();  // ev[0]: start; ev[1 + 2k]: panel k done; ev[2 + 2k]: column k+1 updated
-  constexpr int kReserve = 16;        // SMs the bulk update leaves to the panel / NCCL kernels
+  // SMs the bulk update leaves to the panel (and, with several ranks, the NCCL) kernels
+  const int kReserve = gr.P * gr.Q > 1 ? 16 : 8;
   CK(cudaEventRecord(ev[0], main));
   CK(cudaStreamWaitEvent(side, ev[0], 0));
   RC(dist_panel(rs, gr, cm, 0, 0, side));
