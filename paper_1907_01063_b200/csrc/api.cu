@@ -381,17 +381,6 @@ int block_inverses(const double* Lw, int64_t ld, int64_t B, int64_t b0, int64_t 
   return STAN_CL_OK;
 }
 
-// experiment switch STAN_CL_NARROW_W8 (bit 1: R1 C_bar D^-1, bit 2: R5): run the
-// adjoint's narrow K = 256 GEMMs on the one-tile-per-CTA kernel instead of the
-// persistent one
-inline bool narrow_w8(int bit) {
-  static const int m = [] {
-    const char* e = getenv("STAN_CL_NARROW_W8");
-    return e ? atoi(e) : 0;
-  }();
-  return (m & bit) != 0;
-}
-
 // Blocked reverse sweep with block B = plan.B on the working
 // matrix Wm (initially tril(L_bar)) with factor Lw, both N x N with leading
 // dimension ld.
@@ -433,8 +422,7 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
       // C_adj = C_adj * lower_triangular_inverse(D)
       // computed out of place (persistent TMA GEMM) into Ctmp, consumed from there
       // by the two big products, and written back to A_bar afterwards
-      CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, Ctmp, B, status, st, 0, PROF_TRMM,
-                   !narrow_w8(1)));
+      CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, Ctmp, B, status, st, 0, PROF_TRMM));
       // B_adj = B_adj - C_adj * R
       if (j > 0)
         CK(gemm_full(true, false, (int)m, (int)j, (int)B, -1.0, 1, Ctmp, B, R, ld, Wm + k * ld, ld, status, st));
@@ -455,8 +443,7 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
     CK(adj_diag_fused((int)B, D, ld, Dbar, ld, Db, T1, T2, T3, T4, (unsigned*)status + 16, status, st));
     // R_adj = R_adj - D_adj * R
     if (j > 0)
-      CK(gemm_full(true, false, (int)B, (int)j, (int)B, -1.0, 1, T4, B, R, ld, Wm + j * ld, ld, status, st, 0,
-                   PROF_GEMM, !narrow_w8(2)));
+      CK(gemm_full(true, false, (int)B, (int)j, (int)B, -1.0, 1, T4, B, R, ld, Wm + j * ld, ld, status, st));
     if (out) {  // column block j is final: ship rows j.. of it
       CK(cudaEventRecord(col_done[j / B], st));
       CK(cudaStreamWaitEvent(g.d2h, col_done[j / B], 0));
