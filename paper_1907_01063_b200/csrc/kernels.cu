@@ -798,14 +798,26 @@ __global__ void __launch_bounds__(256, 2) trsm_panel_kernel(double* W, int64_t l
   __shared__ double dg[TRSM_W], rdg[TRSM_W];  // L_jj and RN(1 / L_jj)
   const int tid = threadIdx.x, lane = tid & 31;
   const double* L11 = W + k0 * ld + k0;
-  for (int idx = tid; idx < TRSM_W * TRSM_W; idx += 256) {
-    const int l = idx / TRSM_W, j = idx % TRSM_W;
-    if (j <= l) {
-      const double v = L11[(long long)l * ld + j];
-      LT[j * TRSM_TP + l] = v;
-      if (j == l) {
-        dg[j] = v;
-        rdg[j] = rcp_pos(v);
+  {
+    // all 16 loads in flight before any use (a rolled loop serialised their L2
+    // latency); the upper-triangle values read here are inside the matrix and
+    // simply not stored
+    constexpr int PER = TRSM_W * TRSM_W / 256;
+    double v[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = tid + u * 256, l = idx / TRSM_W, j = idx % TRSM_W;
+      v[u] = L11[(long long)l * ld + j];
+    }
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int idx = tid + u * 256, l = idx / TRSM_W, j = idx % TRSM_W;
+      if (j <= l) {
+        LT[j * TRSM_TP + l] = v[u];
+        if (j == l) {
+          dg[j] = v[u];
+          rdg[j] = rcp_pos(v[u]);
+        }
       }
     }
   }
