@@ -48,7 +48,8 @@ def config(n: int, world: int, mode: str = "single", grid: tuple = (1, 1)) -> di
     return {
         "workload": f"SE-kernel GP covariance n={n} (1-D x~U(-10,10), alpha=rho=1, jitter 1e-6): "
                     "SE build + Cholesky + adjoint (BASELINE.json configs[3])",
-        "n": n, "nb": ("forward: 256-wide outer blocks of 128-wide tiles (two-level); adjoint: "
+        "n": n, "nb": (("forward: 256-wide outer blocks of 128-wide tiles (two-level); adjoint: " if n >= 6144
+                        else "forward: 128-wide blocks; adjoint: ")
                        + ("256" if n >= 4096 else "128") + "-wide blocks"),
         "flops_per_step": n ** 3,
         "flop_convention": "n^3/3 (Cholesky) + 2n^3/3 (adjoint)",

@@ -242,6 +242,16 @@ int copy_rect_d2h(const HostOut& o, const double* W, int64_t ld, int64_t r0, int
   return STAN_CL_OK;
 }
 
+// forward outer block (stan_cl_set_block_size(0) = auto): 256 (two-level: the
+// trailing update runs with K = 256) from n = 6144 on, when it divides n or n is
+// padded anyway; 128 below, where the panel chain dominates and a 128-wide step
+// is shorter (measured: n = 4096 2.85 vs 2.96 ms, 2048 1.28 vs 1.33 ms; 8192
+// 9.35 ms with 256 vs 9.79 ms with 128; tools/nb_sweep.py)
+int64_t fwd_outer_block(int64_t n) {
+  if (n >= 6144) return (n % (2 * NB) == 0 || n % NB != 0) ? 2 * NB : NB;
+  return NB;
+}
+
 // The factored panel of outer block [c0, c0+OB): L11 = chol(A11) and
 // L21 = A21 L11^-T.  OB = 128: one POTRF tile + one TRSM.
 // OB = 256 (two-level blocking): two 128 sub-steps with the second half of the
@@ -330,7 +340,7 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
   CK(cudaMemsetAsync(status, 0, sizeof(int), st));
   // outer block: 256 (two-level) when it divides n, else 128 (set_block_size overrides)
   int64_t OB = g.nb;
-  if (!OB) OB = (n % (2 * NB) == 0) ? 2 * NB : (n % NB == 0) ? NB : (n > 1024 ? 2 * NB : NB);
+  if (!OB) OB = fwd_outer_block(n);
   const int64_t N = round_up(n, OB);
   const bool fast = (N == n) && aligned16(A) && aligned16(L);
   if (fast) {
@@ -804,7 +814,7 @@ int stan_cl_gp_exp_quad_cov(int64_t n, const double* x, double alpha, double rho
 // final.
 int cholesky_host_enqueue(int64_t n, const double* A, double* L) {
   int64_t OB = g.nb;
-  if (!OB) OB = (n % (2 * NB) == 0) ? 2 * NB : (n % NB == 0) ? NB : (n > 1024 ? 2 * NB : NB);
+  if (!OB) OB = fwd_outer_block(n);
   const int64_t N = round_up(n, OB);
   int rc = ensure_ws(al(sizeof(int) * 64));
   if (rc) return rc;
