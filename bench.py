@@ -50,7 +50,7 @@ def config(n: int, world: int, mode: str = "single", grid: tuple = (1, 1)) -> di
                     "SE build + Cholesky + adjoint (BASELINE.json configs[3])",
         "n": n, "nb": (("forward: 256-wide outer blocks of 128-wide tiles (two-level); adjoint: " if n >= 6144
                         else "forward: 128-wide blocks; adjoint: ")
-                       + ("256" if n >= 4096 else "128") + "-wide blocks"),
+                       + ("256" if n >= 768 else "128") + "-wide blocks"),
         "flops_per_step": n ** 3,
         "flop_convention": "n^3/3 (Cholesky) + 2n^3/3 (adjoint)",
         "l2": "inputs exceed L2 (one n x n FP64 matrix = %.1f GiB vs 126 MB L2); no flush needed" % (8 * n * n / 2 ** 30),

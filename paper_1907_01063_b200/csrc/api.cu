@@ -92,7 +92,7 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 struct AdjPlan {
   int64_t N;    // padded order (multiple of B)
   int64_t B;    // adjoint block size: 128 or 256
-  size_t dinv, part, tmp, ctmp, total;
+  size_t dinv, part, tmp, ctmp, hscr, total;
 };
 
 // split-K factor for W = C_bar^T L[k:N, 0:k] (M = B rows; persistent TMA GEMM,
@@ -119,10 +119,12 @@ void splitk_choice(int64_t m, int64_t k, int64_t B, int* splits_out, int* kps_ou
   *splits_out = (int)((m + kps - 1) / kps);
 }
 
-// adjoint block: 256 (fewer, longer-K steps) for large problems, else 128
+// adjoint block: 256 (fewer, longer-K steps; measured faster at every size
+// from n = 1024: 0.47 vs 0.61 ms, 2048: 1.00 vs 1.25 ms, 8192: 14.7 vs 16.0 ms,
+// tools/nb_sweep.py), 128 for the smallest problems (less padding)
 int64_t adj_block(int64_t n) {
   if (g.adj_nb) return g.adj_nb;
-  return n >= 4096 ? 2 * NB : NB;
+  return n >= 768 ? 2 * NB : NB;
 }
 
 AdjPlan adj_plan(int64_t n) {
@@ -142,7 +144,10 @@ AdjPlan adj_plan(int64_t n) {
   p.part = al(part);
   p.tmp = al(4 * (size_t)p.B * p.B * sizeof(double));
   p.ctmp = al((size_t)p.N * p.B * sizeof(double));
-  p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp + p.ctmp;
+  // scratch of the streamed host path's per-block D^-1 (copy stream): its own
+  // region, since the reverse sweep already runs on the main stream meanwhile
+  p.hscr = al((size_t)NB * NB * sizeof(double));
+  p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp + p.ctmp + p.hscr;
   return p;
 }
 
@@ -457,7 +462,13 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
     if (out) {  // column block j is final: ship rows j.. of it
       CK(cudaEventRecord(col_done[j / B], st));
       CK(cudaStreamWaitEvent(g.d2h, col_done[j / B], 0));
-      int rc = copy_rect_d2h(*out, Wm, ld, j, N, j, k, g.d2h);
+      // the diagonal block per 128-row slab (the strict upper outside the 128 x 128
+      // diagonal tiles is left untouched, include/stan_cl.h), then the rows below
+      for (int64_t r0 = j; r0 < k; r0 += NB) {
+        int rc = copy_rect_d2h(*out, Wm, ld, r0, r0 + NB, j, r0 + NB, g.d2h);
+        if (rc) return rc;
+      }
+      int rc = copy_rect_d2h(*out, Wm, ld, k, N, j, k, g.d2h);
       if (rc) return rc;
     }
   }
@@ -871,7 +882,8 @@ int adjoint_host_enqueue(int64_t n, const double* L, const double* L_bar, double
   const int64_t B = plan.B;
   cudaEvent_t* ready = g.xev.data() + 2;
   cudaEvent_t* col_done = ready + nblk;
-  double* scratch = (double*)((char*)g.ws + al(sizeof(int) * 64) + plan.dinv);  // Pbuf, free until the loop
+  // not Pbuf (the split-K partials of the sweep that runs concurrently on the main stream)
+  double* scratch = (double*)((char*)g.ws + al(sizeof(int) * 64) + plan.dinv + plan.part + plan.tmp + plan.ctmp);
   CK(cudaEventRecord(g.xev[0], st));
   CK(cudaStreamWaitEvent(g.h2d, g.xev[0], 0));
   for (int64_t b = nblk - 1; b >= 0; --b) {  // bottom-up: the order the reverse sweep needs

@@ -317,6 +317,26 @@ def test_host_entry_points(sc, n):
     _check_host_output(Ab.numpy(), oracle.cholesky_adjoint(Lo, W), A_BAR_TOL, n)
 
 
+@pytest.mark.parametrize("n", [4096, 5000])
+def test_host_matches_device(sc, n):
+    """The streamed host entry points (packed transfers on copy streams, per-block
+    D^-1 computed on the copy stream while the sweep already runs) reproduce the
+    device-resident calls at sizes with many 256-wide adjoint blocks (the device
+    path is pinned to the oracle elsewhere; the oracle is too slow here)."""
+    K = inputs.gp_x(n)
+    K = oracle.se_cov(K, 1.0, 1.0, 1e-6)
+    W = inputs.lbar(n)
+    Ld = sc.cholesky(torch.from_numpy(K).cuda())
+    Ad = sc.cholesky_adjoint(Ld, torch.from_numpy(W).cuda())
+    Lh = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    assert sc.cholesky_host(torch.from_numpy(K).pin_memory(), Lh) == 0
+    Ah = torch.empty((n, n), dtype=torch.float64).pin_memory()
+    assert sc.cholesky_adjoint_host(Ld.cpu().pin_memory(), torch.from_numpy(W).pin_memory(), Ah) == 0
+    lo = np.tril_indices(n)
+    assert relf(Lh.numpy()[lo], Ld.cpu().numpy()[lo]) <= 1e-14
+    assert relf(Ah.numpy()[lo], Ad.cpu().numpy()[lo]) <= 1e-13
+
+
 def test_host_entry_points_errors(sc):
     n = 400
     A = inputs.toeplitz(n)

@@ -25,3 +25,17 @@ for n in [int(v) for v in sys.argv[1:]] or [1024, 2048, 4096, 8192]:
         out[f"fwd_nb{nb}_ms"] = ev(lambda: sc.cholesky(K, out=L))
     lib.stan_cl_set_block_size(0)
     print(json.dumps(out), flush=True)
+
+# adjoint block 128 vs 256 (stan_cl_set_adjoint_block_size)
+for n in [int(v) for v in sys.argv[1:]] or [1024, 2048, 4096, 8192]:
+    x = torch.from_numpy(inputs.gp_x(n)).cuda()
+    K = sc.gp_exp_quad_cov(x, 1.0, 1.0, 1e-6)
+    L = sc.cholesky(K)
+    W = torch.from_numpy(inputs.lbar(n)).cuda()
+    A = torch.empty_like(K)
+    out = {"n": n}
+    for nb in (128, 256):
+        lib.stan_cl_set_adjoint_block_size(nb)
+        out[f"adj_nb{nb}_ms"] = ev(lambda: sc.cholesky_adjoint(L, W, out=A))
+    lib.stan_cl_set_adjoint_block_size(0)
+    print(json.dumps(out), flush=True)
