@@ -134,10 +134,15 @@ def traffic_from_profiles(kind: str):
 def host_path_bytes(n: int, adj_block: int) -> tuple[int, int]:
     """Bytes the host entry points move per call pair (include/stan_cl.h):
     lower-triangle rectangles, rows [r, r+128) x columns [0, r+128) for K (H2D),
-    L (D2H), and L, L_bar (H2D); A_bar ships per adjoint block column, rows
-    [j, n) x columns [j, j+B) (D2H)."""
+    L (D2H), and L, L_bar (H2D); A_bar ships per adjoint block column j (width
+    B): its diagonal block per 128-row slab, rows [r, r+128) x columns [j, r+128),
+    then rows [j+B, n) x columns [j, j+B) (D2H)."""
     tri = sum(8 * (min(r + 128, n) - r) * min(r + 128, n) for r in range(0, n, 128))
-    cols = sum(8 * (n - j) * (min(j + adj_block, n) - j) for j in range(0, n, adj_block))
+    cols = 0
+    for j in range(0, n, adj_block):
+        k = min(j + adj_block, n)
+        cols += sum(8 * (min(r + 128, n) - r) * (min(r + 128, n) - j) for r in range(j, k, 128))
+        cols += 8 * (n - k) * (k - j)
     return 3 * tri, tri + cols
 
 
@@ -378,9 +383,24 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
         f1.record()
         torch.cuda.synchronize()
         ems = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps, world, dev)
-        hb = host_path_bytes(n, 256 if n >= 4096 else 128)
+        hb = host_path_bytes(n, 256 if n >= 768 else 128)
+        # the host path must reproduce the device-resident results (sampled lower entries;
+        # K was overwritten with the covariance for the upload, so recompute on the device)
+        step()
+        torch.cuda.synchronize()
+        rs = np.random.default_rng(7)
+        ii = rs.integers(0, n, 4096)
+        jj = (rs.random(4096) * (ii + 1)).astype(np.int64)
+        idx = torch.from_numpy(ii * n + jj)
+        Ld_s, Ad_s = K.flatten()[idx.to(dev)].cpu(), Abar.flatten()[idx.to(dev)].cpu()
+        Lh_s, Ah_s = Lh.flatten()[idx], Abh.flatten()[idx]
+        rel_L = float((Lh_s - Ld_s).norm() / Ld_s.norm())
+        rel_A = float((Ah_s - Ad_s).norm() / Ad_s.norm())
+        if not (rel_L <= 1e-13 and rel_A <= 1e-12):
+            raise RuntimeError(f"host-path results differ from the device path: L {rel_L:.2e}, A_bar {rel_A:.2e}")
         e2e = {"value": jobs * flops / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": hb[0], "d2h_bytes_per_step": hb[1],
+               "checked_vs_device": {"samples": 4096, "L_rel": rel_L, "A_bar_rel": rel_A},
                "path": "stan_cl_cholesky_host(K) + stan_cl_cholesky_adjoint_host(L, L_bar), pinned host buffers"}
         del Kh, Lh, Lbh, Abh
 
