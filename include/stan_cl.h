@@ -228,11 +228,11 @@ int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, 
 int stan_cl_set_stream(void* cuda_stream); /* cudaStream_t; NULL = legacy default stream */
 void* stan_cl_get_stream(void);
 /* outer block size of the blocked Cholesky: 0 = auto (256 = two-level blocking
- * with 128-wide diagonal tiles when it pays, else 128), 128 or 256; others ->
+ * with 128-wide diagonal tiles for n >= 6144, else 128), 128 or 256; others ->
  * STAN_CL_EINVAL. */
 int stan_cl_set_block_size(int nb);
 int stan_cl_get_block_size(void);
-/* block size of the blocked adjoint: 0 = auto (256 for n >= 4096, else 128),
+/* block size of the blocked adjoint: 0 = auto (256 for n >= 768, else 128),
  * 128 or 256; others -> STAN_CL_EINVAL */
 int stan_cl_set_adjoint_block_size(int nb);
 /* device workspace the next call of order n would use (bytes) */
