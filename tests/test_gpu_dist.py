@@ -155,6 +155,36 @@ def test_dist_sim2_adjoint(sc, n, P, Q):
     assert np.array_equal(np.tril(sc.dist_gather2(Ws, n, P, Q).cpu().numpy()), oracle.cholesky_adjoint(Li, Wi))
 
 
+@pytest.mark.parametrize("n,P,Q", [(4096, 2, 4), (4096, 4, 2), (3072, 3, 3)])
+def test_dist_sim2_large(sc, n, P, Q):
+    """More steps and wider column exchanges than the oracle-sized cases: the
+    distributed results against the single-GPU device path (itself pinned to the
+    oracle) and the integer-exact families bit for bit."""
+    K = se(n)
+    Kt = torch.from_numpy(K).cuda()
+    L1 = sc.cholesky(Kt)
+    W = inputs.lbar(n)
+    A1 = sc.cholesky_adjoint(L1, torch.from_numpy(W).cuda())
+    locs = scatter2(sc, K, P, Q)
+    assert sc.dist_sim2_cholesky(locs, n, P, Q) == 0
+    Ld = sc.dist_gather2(locs, n, P, Q).cpu().numpy()
+    check_lower_and_tiles(Ld, L1.cpu().numpy(), 1e-11)
+    L1n = L1.cpu().numpy()
+    Ls, Ws = scatter2(sc, L1n, P, Q), scatter2(sc, W, P, Q)
+    assert sc.dist_sim2_cholesky_adjoint(Ls, Ws, n, P, Q) == 0
+    check_lower_and_tiles(sc.dist_gather2(Ws, n, P, Q).cpu().numpy(), A1.cpu().numpy(), 1e-9)
+    L0 = inputs.unit_lower_pm1(n, seed=n + 7)
+    locs = scatter2(sc, inputs.gram_exact(L0), P, Q)
+    assert sc.dist_sim2_cholesky(locs, n, P, Q) == 0
+    assert np.array_equal(np.tril(sc.dist_gather2(locs, n, P, Q).cpu().numpy()), L0)
+    Li = inputs.unit_lower_pm1(n, seed=5, band=2)
+    Wi = inputs.int_lbar(n, seed=6)
+    Ls, Ws = scatter2(sc, Li, P, Q), scatter2(sc, Wi, P, Q)
+    assert sc.dist_sim2_cholesky_adjoint(Ls, Ws, n, P, Q) == 0
+    Ai = sc.cholesky_adjoint(torch.from_numpy(Li).cuda(), torch.from_numpy(Wi).cuda()).cpu().numpy()
+    assert np.array_equal(np.tril(sc.dist_gather2(Ws, n, P, Q).cpu().numpy()), np.tril(Ai))
+
+
 def test_dist_sim2_matches_single_gpu_layout(sc):
     """P = 1 of the 2-D code is the block-column layout: same bits as dist_sim on 1 x G."""
     n = 1280
