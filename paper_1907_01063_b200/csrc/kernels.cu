@@ -1266,8 +1266,92 @@ __device__ __forceinline__ void grid_barrier(unsigned* ctr, unsigned target) {
   __syncthreads();
 }
 
+// One 32 x 32 tile with 256 threads: warp group g (128 threads) contracts the
+// K half [g S/2, (g+1) S/2), both halves' loads in flight at once; group 1's
+// partial tile is added to group 0's through shared memory (sum = half0 + half1).
 template <int S>
-__global__ void __launch_bounds__(128) adj_diag_kernel(const double* __restrict__ D, int64_t ldl,
+constexpr int gemmS2_region() {
+  return 32 * (S / 2 + 4) + (S / 2) * G128_BP;  // doubles per group: As [32][S/2+4], Bs [S/2][36]
+}
+template <int S, bool A_T, bool A_TRIL, bool B_SYM, bool C_SYM>
+__device__ __forceinline__ void gemmS_tile2(const double* __restrict__ A, int64_t lda, const double* __restrict__ B,
+                                            int64_t ldb, double* __restrict__ C, int64_t ldc, int m0, int n0,
+                                            double* sm) {
+  constexpr int CW = S / 2, AP = CW + 4, NQ = CW / 4;
+  const int tid = threadIdx.x, grp = tid >> 7, lt = tid & 127, lane = tid & 31, warp = (tid >> 5) & 3;
+  const int wm = warp >> 1, wn = warp & 1, g = lane >> 2, t = lane & 3;
+  double* As = sm + grp * gemmS2_region<S>();  // [32][AP]  As[m][k - k0]
+  double* Bs = As + 32 * AP;                     // [CW][G128_BP]  Bs[k - k0][n]
+  const int k0 = grp * CW;
+  double va[NQ], vb[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int idx = lt + q * 128;
+    if (A_T) {
+      const int k = k0 + (idx >> 5), m = m0 + (idx & 31);
+      va[q] = (A_TRIL && m > k) ? 0.0 : __ldcg(A + (long long)k * lda + m);
+    } else {
+      const int m = m0 + idx / CW, k = k0 + idx % CW;
+      va[q] = (A_TRIL && k > m) ? 0.0 : __ldcg(A + (long long)m * lda + k);
+    }
+    const int k = k0 + (idx >> 5), gn = n0 + (idx & 31);
+    if (B_SYM) vb[q] = (k >= gn) ? __ldcg(B + (long long)k * ldb + gn) : __ldcg(B + (long long)gn * ldb + k);
+    else vb[q] = __ldcg(B + (long long)k * ldb + gn);
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int idx = lt + q * 128;
+    if (A_T) As[(idx & 31) * AP + (idx >> 5)] = va[q];
+    else As[(idx / CW) * AP + (idx % CW)] = va[q];
+    Bs[(idx >> 5) * G128_BP + (idx & 31)] = vb[q];
+  }
+  __syncthreads();
+  double acc[2][2][2] = {};
+#pragma unroll 8
+  for (int k4 = 0; k4 < CW; k4 += 4) {
+    double af[2], bf[2];
+#pragma unroll
+    for (int i = 0; i < 2; ++i) af[i] = As[(wm * 16 + i * 8 + g) * AP + k4 + t];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) bf[j] = Bs[(k4 + t) * G128_BP + wn * 16 + j * 8 + g];
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+  }
+  __syncthreads();
+  double* red = sm + gemmS2_region<S>();  // group 1's region, free now
+  if (grp == 1) {
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[(e * 4 + warp) * 32 + lane] = acc[e >> 2][(e >> 1) & 1][e & 1];
+  }
+  __syncthreads();
+  if (grp == 0) {
+#pragma unroll
+    for (int i = 0; i < 2; ++i)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        double v[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) v[h] = acc[i][j][h] + red[(((i * 2 + j) * 2 + h) * 4 + warp) * 32 + lane];
+        const int r = m0 + wm * 16 + i * 8 + g, c = n0 + wn * 16 + j * 8 + 2 * t;
+        if (!C_SYM) {
+          *reinterpret_cast<double2*>(C + (long long)r * ldc + c) = make_double2(v[0], v[1]);
+        } else {  // C = sym(tril(product)): element (r, c), r >= c, also lands at (c, r)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            if (r >= c + h) {
+              C[(long long)r * ldc + c + h] = v[h];
+              C[(long long)(c + h) * ldc + r] = v[h];
+            }
+          }
+        }
+      }
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(256) adj_diag_kernel(const double* __restrict__ D, int64_t ldl,
                                                        double* __restrict__ Dbar, int64_t ldw,
                                                        const double* __restrict__ Di, double* __restrict__ T1,
                                                        double* __restrict__ T2, double* __restrict__ T3,
@@ -1279,11 +1363,11 @@ __global__ void __launch_bounds__(128) adj_diag_kernel(const double* __restrict_
   constexpr int TT = S / 32;
   const unsigned nb = gridDim.x;
   const int m0 = (blockIdx.x / TT) * 32, n0 = (blockIdx.x % TT) * 32;
-  if (m0 >= n0) gemmS_tile<S, true, true, false, true>(D, ldl, Dbar, ldw, T1, S, 1.0, m0, n0, sm);
+  if (m0 >= n0) gemmS_tile2<S, true, true, false, true>(D, ldl, Dbar, ldw, T1, S, m0, n0, sm);
   grid_barrier(ctr, nb);
-  gemmS_tile<S, true, false, false, false>(Di, S, T1, S, T2, S, 1.0, m0, n0, sm);
+  gemmS_tile2<S, true, false, false, false>(Di, S, T1, S, T2, S, m0, n0, sm);
   grid_barrier(ctr, 2 * nb);
-  gemmS_tile<S, false, false, false, false>(T2, S, Di, S, T3, S, 1.0, m0, n0, sm);
+  gemmS_tile2<S, false, false, false, false>(T2, S, Di, S, T3, S, m0, n0, sm);
   grid_barrier(ctr, 3 * nb);
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < S * S; idx += nb * blockDim.x) {
     const int a = idx / S, b = idx - a * S;
@@ -1300,6 +1384,9 @@ __global__ void __launch_bounds__(128) adj_diag_kernel(const double* __restrict_
   }
 }
 
+template <int S>
+constexpr int ADJ_DIAG_SMEM = 2 * gemmS2_region<S>() * (int)sizeof(double);
+
 cudaError_t adj_diag_fused(int S, const double* D, int64_t ldl, double* Dbar, int64_t ldw, const double* Di,
                            double* T1, double* T2, double* T3, double* Ssym, unsigned* ctr, const int* status,
                            cudaStream_t st) {
@@ -1308,20 +1395,20 @@ cudaError_t adj_diag_fused(int S, const double* D, int64_t ldl, double* Dbar, in
   if (S == 256) {
     static bool attr = false;
     if (!attr) {
-      e = cudaFuncSetAttribute(adj_diag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, G128_SMEM);
+      e = cudaFuncSetAttribute(adj_diag_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, ADJ_DIAG_SMEM<256>);
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    e = launch_pdl(adj_diag_kernel<256>, 64, 128, G128_SMEM, st, D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
+    e = launch_pdl(adj_diag_kernel<256>, 64, 256, ADJ_DIAG_SMEM<256>, st, D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
     if (e != cudaSuccess) return e;
   } else if (S == 128) {
     static bool attr = false;
     if (!attr) {
-      e = cudaFuncSetAttribute(adj_diag_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, G128_SMEM);
+      e = cudaFuncSetAttribute(adj_diag_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, ADJ_DIAG_SMEM<128>);
       if (e != cudaSuccess) return e;
       attr = true;
     }
-    e = launch_pdl(adj_diag_kernel<128>, 16, 128, G128_SMEM, st, D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
+    e = launch_pdl(adj_diag_kernel<128>, 16, 256, ADJ_DIAG_SMEM<128>, st, D, ldl, Dbar, ldw, Di, T1, T2, T3, Ssym, ctr, status);
     if (e != cudaSuccess) return e;
   } else {
     return cudaErrorInvalidValue;
