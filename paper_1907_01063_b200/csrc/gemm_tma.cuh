@@ -141,6 +141,33 @@ __device__ __forceinline__ double frag(const double* s, int rc, int k) {
 template <class CF, int MODE>
 struct TItemMap {
   int ntn, ntiles, ktiles_full;
+  // block-cyclic mode (GemmArgs::cyc, MODE_FULL): items enumerate, per 256-wide
+  // block column j, only its tile rows from the first block row that reaches
+  // the diagonal (2 f_j) down; cyc_pref[j] = first item of block column j
+  static constexpr int kCycMax = (MODE == MODE_FULL) ? 512 : 1;
+  int cyc_nb = 0;
+  int cyc_pref[kCycMax + 1];
+  // item -> tile (tm, tn) in the rectangle (cyc) or row-major (otherwise)
+  __device__ __forceinline__ void tile_of(const GemmArgs& p, int tile, int& tm, int& tn) const {
+    if constexpr (MODE == MODE_FULL) {
+      if (p.cyc) {
+        int lo = 0, hi = cyc_nb;  // largest j with cyc_pref[j] <= tile
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (cyc_pref[mid] <= tile) lo = mid;
+          else hi = mid;
+        }
+        const int rows = (cyc_pref[lo + 1] - cyc_pref[lo]) / 4;  // tile rows of block column lo
+        const int first = 2 * (p.M / 256) - rows;                  // = 2 f_j
+        const int local = tile - cyc_pref[lo];
+        tm = first + local / 4;
+        tn = 4 * lo + (local & 3);
+        return;
+      }
+    }
+    tm = tile / ntn;
+    tn = tile - tm * ntn;
+  }
   // block-cyclic lower mask (GemmArgs::cyc): is the item computed, and the
   // diagonal offset d of its block (elements kept iff r >= c + d) if masked
   __device__ __forceinline__ bool valid(const GemmArgs& p, int item, bool& masked, int& d) const {
@@ -150,7 +177,8 @@ struct TItemMap {
       return true;
     } else {
       if (!p.cyc) return true;
-      const int tm = item / ntn, tn = item - (item / ntn) * ntn;
+      int tm, tn;
+      tile_of(p, item, tm, tn);
       const int bi = tm / (256 / CF::BM), bj = tn / (256 / CF::BN);
       const long long I = (long long)(p.cy_li + bi) * p.cy_P + p.cy_p, J = (long long)(p.cy_lj + bj) * p.cy_Q + p.cy_q;
       if (I < J) return false;
@@ -179,8 +207,7 @@ struct TItemMap {
     if constexpr (MODE == MODE_LOWER) {
       tri_index<CF::BM / CF::BN>(tile, tm, tn);
     } else {
-      tm = tile / ntn;
-      tn = tile - tm * ntn;
+      tile_of(p, tile, tm, tn);
     }
     m0 = tm * CF::BM;
     n0 = tn * CF::BN;
@@ -418,6 +445,22 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reser
     ntiles = R * T * (T + 1) / 2;
   } else {
     ntiles = (p.M / CF::BM) * map.ntn;
+  }
+  if constexpr (MODE == MODE_FULL) {
+    if (p.cyc) {  // valid tile rows per 256-wide block column (BM = 128, BN = 64)
+      const int nbc = p.N / 256, nbr = p.M / 256;
+      if (nbc > TItemMap<CF, MODE>::kCycMax) return cudaErrorInvalidValue;
+      map.cyc_nb = nbc;
+      map.cyc_pref[0] = 0;
+      for (int j = 0; j < nbc; ++j) {
+        const long long J = (long long)(p.cy_lj + j) * p.cy_Q + p.cy_q;
+        // first local block row with global I >= J, relative to the rectangle's first row
+        long long f = (J > p.cy_p ? (J - p.cy_p + p.cy_P - 1) / p.cy_P : 0) - p.cy_li;
+        f = f < 0 ? 0 : (f > nbr ? nbr : f);
+        map.cyc_pref[j + 1] = map.cyc_pref[j] + 8 * (int)(nbr - f);
+      }
+      ntiles = map.cyc_pref[nbc];
+    }
   }
   map.ntiles = ntiles;
   const int nitems = ntiles * (MODE == MODE_SPLITK ? splits : 1);
