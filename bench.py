@@ -44,10 +44,15 @@ REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_pow
                0x100: "display_clock_setting"}
 
 
+def baseline_config_index(n: int, world: int) -> str:
+    idx = {64: 0, 1024: 1, 8192: 2, 16384: 3, 65536: 4}.get(n)
+    return f"BASELINE.json configs[{idx}]" if idx is not None else "not a BASELINE.json config"
+
+
 def config(n: int, world: int, mode: str = "single", grid: tuple = (1, 1)) -> dict:
     return {
         "workload": f"SE-kernel GP covariance n={n} (1-D x~U(-10,10), alpha=rho=1, jitter 1e-6): "
-                    "SE build + Cholesky + adjoint (BASELINE.json configs[3])",
+                    f"SE build + Cholesky + adjoint ({baseline_config_index(n, world)})",
         "n": n, "nb": (("forward: 256-wide outer blocks of 128-wide tiles (two-level); adjoint: " if n >= 6144
                         else "forward: 128-wide blocks; adjoint: ")
                        + ("256" if n >= 768 else "128") + "-wide blocks"),
@@ -245,7 +250,12 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
         gp, gq = divmod(rank, Q)
         x = torch.from_numpy(inputs.gp_x(n)).to(dev)
         hrows, w = sc.dist_local_shape(n, P, Q, gp, gq)
-        Lbar_loc = sc.dist_scatter2(torch.from_numpy(inputs.lbar(n)), P, Q, gp, gq).contiguous().to(dev)
+        # L_bar's local tiles ~ N(0, 1), drawn on the device per rank (seed 43 + rank):
+        # the full n x n host matrix would be 32 GiB per rank at n = 65536; only
+        # lower tiles are read (the tiles above the diagonal are ignored)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(inputs.LBAR_SEED + rank)
+        Lbar_loc = torch.randn((hrows, w), dtype=torch.float64, device=dev, generator=gen)
         K_loc = torch.empty((hrows, w), dtype=torch.float64, device=dev)
         W_loc = torch.empty_like(K_loc)
 
@@ -255,20 +265,27 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
             W_loc.copy_(Lbar_loc)
             sc.dist_cholesky_adjoint(K_loc, W_loc, n)                           # R0-R5, NCCL broadcasts
 
+        # two pinned host buffers per rank: K in / L out share one (the upload
+        # precedes the download on the stream), L_bar in / A_bar out the other
         Kh = torch.empty((hrows, w), dtype=torch.float64).pin_memory()
-        Lbh = Lbar_loc.cpu().pin_memory()
-        Lh = torch.empty_like(Kh).pin_memory()
-        Abh = torch.empty_like(Kh).pin_memory()
+        Lbh = torch.empty((hrows, w), dtype=torch.float64).pin_memory()
+        Lbh.copy_(Lbar_loc)
+        Khost = torch.empty_like(Kh)
         sc.gp_exp_quad_cov_tiles(x, K_loc, P, Q, gp, gq, ALPHA, RHO, JITTER)
-        Kh.copy_(K_loc)
+        Khost.copy_(K_loc)
+        Lbhost = Lbh.clone()
 
         def e2e_fn():
             K_loc.copy_(Kh, non_blocking=True)
             sc.dist_cholesky(K_loc, n)
-            Lh.copy_(K_loc, non_blocking=True)
+            Kh.copy_(K_loc, non_blocking=True)                 # L out
             W_loc.copy_(Lbh, non_blocking=True)
             sc.dist_cholesky_adjoint(K_loc, W_loc, n)
-            Abh.copy_(W_loc, non_blocking=True)
+            Lbh.copy_(W_loc, non_blocking=True)                # A_bar out
+
+        def e2e_reset():                                       # fresh inputs before each timed e2e step
+            Kh.copy_(Khost)
+            Lbh.copy_(Lbhost)
         e2e_bytes = (2 * 8 * hrows * w, 2 * 8 * hrows * w)
         e2e_path = "per rank: pinned H2D of its K and L_bar tiles, dist_cholesky + dist_cholesky_adjoint, D2H of L and A_bar"
     else:
@@ -344,17 +361,22 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
     # end-to-end through the public host-buffer API (pinned host in/out)
     e2e = None
     if args.e2e_steps > 0 and e2e_fn is not None:
+        e2e_reset()
         e2e_fn()
         torch.cuda.synchronize()
-        barrier()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record()
+        ems_l = []
         for _ in range(args.e2e_steps):
+            e2e_reset()                                        # host-side refill, outside the timed region
+            barrier()
+            torch.cuda.synchronize()
+            f0 = torch.cuda.Event(enable_timing=True)
+            f1 = torch.cuda.Event(enable_timing=True)
+            f0.record()
             e2e_fn()
-        f1.record()
-        torch.cuda.synchronize()
-        ems = max_over_ranks(f0.elapsed_time(f1) / args.e2e_steps, world, dev)
+            f1.record()
+            torch.cuda.synchronize()
+            ems_l.append(f0.elapsed_time(f1))
+        ems = max_over_ranks(sum(ems_l) / len(ems_l), world, dev)
         e2e = {"value": flops / (ems / 1e3) / 1e9, "unit": UNIT, "ms_per_step": ems,
                "h2d_bytes_per_step": int(e2e_bytes[0]) * world, "d2h_bytes_per_step": int(e2e_bytes[1]) * world,
                "path": e2e_path}
@@ -421,12 +443,53 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
     print(json.dumps(line), flush=True)
 
 
+def dry_run(args, rank: int, world: int):
+    """No device work: rendezvous over gloo, barrier, max over ranks of a per-rank
+    number, one JSON line on rank 0 (tests/test_bench_cpu.py)."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    try:
+        t0 = time.perf_counter()
+        if world > 1:
+            dist.barrier()
+        for _ in range(args.warmup + args.steps):
+            pass
+        ms = (time.perf_counter() - t0) * 1e3
+        if world > 1:
+            t = torch.tensor([ms], dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        if rank == 0:
+            grid = dist_grid_default(world)
+            print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "unit": UNIT, "n_gpus": world,
+                              "steps": args.steps, "warmup": args.warmup, "ms_per_step": None,
+                              "host_ms_max_over_ranks": ms, "higher_is_better": True,
+                              "scaling": "strong" if world > 1 else "weak",
+                              "config": config(args.n, world, "dist" if world > 1 else "single", grid)}),
+                  flush=True)
+    finally:
+        if world > 1:
+            dist.destroy_process_group()
+
+
+def dist_grid_default(G: int) -> tuple:
+    """Same rule as paper_1907_01063_b200.dist_grid (1x1, 1x2, 2x2, 2x4, ...)."""
+    P = max(d for d in range(1, int(G ** 0.5) + 1) if G % d == 0)
+    return P, G // P
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--n", type=int, default=16384)
+    ap.add_argument("--n", type=int, default=None,
+                    help="order (default: 16384 = BASELINE configs[3] at N=1; 65536 = configs[4] at N>1)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="CPU plumbing check: launch/rendezvous (gloo), barrier, max-over-ranks and the JSON "
+                         "line, with no device work (value is null)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--oracle-n", type=int, default=ORACLE_SAMPLE_N)
@@ -437,9 +500,32 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    if args.n is None:
+        args.n = 16384 if args.gpus == 1 else 65536
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        # one process per GPU: re-launch this script under torchrun (the driver
+        # normally does this itself; a bare `bench.py --gpus N` must not silently
+        # run one GPU)
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        print(f"[bench] launching {args.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print(f"[bench] refusing to report: WORLD_SIZE={world} but --gpus {args.gpus}", file=sys.stderr, flush=True)
+        sys.exit(2)
+    if args.dry_run:
+        dry_run(args, rank, world)
+        return
     if args.impl == "reference":
         bench_reference(args, rank, world)
         return

@@ -19,9 +19,14 @@
  *     points return immediately and leave the status in device memory.
  *
  * Ownership: the caller owns every buffer passed in.  The library owns only
- * its internal workspace (allocated lazily, released by stan_cl_finalize);
- * no pointer is retained after a call returns.  Calls are not thread-safe
- * with respect to each other (one library stream and workspace per process).
+ * its internal workspace (allocated lazily, released by stan_cl_finalize), or
+ * uses a caller-provided one instead (stan_cl_set_workspace).  No pointer is
+ * dereferenced after a call returns; the CUDA-graph cache of the n <= 4096
+ * device calls remembers the buffer addresses of a call only as a lookup key
+ * (a replay happens only for a call with the same addresses, and a cached
+ * graph is discarded whenever a workspace buffer it wrote through moved).
+ * Calls are not thread-safe with respect to each other (one library stream
+ * and workspace per process).
  *
  * Return values: 0 = success; k > 0 = numerical failure (see each call);
  * negative = STAN_CL_E* error codes below.
@@ -104,10 +109,12 @@ int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_b
  * ships each factored panel while the trailing update continues; the adjoint
  * uploads row blocks bottom-up (the order its reverse sweep consumes them) and
  * ships each column block of A_bar as soon as it is final.  The call returns
- * after the last copy-back.  Output contract: the lower triangle of the host
- * output is written; inside the 128 x 128 diagonal tiles the strict upper part
- * is written as +0.0; the rest of the strict upper triangle is NOT written
- * (LAPACK convention).  Same return values as the device calls.
+ * after the last copy-back.  Output contract as the device calls: the whole
+ * n x n host output is written, strict upper triangle +0.0 (the diagonal
+ * tiles' upper part comes over PCIe with them; the rest is zero-filled by host
+ * threads while the device computes, so it costs no PCIe traffic).  A == L
+ * (forward) and L_bar == A_bar (adjoint) are allowed; other overlaps ->
+ * STAN_CL_EINVAL.  Same return values as the device calls.
  */
 int stan_cl_cholesky_host(int64_t n, const double* A, double* L);
 int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar);
@@ -167,6 +174,21 @@ int stan_cl_dist_sim2_cholesky(int64_t n, int P, int Q, double* const* A_locals,
 int stan_cl_dist_sim2_cholesky_adjoint(int64_t n, int P, int Q, const double* const* L_locals,
                                        double* const* W_locals, int64_t ld_local);
 int stan_cl_dist_sim_cholesky(int64_t n, int G, double* const* A_locals, int64_t ld_local);
+/* Collective trace of rank (p, q) of a P x Q grid, for checking the multi-GPU
+ * schedule on one device: runs the real per-rank path of stan_cl_dist_cholesky
+ * (adjoint == 0; A_local in place) or stan_cl_dist_cholesky_adjoint
+ * (adjoint != 0; L_local, A_local = L_bar in place) with every NCCL call
+ * replaced by a record of what it would issue, in host issue order (no data
+ * moves, so the numbers are meaningless).  Each record is 6 int64 in out:
+ * communicator kind (0 row, 1 column, 2 world), its index (p, q or 0), op
+ * (0 broadcast, 1 sum-reduce, 2 max-all-reduce), root index within the
+ * communicator (-1 for none), element count, stream (0 library stream,
+ * 1 side stream).  Writes at most max_entries records; returns the total
+ * number of records (>= 0) or a negative error.  Every member of a
+ * communicator must produce the same sequence of records on it, else the
+ * NCCL path would deadlock or mismatch counts (tests/test_gpu_dist.py). */
+int stan_cl_dist_trace(int64_t n, int P, int Q, int p, int q, int adjoint, const double* L_local,
+                       double* A_local, int64_t ld_local, int64_t* out, int64_t max_entries);
 int stan_cl_dist_sim_cholesky_adjoint(int64_t n, int G, const double* const* L_locals, double* const* W_locals,
                                       int64_t ld_local);
 
@@ -235,8 +257,30 @@ int stan_cl_get_block_size(void);
 /* block size of the blocked adjoint: 0 = auto (256 for n >= 768, else 128),
  * 128 or 256; others -> STAN_CL_EINVAL */
 int stan_cl_set_adjoint_block_size(int nb);
-/* device workspace the next call of order n would use (bytes) */
+/*
+ * Caller-owned workspace (SURVEY.md §8(b) "lazily allocated ... or
+ * caller-provided").  stan_cl_set_workspace(ptr, bytes): every device buffer
+ * the library needs (status word, D^-1 blocks, split-K partials, padded
+ * copies, GP matrices, the multi-GPU scratch) is carved from [ptr, ptr+bytes)
+ * afresh by each call; the library then allocates no device memory of its own
+ * (library-owned workspace is freed here) and never frees ptr.  ptr must be a
+ * device pointer aligned to 256 bytes with bytes >= 256; NULL reverts to
+ * library-owned workspace.  Synchronises the device.  A call whose needs
+ * exceed bytes returns STAN_CL_ENOMEM and does nothing else (stan_cl_status_string
+ * names the size it needed).  The buffer must stay allocated until
+ * stan_cl_set_workspace(NULL, 0) or stan_cl_finalize.  Returns STAN_CL_EINVAL
+ * for a misaligned / too small buffer.
+ * stan_cl_workspace_bytes(n): bytes that suffice for every single-matrix entry
+ * point at order n (cholesky, cholesky_adjoint, their _async and _host forms,
+ * trsv, gp_lpdf_grad) with the current block-size settings and 16-byte
+ * aligned arguments (an unaligned argument takes the padded path: add
+ * 2 * 8 * N^2, N = n rounded up to 256).
+ * stan_cl_batched_workspace_bytes(batch, n, with_info): the same for the batched
+ * calls (with_info != 0: the caller passes its own info array).
+ */
+int stan_cl_set_workspace(void* dev_ptr, size_t bytes);
 size_t stan_cl_workspace_bytes(int64_t n);
+size_t stan_cl_batched_workspace_bytes(int64_t batch, int64_t n, int with_info);
 const char* stan_cl_status_string(int status);
 /* number of CUDA kernel launches the library has issued so far (process-wide) */
 long long stan_cl_kernel_launches(void);

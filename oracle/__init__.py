@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
-CFLAGS = ["-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared"]
+CFLAGS = ["-std=c99", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fopenmp", "-fPIC", "-shared"]
 
 _lib = None
 
@@ -46,6 +46,8 @@ def _load():
         for name in ("oracle_cholesky", "oracle_cholesky_ld"):
             getattr(lib, name).argtypes = [I64, P, P]
             getattr(lib, name).restype = ctypes.c_int
+        lib.oracle_cholesky_par.argtypes = [I64, P, P, ctypes.c_int]
+        lib.oracle_cholesky_par.restype = ctypes.c_int
         lib.oracle_cholesky_adjoint.argtypes = [I64, P, P, P]
         lib.oracle_cholesky_adjoint.restype = ctypes.c_int
         lib.oracle_trsv.argtypes = [I64, P, P, ctypes.c_int, P]
@@ -92,6 +94,24 @@ def cholesky_info(A) -> tuple[np.ndarray, int]:
 
 def cholesky(A) -> np.ndarray:
     L, info = cholesky_info(A)
+    if info != 0:
+        raise NotPositiveDefinite(info)
+    return L
+
+
+def cholesky_par_info(A, nthreads: int = 0) -> tuple[np.ndarray, int]:
+    """(L, info) of ``cholesky_info`` bit for bit, independent entries on
+    ``nthreads`` threads (0 = all cores; oracle.c oracle_cholesky_par)."""
+    A = _c(A)
+    n = A.shape[0]
+    assert A.shape == (n, n)
+    L = np.empty_like(A)
+    info = _load().oracle_cholesky_par(n, _ptr(A), _ptr(L), int(nthreads or os.cpu_count() or 1))
+    return L, int(info)
+
+
+def cholesky_par(A, nthreads: int = 0) -> np.ndarray:
+    L, info = cholesky_par_info(A, nthreads)
     if info != 0:
         raise NotPositiveDefinite(info)
     return L

@@ -17,6 +17,8 @@
  *   oracle_se_cov              pinned (symmetry, diagonal, closed-form entries)
  *   oracle_cholesky            pinned (closed forms, reconstruction, exact log-det,
  *                               integer-exact family, non-PD cases)
+ *   oracle_cholesky_par        oracle_cholesky with independent entries computed by
+ *                               several threads; pinned by bit-identity with it
  *   oracle_cholesky_ld         long-double twin of oracle_cholesky, used only as a
  *                               truth proxy for rounding-floor studies; pinned by
  *                               the same closed forms
@@ -82,6 +84,59 @@ int oracle_cholesky(int64_t n, const double* A, double* L) {
       }
     }
     for (int64_t j = i + 1; j < n; ++j) L[IDX(i, j)] = 0.0;
+  }
+  return 0;
+}
+
+/*
+ * oracle_cholesky with its independent work spread over threads, bit for bit
+ * the same result.  Each entry L[i][j] is computed by the same statements, in
+ * the same order, from the same operands as in oracle_cholesky -- only the
+ * order in which DIFFERENT entries are computed changes, and only among
+ * entries whose operands are already final:
+ *   for each block of 32 rows [r0, r1):
+ *     (1) entries j < r0 of every row in the block, one row per thread (they
+ *         need rows < r0, complete, and the row's own entries to their left);
+ *     (2) entries r0 <= j <= i, rows in order (the block's own triangle),
+ *         with the pivot test of oracle_cholesky.
+ * So info (the first failing pivot row + 1) is oracle_cholesky's as well.
+ * Used only to rebuild the oracle's L at n = 8192 / 16384 in a GPU test (a
+ * single thread needs ~20 min at 16384); pinned by bit-identity with
+ * oracle_cholesky (tests/test_oracle.py) and by the SHA-256 of the sequential
+ * oracle's L stored in tests/golden/.
+ */
+int oracle_cholesky_par(int64_t n, const double* A, double* L, int nthreads) {
+  const int64_t RB = 32;
+  if (nthreads < 1) nthreads = 1;
+  for (int64_t r0 = 0; r0 < n; r0 += RB) {
+    const int64_t r1 = (r0 + RB < n) ? r0 + RB : n;
+#pragma omp parallel for schedule(static, 1) num_threads(nthreads)
+    for (int64_t i = r0; i < r1; ++i) {
+      for (int64_t j = 0; j < r0; ++j) {
+        double s = A[IDX(i, j)];
+        for (int64_t k = 0; k < j; ++k) {
+          double p = L[IDX(i, k)] * L[IDX(j, k)];
+          s = s - p;
+        }
+        L[IDX(i, j)] = s / L[IDX(j, j)];
+      }
+    }
+    for (int64_t i = r0; i < r1; ++i) {
+      for (int64_t j = r0; j <= i; ++j) {
+        double s = A[IDX(i, j)];
+        for (int64_t k = 0; k < j; ++k) {
+          double p = L[IDX(i, k)] * L[IDX(j, k)];
+          s = s - p;
+        }
+        if (i == j) {
+          if (!(s > 0.0)) return (int)(i + 1);
+          L[IDX(i, i)] = sqrt(s);
+        } else {
+          L[IDX(i, j)] = s / L[IDX(j, j)];
+        }
+      }
+      for (int64_t j = i + 1; j < n; ++j) L[IDX(i, j)] = 0.0;
+    }
   }
   return 0;
 }

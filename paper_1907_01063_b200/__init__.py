@@ -22,7 +22,8 @@ import torch
 __all__ = [
     "cholesky", "cholesky_adjoint", "gp_exp_quad_cov", "cholesky_async", "cholesky_adjoint_async",
     "cholesky_host", "cholesky_adjoint_host", "kernel_launches", "library_path", "load",
-    "StanClError", "NotPositiveDefinite", "STATUS", "workspace_bytes", "finalize",
+    "StanClError", "NotPositiveDefinite", "STATUS", "workspace_bytes", "finalize", "set_workspace",
+    "batched_workspace_bytes",
     "profile_enable", "profile_reset", "profile_read", "PROFILE_KINDS",
 ]
 
@@ -53,6 +54,8 @@ SIGNATURES = {
     "stan_cl_get_block_size": (_I, []),
     "stan_cl_set_adjoint_block_size": (_I, [_I]),
     "stan_cl_workspace_bytes": (ctypes.c_size_t, [_I64]),
+    "stan_cl_batched_workspace_bytes": (ctypes.c_size_t, [_I64, _I64, _I]),
+    "stan_cl_set_workspace": (_I, [_P, ctypes.c_size_t]),
     "stan_cl_status_string": (ctypes.c_char_p, [_I]),
     "stan_cl_kernel_launches": (ctypes.c_longlong, []),
     "stan_cl_profile_enable": (_I, [_I]),
@@ -66,6 +69,7 @@ SIGNATURES = {
     "stan_cl_dist_cholesky": (_I, [_I64, _I, _P, _I64]),
     "stan_cl_dist_cholesky_adjoint": (_I, [_I64, _I, _P, _P, _I64]),
     "stan_cl_dist_finalize": (_I, []),
+    "stan_cl_dist_trace": (_I, [_I64, _I, _I, _I, _I, _I, _P, _P, _I64, _P, _I64]),
     "stan_cl_dist_sim_cholesky": (_I, [_I64, _I, _P, _I64]),
     "stan_cl_gp_exp_quad_cov_cols": (_I, [_I64, _P, _D, _D, _D, _P, _I64, _I, _I]),
     "stan_cl_dist_sim_cholesky_adjoint": (_I, [_I64, _I, _P, _P, _I64]),
@@ -128,11 +132,33 @@ def _dev_matrix(t: torch.Tensor, name: str) -> torch.Tensor:
     return t.contiguous()
 
 
+def _out(out: torch.Tensor | None, shape: tuple, device: torch.device, name: str = "out",
+         dtype: torch.dtype = torch.float64) -> torch.Tensor:
+    """A new output tensor, or the caller's one checked: CUDA, dtype, shape, same
+    device and contiguous (the library writes a dense row-major block through its
+    data pointer, so a strided view is refused rather than silently copied)."""
+    if out is None:
+        return torch.empty(shape, dtype=dtype, device=device)
+    if not isinstance(out, torch.Tensor) or not out.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if out.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}")
+    if tuple(out.shape) != tuple(shape):
+        raise ValueError(f"{name} must have shape {tuple(shape)}, got {tuple(out.shape)}")
+    if out.device != device:
+        raise ValueError(f"{name} is on {out.device}, the inputs on {device}")
+    if not out.is_contiguous():
+        raise ValueError(f"{name} must be contiguous (in-place / out= on a strided view is not supported)")
+    return out
+
+
 def cholesky(A: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
     """L = chol(A) (stan_cl_cholesky).  ``out`` may be ``A`` (in place)."""
+    if out is not None and out is A and not A.is_contiguous():
+        raise ValueError("in-place cholesky needs a contiguous A")
     A = _dev_matrix(A, "A")
     n = A.shape[0]
-    L = torch.empty_like(A) if out is None else out
+    L = _out(out, (n, n), A.device)
     with torch.cuda.device(A.device):
         _bind_stream(A.device)
         rc = _check("stan_cl_cholesky", load().stan_cl_cholesky(n, A.data_ptr(), L.data_ptr()))
@@ -148,7 +174,9 @@ def cholesky_adjoint(L: torch.Tensor, Lbar: torch.Tensor, out: torch.Tensor | No
     n = L.shape[0]
     if Lbar.shape[0] != n:
         raise ValueError("L and Lbar differ in shape")
-    Abar = torch.empty_like(L) if out is None else out
+    if Lbar.device != L.device:
+        raise ValueError("L and Lbar are on different devices")
+    Abar = _out(out, (n, n), L.device)
     with torch.cuda.device(L.device):
         _bind_stream(L.device)
         rc = _check("stan_cl_cholesky_adjoint",
@@ -165,7 +193,7 @@ def gp_exp_quad_cov(x: torch.Tensor, alpha: float = 1.0, rho: float = 1.0, jitte
         raise ValueError("x must be a 1-D float64 CUDA tensor")
     x = x.contiguous()
     n = x.shape[0]
-    K = torch.empty((n, n), dtype=torch.float64, device=x.device) if out is None else out
+    K = _out(out, (n, n), x.device)
     with torch.cuda.device(x.device):
         _bind_stream(x.device)
         _check("stan_cl_gp_exp_quad_cov",
@@ -188,7 +216,9 @@ def trsv(L: torch.Tensor, b: torch.Tensor, trans: bool = False, out: torch.Tenso
     L = _dev_matrix(L, "L")
     n = L.shape[0]
     b = _dev_vector(b, "b", n)
-    x = torch.empty_like(b) if out is None else out
+    if b.device != L.device:
+        raise ValueError("L and b are on different devices")
+    x = _out(out, (n,), L.device)
     with torch.cuda.device(L.device):
         _bind_stream(L.device)
         rc = _check("stan_cl_trsv", load().stan_cl_trsv(n, L.data_ptr(), b.data_ptr(), x.data_ptr(),
@@ -230,7 +260,7 @@ def cholesky_batched(A: torch.Tensor, out: torch.Tensor | None = None) -> tuple[
     Returns (L, info) with info the per-matrix LAPACK code (cuda int32)."""
     A = _dev_batch(A, "A")
     batch, n = A.shape[0], A.shape[1]
-    L = torch.empty_like(A) if out is None else out
+    L = _out(out, tuple(A.shape), A.device)
     info = torch.empty(batch, dtype=torch.int32, device=A.device)
     with torch.cuda.device(A.device):
         _bind_stream(A.device)
@@ -246,7 +276,9 @@ def cholesky_adjoint_batched(L: torch.Tensor, Lbar: torch.Tensor,
     L = _dev_batch(L, "L")
     Lbar = _dev_batch(Lbar, "Lbar")
     batch, n = L.shape[0], L.shape[1]
-    Ab = torch.empty_like(L) if out is None else out
+    if tuple(Lbar.shape) != tuple(L.shape) or Lbar.device != L.device:
+        raise ValueError("L and Lbar differ in shape or device")
+    Ab = _out(out, tuple(L.shape), L.device)
     info = torch.empty(batch, dtype=torch.int32, device=L.device)
     with torch.cuda.device(L.device):
         _bind_stream(L.device)
@@ -255,8 +287,25 @@ def cholesky_adjoint_batched(L: torch.Tensor, Lbar: torch.Tensor,
     return Ab, info
 
 
+def _async_args(mats, info):
+    """The async wrappers pass raw pointers: every matrix must already be a square,
+    contiguous float64 CUDA tensor of one shape on one device (no copies are made:
+    a copy would be freed before the enqueued work reads it)."""
+    dev = mats[0][0].device if isinstance(mats[0][0], torch.Tensor) else None
+    for t, name in mats:
+        if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or t.dim() != 2 \
+                or t.shape[0] != t.shape[1] or not t.is_contiguous():
+            raise ValueError(f"{name} must be a square contiguous float64 CUDA tensor")
+        if t.device != dev or t.shape != mats[0][0].shape:
+            raise ValueError(f"{name} differs in shape or device from {mats[0][1]}")
+    if info is not None and (not isinstance(info, torch.Tensor) or not info.is_cuda or info.dtype != torch.int32
+                             or info.numel() < 1 or info.device != dev):
+        raise ValueError("info must be a cuda int32 tensor with >= 1 element on the inputs' device")
+
+
 def cholesky_async(A: torch.Tensor, L: torch.Tensor, info: torch.Tensor | None = None) -> None:
     """Enqueue L = chol(A) without synchronising; ``info`` (cuda int32[1]) gets the status."""
+    _async_args([(A, "A"), (L, "L")], info)
     n = A.shape[0]
     with torch.cuda.device(A.device):
         _bind_stream(A.device)
@@ -266,6 +315,7 @@ def cholesky_async(A: torch.Tensor, L: torch.Tensor, info: torch.Tensor | None =
 
 def cholesky_adjoint_async(L: torch.Tensor, Lbar: torch.Tensor, Abar: torch.Tensor,
                            info: torch.Tensor | None = None) -> None:
+    _async_args([(L, "L"), (Lbar, "Lbar"), (Abar, "Abar")], info)
     n = L.shape[0]
     with torch.cuda.device(L.device):
         _bind_stream(L.device)
@@ -457,6 +507,21 @@ def dist_cholesky_adjoint(L_local: torch.Tensor, W_local: torch.Tensor, n: int) 
             n, 0, L_local.data_ptr(), W_local.data_ptr(), L_local.stride(0)))
 
 
+def dist_trace(n: int, P: int, Q: int, p: int, q: int, adjoint: bool, A_local: torch.Tensor,
+               L_local: torch.Tensor | None = None) -> list:
+    """The NCCL calls rank (p, q) would issue, in order (stan_cl_dist_trace):
+    [(comm_kind, comm_index, op, root, count, stream), ...]."""
+    cap = 1 << 16
+    buf = (ctypes.c_int64 * (6 * cap))()
+    with torch.cuda.device(A_local.device):
+        _bind_stream(A_local.device)
+        m = _check("stan_cl_dist_trace", load().stan_cl_dist_trace(
+            n, P, Q, p, q, int(bool(adjoint)), None if L_local is None else L_local.data_ptr(),
+            A_local.data_ptr(), A_local.stride(0), ctypes.cast(buf, ctypes.c_void_p), cap))
+    assert m <= cap
+    return [tuple(buf[6 * i:6 * i + 6]) for i in range(m)]
+
+
 def kernel_launches() -> int:
     return int(load().stan_cl_kernel_launches())
 
@@ -495,7 +560,26 @@ def profile_read() -> dict:
 
 
 def workspace_bytes(n: int) -> int:
+    """Caller workspace that suffices for every single-matrix call at order n."""
     return int(load().stan_cl_workspace_bytes(n))
+
+
+def batched_workspace_bytes(batch: int, n: int, with_info: bool = True) -> int:
+    return int(load().stan_cl_batched_workspace_bytes(batch, n, int(bool(with_info))))
+
+
+def set_workspace(buf: torch.Tensor | None) -> None:
+    """Hand the library a caller-owned device buffer (stan_cl_set_workspace): every
+    later call carves its device memory from it (None: back to library-owned).
+    The tensor must stay alive until set_workspace(None) / finalize()."""
+    if buf is None:
+        _check("stan_cl_set_workspace", load().stan_cl_set_workspace(None, 0))
+        return
+    if not isinstance(buf, torch.Tensor) or not buf.is_cuda or not buf.is_contiguous():
+        raise ValueError("workspace must be a contiguous CUDA tensor")
+    with torch.cuda.device(buf.device):
+        _check("stan_cl_set_workspace",
+               load().stan_cl_set_workspace(buf.data_ptr(), buf.numel() * buf.element_size()))
 
 
 def finalize() -> None:

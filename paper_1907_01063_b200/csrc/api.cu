@@ -22,6 +22,7 @@
 #include <numeric>
 #include <tuple>
 #include <mutex>
+#include <thread>
 #include <vector>
 
 #include "../../include/stan_cl.h"
@@ -49,6 +50,15 @@ struct State {
   size_t ws_cap = 0;
   int* h_status = nullptr;  // pinned host word for the synchronous calls
   char last_err[256] = {0};
+  // caller-provided workspace (stan_cl_set_workspace): every device buffer the
+  // library needs is carved from it, per call, by a bump pointer
+  char* user_ws = nullptr;
+  size_t user_cap = 0;
+  size_t user_next = 0;  // next free byte of this call
+  int depth = 0;         // nesting of public calls (the GP gradient calls the others)
+  // bumped whenever a workspace buffer moves: cached CUDA graphs captured with an
+  // older generation point at freed memory and are re-captured
+  unsigned long long gen = 1;
 };
 State g;
 
@@ -151,8 +161,34 @@ AdjPlan adj_plan(int64_t n) {
   return p;
 }
 
+constexpr size_t kHdr = 256;  // int header: status word + grid-barrier counters
+
+int user_enomem(size_t need) {
+  snprintf(g.last_err, sizeof(g.last_err), "caller workspace too small: need >= %zu bytes, have %zu", need,
+           g.user_cap);
+  return STAN_CL_ENOMEM;
+}
+
+// Caller workspace: [header + shared workspace of this call][matrix slots ...].
+// The shared workspace sits at offset 0 and may only grow before the first
+// slot of the call is carved (every entry point sizes it first).
+int user_ws(size_t bytes) {
+  bytes = al(std::max(bytes, kHdr));
+  if (bytes <= g.ws_cap) return STAN_CL_OK;
+  if (g.user_next > g.ws_cap) {
+    snprintf(g.last_err, sizeof(g.last_err), "internal: workspace grown after a slot was carved");
+    return STAN_CL_EINVAL;
+  }
+  if (bytes > g.user_cap) return user_enomem(bytes);
+  g.ws_cap = bytes;
+  g.user_next = bytes;
+  return STAN_CL_OK;
+}
+
 int ensure_ws(size_t bytes) {
+  if (g.user_ws) return user_ws(bytes);
   if (g.ws_cap >= bytes && g.ws) return STAN_CL_OK;
+  ++g.gen;
   if (g.ws) {
     CK(cudaStreamSynchronize(g.stream));
     CK(cudaFree(g.ws));
@@ -181,7 +217,22 @@ int ensure_host_status() {
 // cached working matrix `slot` of at least `bytes` (grown with a sync, kept across
 // calls: re-mapping GBs of device memory per call costs 10-1000 ms)
 int ensure_mat(int slot, size_t bytes, double** p) {
+  if (g.user_ws) {
+    if (g.mat[slot] && g.mat_cap[slot] >= bytes) {
+      *p = (double*)g.mat[slot];
+      return STAN_CL_OK;
+    }
+    if (g.user_next < g.ws_cap) g.user_next = g.ws_cap;
+    const size_t need = g.user_next + al(bytes);
+    if (need > g.user_cap) return user_enomem(need);
+    g.mat[slot] = g.user_ws + g.user_next;
+    g.mat_cap[slot] = al(bytes);
+    g.user_next = need;
+    *p = (double*)g.mat[slot];
+    return STAN_CL_OK;
+  }
   if (g.mat_cap[slot] < bytes || !g.mat[slot]) {
+    ++g.gen;
     if (g.mat[slot]) {
       CK(cudaDeviceSynchronize());
       CK(cudaFree(g.mat[slot]));
@@ -201,6 +252,23 @@ int ensure_mat(int slot, size_t bytes, double** p) {
   return STAN_CL_OK;
 }
 
+
+// Scope of one public call: with a caller workspace, the outermost call lays
+// its buffers out afresh from the start of that workspace.
+struct CallScope {
+  CallScope() {
+    if (g.depth++ == 0 && g.user_ws) {
+      g.ws = g.user_ws;
+      g.ws_cap = kHdr;
+      g.user_next = kHdr;
+      for (int i = 0; i < 5; ++i) {
+        g.mat[i] = nullptr;
+        g.mat_cap[i] = 0;
+      }
+    }
+  }
+  ~CallScope() { --g.depth; }
+};
 
 // ------------------------------------------------------------------ forward
 int ensure_side(size_t nevents) {
@@ -574,6 +642,7 @@ struct GraphEntry {
   long long launches = 0;
   int seen = 0;
   bool broken = false;
+  unsigned long long gen = 0;  // workspace generation the graph was captured with
 };
 std::map<GraphKey, GraphEntry> g_graphs;
 
@@ -604,6 +673,14 @@ int run_cached(const GraphKey& key, F&& enqueue) {
     it = g_graphs.emplace(key, GraphEntry{}).first;
   }
   GraphEntry& e = it->second;
+  if (e.exec && e.gen != g.gen) {
+    // a workspace buffer the graph writes through was freed / moved since the
+    // capture: drop it and run eagerly (this also re-sizes the workspace); the
+    // next call re-captures
+    cudaGraphExecDestroy(e.exec);
+    e.exec = nullptr;
+    e.seen = 0;
+  }
   if (e.broken || e.seen++ == 0) return enqueue();
   if (!e.exec) {
     if (!g.cap) CK(cudaStreamCreateWithFlags(&g.cap, cudaStreamNonBlocking));
@@ -632,6 +709,7 @@ int run_cached(const GraphKey& key, F&& enqueue) {
       return enqueue();
     }
     e.launches = captured;
+    e.gen = g.gen;
   }
   CK(cudaGraphLaunch(e.exec, g.stream));
   count_launch((int)e.launches);
@@ -642,12 +720,14 @@ int run_cached(const GraphKey& key, F&& enqueue) {
 extern "C" {
 
 int stan_cl_cholesky_async(int64_t n, const double* A, double* L, int* d_info) {
+  CallScope call_;
   if (n <= 0) return cholesky_enqueue(n, A, L, d_info);
   return run_cached(GraphKey{0, n, {A, L, d_info, nullptr}, g.nb, 0},
                     [&] { return cholesky_enqueue(n, A, L, d_info); });
 }
 
 int stan_cl_cholesky(int64_t n, const double* A, double* L) {
+  CallScope call_;
   int rc = stan_cl_cholesky_async(n, A, L, nullptr);
   if (rc || n == 0) return rc;
   return read_status();
@@ -655,18 +735,21 @@ int stan_cl_cholesky(int64_t n, const double* A, double* L) {
 
 int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_bar, double* A_bar,
                                    int* d_info) {
+  CallScope call_;
   if (n <= 0) return adjoint_enqueue(n, L, L_bar, A_bar, d_info);
   return run_cached(GraphKey{1, n, {L, L_bar, A_bar, d_info}, g.adj_nb, 0},
                     [&] { return adjoint_enqueue(n, L, L_bar, A_bar, d_info); });
 }
 
 int stan_cl_cholesky_adjoint(int64_t n, const double* L, const double* L_bar, double* A_bar) {
+  CallScope call_;
   int rc = stan_cl_cholesky_adjoint_async(n, L, L_bar, A_bar, nullptr);
   if (rc || n == 0) return rc;
   return read_status();
 }
 
 int stan_cl_trsv(int64_t n, const double* L, const double* b, double* x, int trans) {
+  CallScope call_;
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!L || !b || !x) return STAN_CL_EINVAL;
@@ -687,6 +770,7 @@ int stan_cl_trsv(int64_t n, const double* L, const double* b, double* x, int tra
 
 int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alpha, double rho, double sigma,
                          double* out, double* y_bar) {
+  CallScope call_;
   if (n < 0) return STAN_CL_EINVAL;
   if (n > 0 && (!x || !y || !out)) return STAN_CL_EINVAL;
   if (!(rho != 0.0) || !(rho - rho == 0.0) || !(alpha - alpha == 0.0) || !(sigma - sigma == 0.0))
@@ -698,14 +782,14 @@ int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alp
   }
   const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
   double *K = nullptr, *W = nullptr;
-  int rc = ensure_mat(2, bytes, &K);
+  // size the shared workspace for the adjoint first: growing it later would
+  // move the status word the kernels below are given
+  int rc = ensure_ws(adj_plan(n).total);
   if (rc) return rc;
+  if ((rc = ensure_mat(2, bytes, &K))) return rc;
   if ((rc = ensure_mat(3, bytes, &W))) return rc;
   VecScratch v;
   if ((rc = vec_scratch(n, &v))) return rc;
-  // size the shared workspace for the adjoint now: growing it later would
-  // move the status word the kernels below are given
-  if ((rc = ensure_ws(adj_plan(n).total))) return rc;
   // K = SE + sigma^2 I;  L = chol(K) in place (the hot path's forward)
   CK(se_cov(n, x, alpha, rho, sigma * sigma, K, st));
   if ((rc = cholesky_enqueue(n, K, K, nullptr))) return rc;
@@ -726,6 +810,7 @@ int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alp
 
 // ---- NEXT-4: batched small matrices ----------------------------------------
 int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* L, int* info) {
+  CallScope call_;
   if (batch < 0 || n < 0 || n > NB) return STAN_CL_EINVAL;
   if (batch == 0 || n == 0) return STAN_CL_OK;
   if (!A || !L) return STAN_CL_EINVAL;
@@ -753,6 +838,7 @@ int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* 
 
 int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, const double* L_bar,
                                      double* A_bar, int* info) {
+  CallScope call_;
   if (batch < 0 || n < 0 || n > NB) return STAN_CL_EINVAL;
   if (batch == 0 || n == 0) return STAN_CL_OK;
   if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
@@ -853,11 +939,47 @@ int cholesky_host_enqueue(int64_t n, const double* A, double* L) {
   return STAN_CL_OK;
 }
 
+// +0.0 into the strict upper triangle of a host output outside the 128 x 128
+// diagonal tiles (the streamed copies write the lower rectangles and the
+// diagonal tiles, include/stan_cl.h), by host threads while the device works:
+// row r gets columns [end of r's 128-row tile, n), disjoint from every copy.
+struct HostUpperZero {
+  std::vector<std::thread> th;
+  HostUpperZero(double* out, int64_t n) {
+    if (n <= NB) return;
+    const unsigned hc = std::thread::hardware_concurrency();
+    const int T = (int)std::max(1u, std::min(8u, hc ? hc / 2 : 1u));
+    // rows split by equal zero-fill volume: row r has about n - r entries to fill
+    std::vector<int64_t> cut{0};
+    const double total = 0.5 * (double)n * (double)n;
+    int64_t r = 0;
+    double acc = 0;
+    for (int t = 1; t < T; ++t) {
+      while (r < n && acc < total * t / T) acc += (double)(n - r++);
+      cut.push_back(r);
+    }
+    cut.push_back(n);
+    for (int t = 0; t < T; ++t)
+      th.emplace_back([=] {
+        for (int64_t i = cut[t]; i < cut[t + 1]; ++i) {
+          const int64_t c0 = std::min(n, (i / NB + 1) * NB);
+          if (c0 < n) memset(out + i * n + c0, 0, (size_t)(n - c0) * sizeof(double));
+        }
+      });
+  }
+  ~HostUpperZero() {
+    for (auto& t : th) t.join();
+  }
+};
+
 int stan_cl_cholesky_host(int64_t n, const double* A, double* L) {
+  CallScope call_;
   PdlOff pdl_off_;
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!A || !L) return STAN_CL_EINVAL;
+  if (A != L && ranges_overlap(A, L, (size_t)n * (size_t)n * sizeof(double))) return STAN_CL_EINVAL;
+  HostUpperZero zero_(L, n);
   int rc = run_cached(GraphKey{2, n, {A, L, nullptr, nullptr}, g.nb, 0},
                       [&] { return cholesky_host_enqueue(n, A, L); });
   if (rc) return rc;
@@ -911,10 +1033,15 @@ int adjoint_host_enqueue(int64_t n, const double* L, const double* L_bar, double
 }
 
 int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar) {
+  CallScope call_;
   PdlOff pdl_off_;
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
+  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  if (ranges_overlap(L, A_bar, bytes)) return STAN_CL_EINVAL;
+  if (L_bar != A_bar && ranges_overlap(L_bar, A_bar, bytes)) return STAN_CL_EINVAL;
+  HostUpperZero zero_(A_bar, n);
   int rc = run_cached(GraphKey{3, n, {L, L_bar, A_bar, nullptr}, g.adj_nb, 0},
                       [&] { return adjoint_host_enqueue(n, L, L_bar, A_bar); });
   if (rc) return rc;
@@ -946,18 +1073,72 @@ int stan_cl_set_adjoint_block_size(int nb) {
   return STAN_CL_EINVAL;
 }
 
+// Bytes of caller workspace the single-GPU entry points need at order n, laid
+// out as CallScope / ensure_ws / ensure_mat carve them (16-byte aligned
+// buffers assumed: an unaligned caller buffer takes the padded path, which
+// needs the padded matrices below even when n divides the block).
 size_t stan_cl_workspace_bytes(int64_t n) {
-  if (n <= 0) return 0;
+  if (n <= 0) return kHdr;
   const AdjPlan p = adj_plan(n);
-  size_t pad = (p.N == n) ? 0 : 2 * (size_t)p.N * p.N * sizeof(double);
-  return p.total + pad;
+  const int64_t OB = g.nb ? g.nb : fwd_outer_block(n);
+  const size_t Nf = (size_t)round_up(n, OB), Na = (size_t)p.N, nn = (size_t)n;
+  const size_t mat_f = al(Nf * Nf * sizeof(double)), mat_a = al(Na * Na * sizeof(double));
+  const size_t vec = al((2 * nn + gp_hyper_scratch_doubles() + 8) * sizeof(double) + sizeof(int) * (nn / 64 + 4));
+  const size_t adj_ws = al(std::max(p.total, kHdr));
+  size_t need = kHdr + ((Nf == nn) ? 0 : mat_f);                     // cholesky
+  need = std::max(need, adj_ws + ((Na == nn) ? 0 : 2 * mat_a));     // cholesky_adjoint
+  need = std::max(need, kHdr + mat_f);                               // cholesky_host
+  need = std::max(need, adj_ws + 2 * mat_a);                         // cholesky_adjoint_host
+  need = std::max(need, kHdr + vec);                                 // trsv
+  // gp_lpdf_grad: K, W (n x n), the O(n) scratch, then the padded matrices of
+  // the inner cholesky / adjoint when n is not a block multiple
+  const size_t pads = std::max((Nf == nn) ? 0 : mat_f, (Na == nn) ? 0 : 2 * mat_a);
+  need = std::max(need, adj_ws + 2 * al(nn * nn * sizeof(double)) + vec + pads);
+  return need;
+}
+
+size_t stan_cl_batched_workspace_bytes(int64_t batch, int64_t n, int with_info) {
+  if (batch <= 0 || n <= 0) return kHdr;
+  const size_t inf = with_info ? 0 : al(sizeof(int) * (size_t)batch);
+  if (n <= 32) return kHdr + inf;
+  const size_t chunk = (size_t)std::min<int64_t>(batch, 4096);
+  return kHdr + al(sizeof(double) * 4 * chunk * (size_t)NB * NB) + inf;
+}
+
+int stan_cl_set_workspace(void* dev_ptr, size_t bytes) {
+  if (g.depth) return STAN_CL_EINVAL;
+  if (dev_ptr && (((uintptr_t)dev_ptr & (kAlign - 1)) != 0 || bytes < kHdr)) return STAN_CL_EINVAL;
+  // drop every library-owned buffer (the caller's memory bound is the point)
+  CK(cudaDeviceSynchronize());
+  clear_graphs();
+  if (!g.user_ws && g.ws) CK(cudaFree(g.ws));
+  for (int i = 0; i < 5; ++i)
+    if (!g.user_ws && g.mat[i]) CK(cudaFree(g.mat[i]));
+  for (int i = 0; i < 5; ++i) {
+    g.mat[i] = nullptr;
+    g.mat_cap[i] = 0;
+  }
+  g.ws = nullptr;
+  g.ws_cap = 0;
+  ++g.gen;
+  g.user_ws = (char*)dev_ptr;
+  g.user_cap = dev_ptr ? bytes : 0;
+  g.user_next = 0;
+  if (dev_ptr) {
+    // the header (status word, grid-barrier counters) starts at zero; the
+    // kernels leave the counters at zero
+    CK(cudaMemset(dev_ptr, 0, kHdr));
+    g.ws = g.user_ws;
+    g.ws_cap = kHdr;
+  }
+  return STAN_CL_OK;
 }
 
 const char* stan_cl_status_string(int status) {
   switch (status) {
     case STAN_CL_OK: return "ok";
     case STAN_CL_EINVAL: return "invalid argument";
-    case STAN_CL_ENOMEM: return "device workspace allocation failed";
+    case STAN_CL_ENOMEM: return g.last_err[0] ? g.last_err : "device workspace allocation failed";
     case STAN_CL_ECUDA: return g.last_err[0] ? g.last_err : "CUDA error";
     case STAN_CL_ENCCL: return "NCCL error";
     default: return status > 0 ? "numerical failure (not positive definite / bad diagonal)" : "unknown status";
@@ -998,7 +1179,7 @@ int stan_cl_finalize(void) {
   }
   if (g.ws) {
     cudaStreamSynchronize(g.stream);
-    cudaFree(g.ws);
+    if (!g.user_ws) cudaFree(g.ws);
     g.ws = nullptr;
     g.ws_cap = 0;
   }
@@ -1011,10 +1192,13 @@ int stan_cl_finalize(void) {
   for (cudaEvent_t e : g.xev) cudaEventDestroy(e);
   g.xev.clear();
   for (int i = 0; i < 5; ++i) {
-    if (g.mat[i]) cudaFree(g.mat[i]);
+    if (g.mat[i] && !g.user_ws) cudaFree(g.mat[i]);
     g.mat[i] = nullptr;
     g.mat_cap[i] = 0;
   }
+  g.user_ws = nullptr;  // the caller's workspace is never freed by the library
+  g.user_cap = g.user_next = 0;
+  ++g.gen;
   if (g.h2d) {
     cudaStreamDestroy(g.h2d);
     g.h2d = nullptr;
@@ -1183,6 +1367,20 @@ struct Rank {
   double* lrow(int b) const { return base + pl.lrow + b * pl.lrow_sz; }
 };
 
+// Collective trace (stan_cl_dist_trace): when set, the real (one rank per
+// process) path records each NCCL call it would issue -- communicator, op,
+// root, count, stream -- in host issue order instead of calling NCCL.
+struct TraceEntry {
+  int64_t comm_kind;  // 0 = row communicator, 1 = column, 2 = world
+  int64_t comm_index; // p for a row, q for a column, 0 for the world
+  int64_t op;         // 0 = broadcast, 1 = reduce (sum), 2 = all-reduce (max)
+  int64_t root;       // root's index within the communicator (-1: none)
+  int64_t count;      // elements
+  int64_t stream;     // 0 = library stream, 1 = side (lookahead) stream, 2 = other
+};
+std::vector<TraceEntry>* g_trace = nullptr;
+int64_t stream_role(cudaStream_t st) { return st == g.stream ? 0 : (st == g.side ? 1 : 2); }
+
 struct Comm {
   bool sim;
   int P, Q;
@@ -1210,6 +1408,10 @@ struct Comm {
     Rank& me = rs[0];
     if ((row ? me.p : me.q) != idx) return STAN_CL_OK;
     double* b = ptr(me);
+    if (g_trace) {
+      g_trace->push_back(TraceEntry{row ? 0 : 1, idx, 0, root, (int64_t)count, stream_role(st)});
+      return STAN_CL_OK;
+    }
     if (g_nccl.broadcast(b, b, count, ncclFloat64, root, row ? g_dist.rowc : g_dist.colc, st) != ncclSuccess)
       return STAN_CL_ENCCL;
     return STAN_CL_OK;
@@ -1230,6 +1432,10 @@ struct Comm {
     Rank& me = rs[0];
     if (me.q != q) return STAN_CL_OK;
     double* b = ptr(me);
+    if (g_trace) {
+      g_trace->push_back(TraceEntry{1, q, 1, root, (int64_t)count, stream_role(st)});
+      return STAN_CL_OK;
+    }
     if (g_nccl.reduce(b, b, count, ncclFloat64, ncclSum, root, g_dist.colc, st) != ncclSuccess) return STAN_CL_ENCCL;
     return STAN_CL_OK;
   }
@@ -1565,9 +1771,9 @@ int dist_run(bool adjoint, int64_t n, int P, int Q, bool sim, int p0, int q0, co
     total += plans.back().total;
   }
   double* buf = nullptr;
-  int rc = ensure_mat(0, std::max<size_t>(total, 1) * sizeof(double), &buf);
+  int rc = ensure_ws(al(sizeof(int) * 64) + NB * NB * sizeof(double));
   if (rc) return rc;
-  rc = ensure_ws(al(sizeof(int) * 64) + NB * NB * sizeof(double));
+  rc = ensure_mat(0, std::max<size_t>(total, 1) * sizeof(double), &buf);
   if (rc) return rc;
   int* status = (int*)g.ws;
   CK(cudaMemsetAsync(status, 0, sizeof(int), g.stream));
@@ -1637,6 +1843,7 @@ static int dist_status_allreduce(int rc) {
 }
 
 int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local) {
+  CallScope call_;
   if (!g_dist.comm || (nb != 0 && nb != (int)DB)) return STAN_CL_EINVAL;
   double* Ws[1] = {A_local};
   const int p = g_dist.rank / g_dist.Q, q = g_dist.rank % g_dist.Q;
@@ -1646,12 +1853,32 @@ int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local) 
 
 int stan_cl_dist_cholesky_adjoint(int64_t n, int nb, const double* L_local, double* Lbar_to_Abar_local,
                                   int64_t ld_local) {
+  CallScope call_;
   if (!g_dist.comm || (nb != 0 && nb != (int)DB)) return STAN_CL_EINVAL;
   const double* Ls[1] = {L_local};
   double* Ws[1] = {Lbar_to_Abar_local};
   const int p = g_dist.rank / g_dist.Q, q = g_dist.rank % g_dist.Q;
   int rc = dist_run(true, n, g_dist.P, g_dist.Q, false, p, q, Ls, Ws, ld_local);
   return n == 0 ? rc : dist_status_allreduce(rc);
+}
+
+int stan_cl_dist_trace(int64_t n, int P, int Q, int p, int q, int adjoint, const double* L_local,
+                       double* A_local, int64_t ld_local, int64_t* out, int64_t max_entries) {
+  CallScope call_;
+  if (P < 1 || Q < 1 || p < 0 || p >= P || q < 0 || q >= Q || max_entries < 0 || (max_entries && !out))
+    return STAN_CL_EINVAL;
+  std::vector<TraceEntry> tr;
+  g_trace = &tr;
+  const double* Ls[1] = {L_local};
+  double* Ws[1] = {A_local};
+  int rc = dist_run(adjoint != 0, n, P, Q, false, p, q, adjoint ? Ls : nullptr, Ws, ld_local);
+  g_trace = nullptr;
+  if (rc) return rc;
+  if (n > 0) tr.push_back(TraceEntry{2, 0, 2, -1, 1, 0});  // dist_status_allreduce
+  CK(cudaStreamSynchronize(g.stream));
+  const int64_t m = std::min<int64_t>((int64_t)tr.size(), max_entries);
+  for (int64_t i = 0; i < m; ++i) memcpy(out + 6 * i, &tr[i], sizeof(TraceEntry));
+  return (int)tr.size();
 }
 
 int stan_cl_dist_finalize(void) {
@@ -1679,6 +1906,7 @@ int stan_cl_gp_exp_quad_cov_cols(int64_t n, const double* x, double alpha, doubl
 }
 
 int stan_cl_dist_sim2_cholesky(int64_t n, int P, int Q, double* const* A_locals, int64_t ld_local) {
+  CallScope call_;
   if (!A_locals || P < 1 || Q < 1) return STAN_CL_EINVAL;
   int rc = dist_run(false, n, P, Q, true, 0, 0, nullptr, A_locals, ld_local);
   return (rc || n == 0) ? rc : read_status();
@@ -1686,6 +1914,7 @@ int stan_cl_dist_sim2_cholesky(int64_t n, int P, int Q, double* const* A_locals,
 
 int stan_cl_dist_sim2_cholesky_adjoint(int64_t n, int P, int Q, const double* const* L_locals,
                                        double* const* W_locals, int64_t ld_local) {
+  CallScope call_;
   if (!L_locals || !W_locals || P < 1 || Q < 1) return STAN_CL_EINVAL;
   int rc = dist_run(true, n, P, Q, true, 0, 0, L_locals, W_locals, ld_local);
   return (rc || n == 0) ? rc : read_status();

@@ -123,4 +123,15 @@ struct Status {
   int info;
 };
 
+// CTA-uniform "the status word is set" test.  Every thread of the CTA must
+// reach it (call it first, after pdl_enter).  Thread 0 reads the word once and
+// __syncthreads_or hands its answer to every thread, so a status write from
+// another stream landing while the CTA starts (the lookahead POTRF, the host
+// path's check_diag) cannot send some warps home while others wait on a
+// barrier.  Kernels that synchronise ACROSS CTAs (grid barriers, ready flags)
+// must not exit early at all: a per-CTA snapshot is not grid-uniform.
+__device__ __forceinline__ bool cta_status_set(const int* status) {
+  return __syncthreads_or(threadIdx.x == 0 && status != nullptr && *(volatile const int*)status != 0) != 0;
+}
+
 }  // namespace stancl

@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(CF::THREADS, CF::MIN_CTAS) gemm_dmma_kernel(Ge
   using TA = Tile<BM, A_KMAJ, BK>;
   using TB = Tile<BN, B_KMAJ, BK>;
   pdl_enter();
-  if (p.status && *p.status != 0) return;
+  if (cta_status_set(p.status)) return;
   extern __shared__ __align__(16) double smem[];
   double* sA = smem;
   double* sB = smem + STAGES * TA::ELEMS;

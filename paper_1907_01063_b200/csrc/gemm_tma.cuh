@@ -246,7 +246,7 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
   using SB = Slab<BN, B_KMAJ, BKS>;
   using SM = Smem<CF, A_KMAJ, B_KMAJ>;
   pdl_enter();
-  if (p.status && *p.status != 0) return;
+  if (cta_status_set(p.status)) return;
   if ((int)blockIdx.x >= nitems) return;
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   // 1024-B aligned slab base (128B-swizzle atoms) as an OFFSET from the shared

@@ -42,7 +42,9 @@ template <bool TRANS>
 __global__ void __launch_bounds__(256) trsv_kernel(const double* __restrict__ L, int64_t ld, int64_t n,
                                                    const double* b, double* x, int* flags, int* ticket,
                                                    const int* status) {
-  if (*status != 0) return;
+  // no early exit on a set status: the CTAs wait on each other's ready flags, so a
+  // per-CTA decision could strand a waiter (the result is unspecified on failure)
+  (void)status;
   __shared__ double Ld[TV][TV + 1];
   __shared__ double rc[TV];
   __shared__ double part[8][TV];
@@ -203,7 +205,7 @@ cudaError_t trsv(const double* L, int64_t ld, int64_t n, const double* b, double
 // lp = -1/2 z.z - sum log L_ii - n/2 log(2 pi), one CTA, fixed-order tree
 __global__ void __launch_bounds__(256) gp_lp_kernel(const double* L, int64_t ld, int64_t n, const double* z,
                                                     double* out, const int* status) {
-  if (*status != 0) return;
+  if (cta_status_set(status)) return;
   __shared__ double s_zz[256], s_ld[256];
   double zz = 0.0, lg = 0.0;
   for (int64_t i = threadIdx.x; i < n; i += 256) {
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(256) gp_lp_kernel(const double* L, int64_t ld,
 // L_bar = tril(a z^T) - diag(1 / L_ii), lower triangle only (d lp / d L)
 __global__ void gp_lbar_kernel(const double* L, int64_t ld, int64_t n, const double* a, const double* z, double* W,
                                int64_t ldw, const int* status) {
-  if (*status != 0) return;
+  if (cta_status_set(status)) return;
   for (int64_t i = blockIdx.x; i < n; i += gridDim.x) {
     const double ai = a[i];
     double* Wi = W + i * ldw;
@@ -244,7 +246,7 @@ __global__ void __launch_bounds__(256) gp_hyper_partial_kernel(const double* A, 
                                                                const double* x, double alpha, double rho,
                                                                double sigma, double* partial,
                                                                const int* status) {
-  if (*status != 0) return;
+  if (cta_status_set(status)) return;
   __shared__ double s[3][256];
   const double c = -0.5 / (rho * rho), ra = 2.0 * alpha, rr = alpha * alpha / (rho * rho * rho);
   double g0 = 0.0, g1 = 0.0, g2 = 0.0;
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(256) gp_hyper_partial_kernel(const double* A, 
 }
 
 __global__ void gp_hyper_final_kernel(const double* partial, int nparts, double* out, const int* status) {
-  if (*status != 0) return;
+  if (cta_status_set(status)) return;
   if (threadIdx.x < 3) {
     double v = 0.0;
     for (int p = 0; p < nparts; ++p) v += partial[p * 3 + threadIdx.x];
@@ -283,7 +285,7 @@ __global__ void gp_hyper_final_kernel(const double* partial, int nparts, double*
 }
 
 __global__ void negate_kernel(const double* a, double* y, int64_t n, const int* status) {
-  if (*status != 0) return;
+  if (cta_status_set(status)) return;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     y[i] = -a[i];
 }

@@ -50,7 +50,7 @@ def test_binding_signatures_cover_header(lib_path):
     assert lib.stan_cl_set_block_size(256) == 0 and lib.stan_cl_get_block_size() == 256
     assert lib.stan_cl_set_block_size(0) == 0 and lib.stan_cl_get_block_size() == 0
     assert lib.stan_cl_set_block_size(96) == -1
-    assert lib.stan_cl_workspace_bytes(0) == 0
+    assert lib.stan_cl_workspace_bytes(0) == 256         # the status header alone
     assert lib.stan_cl_workspace_bytes(16384) > 16384 * 128 * 8
 
 

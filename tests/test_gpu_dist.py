@@ -222,7 +222,10 @@ def _free_port():
     return p
 
 
-def _nccl_worker(rank, world, port, n, q):
+def _nccl_worker(rank, world, port, n, P, Q, q):
+    """One rank of a real NCCL run on a P x Q grid: forward on the SE covariance,
+    adjoint on the ORACLE's L (the A_bar bar is for the same L bits on both sides;
+    no oracle input comes from the CUDA path)."""
     import sys
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     import torch.distributed as dist
@@ -231,13 +234,22 @@ def _nccl_worker(rank, world, port, n, q):
     dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world,
                             device_id=torch.device("cuda", rank))
     try:
-        sc.dist_init_from_torch()
+        sc.dist_init_from_torch(None, P, Q)
+        p_, q_ = divmod(rank, Q)
         K = torch.from_numpy(se(n)).cuda()
-        loc = sc.dist_scatter(K, world, rank).contiguous()
+        loc = sc.dist_scatter2(K, P, Q, p_, q_).contiguous()
         rc = sc.dist_cholesky(loc, n)
-        gathered = [None] * world
-        dist.all_gather_object(gathered, loc.cpu())
-        q.put((rank, rc, [g.numpy() for g in gathered] if rank == 0 else None))
+        Lo = torch.from_numpy(oracle.cholesky(se(n))).cuda()
+        Lloc = sc.dist_scatter2(Lo, P, Q, p_, q_).contiguous()
+        W = sc.dist_scatter2(torch.from_numpy(inputs.lbar(n)).cuda(), P, Q, p_, q_).contiguous()
+        rca = sc.dist_cholesky_adjoint(Lloc, W, n)
+        gl, gw = [None] * world, [None] * world
+        dist.all_gather_object(gl, loc.cpu())
+        dist.all_gather_object(gw, W.cpu())
+        q.put((rank, rc, rca, [g.numpy() for g in gl] if rank == 0 else None,
+               [g.numpy() for g in gw] if rank == 0 else None))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, "error", repr(e), None, None))
     finally:
         sc.load().stan_cl_dist_finalize()
         dist.destroy_process_group()
@@ -259,8 +271,10 @@ def _nccl_single_worker(port, n, q):
         loc = sc.dist_scatter2(K, 1, 1, 0, 0).contiguous()
         rc = sc.dist_cholesky(loc, n)
         L = loc.cpu().numpy()
+        Lo = torch.from_numpy(oracle.cholesky(se(n))).cuda()
+        Lloc = sc.dist_scatter2(Lo, 1, 1, 0, 0).contiguous()
         W = torch.from_numpy(inputs.lbar(n)).cuda().contiguous()
-        rca = sc.dist_cholesky_adjoint(loc, W, n)
+        rca = sc.dist_cholesky_adjoint(Lloc, W, n)
         A = sc.load().stan_cl_dist_init(1, 0, None, 1, 1)        # already initialised / bad id
         q.put((grid, rc, rca, L, W.cpu().numpy(), A))
     except Exception as e:  # noqa: BLE001
@@ -283,23 +297,91 @@ def test_nccl_single_rank(sc):
     grid, rc, rca, L, Ab, again = res
     assert grid == (1, 1) and rc == 0 and rca == 0 and again == -1
     K = se(n)
-    check_lower_and_tiles(L, oracle.cholesky(K), 1e-11)
-    check_lower_and_tiles(Ab, oracle.cholesky_adjoint(L, inputs.lbar(n)), 1e-9)
+    Lo = oracle.cholesky(K)
+    check_lower_and_tiles(L, Lo, 1e-11)
+    check_lower_and_tiles(Ab, oracle.cholesky_adjoint(Lo, inputs.lbar(n)), 1e-9)
 
 
-@pytest.mark.skipif(not torch.cuda.is_available() or torch.cuda.device_count() < 2, reason="needs 2 GPUs")
-def test_nccl_ranks(sc):
+@pytest.mark.parametrize("P,Q", [(1, 2), (2, 1), (2, 2)])
+def test_nccl_ranks(sc, P, Q):
+    """Real ncclBroadcast / ncclReduce on P x Q ranks (one GPU each): forward and
+    adjoint against the oracle."""
     import torch.multiprocessing as mp
-    world, n = 2, 1024
+    world, n = P * Q, 1536
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
     port = _free_port()
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_nccl_worker, args=(r, world, port, n, q)) for r in range(world)]
+    ps = [ctx.Process(target=_nccl_worker, args=(r, world, port, n, P, Q, q)) for r in range(world)]
     for p in ps:
         p.start()
-    res = dict((r, (rc, g)) for r, rc, g in [q.get(timeout=300) for _ in range(world)])
+    res = {}
+    for _ in range(world):
+        r, rc, rca, gl, gw = q.get(timeout=300)
+        res[r] = (rc, rca, gl, gw)
     for p in ps:
         p.join(timeout=60)
-    assert all(rc == 0 for rc, _ in res.values())
-    got = sc.dist_gather([torch.from_numpy(g) for g in res[0][1]], n).numpy()
-    check_lower_and_tiles(got, oracle.cholesky(se(n)), 1e-11)
+    assert all(v[0] == 0 and v[1] == 0 for v in res.values()), res
+    L = sc.dist_gather2([torch.from_numpy(g) for g in res[0][2]], n, P, Q).numpy()
+    Ab = sc.dist_gather2([torch.from_numpy(g) for g in res[0][3]], n, P, Q).numpy()
+    K = se(n)
+    Lo = oracle.cholesky(K)
+    check_lower_and_tiles(L, Lo, 1e-11)
+    check_lower_and_tiles(Ab, oracle.cholesky_adjoint(Lo, inputs.lbar(n)), 1e-9)
+
+
+def _trace_all(sc, n, P, Q, adjoint):
+    """Every rank's recorded NCCL sequence (stan_cl_dist_trace), run one rank at a
+    time on this device through the real per-rank code path."""
+    out = {}
+    for r in range(P * Q):
+        p, q = divmod(r, Q)
+        rows, cols = sc.dist_local_shape(n, P, Q, p, q)
+        A = torch.zeros((max(rows, 1), max(cols, B)), dtype=torch.float64, device="cuda")
+        L = torch.zeros_like(A) if adjoint else None
+        out[(p, q)] = sc.dist_trace(n, P, Q, p, q, adjoint, A, L)
+    return out
+
+
+@pytest.mark.parametrize("P,Q", [(1, 2), (2, 1), (2, 2), (2, 4), (4, 2), (3, 3)])
+@pytest.mark.parametrize("adjoint", [False, True])
+def test_collective_schedule_consistent(sc, P, Q, adjoint):
+    """Deadlock / count check of the multi-GPU schedule:
+    every member of each row, column and world communicator must issue the same
+    sequence of (op, root, count, stream) on it, as NCCL requires; roots are
+    members; every broadcast moves whole 256 x 256 tiles."""
+    n = 256 * 11                                       # 11 block rows: ragged over every grid
+    tr = _trace_all(sc, n, P, Q, adjoint)
+    ranks = sorted(tr)
+    seqs = {}
+    for (p, q) in ranks:
+        for kind, idx, op, root, cnt, st in tr[(p, q)]:
+            if kind == 0:
+                assert idx == p
+                assert 0 <= root < Q
+            elif kind == 1:
+                assert idx == q
+                assert 0 <= root < P
+            seqs.setdefault((kind, idx), {}).setdefault((p, q), []).append((op, root, cnt, st))
+            if op == 0:
+                assert cnt > 0 and cnt % B == 0
+    # every member of a communicator appears with an identical sequence
+    for (kind, idx), per in seqs.items():
+        members = [(idx, q) for q in range(Q)] if kind == 0 else \
+                  [(p, idx) for p in range(P)] if kind == 1 else ranks
+        assert sorted(per) == sorted(members), (kind, idx, sorted(per))
+        first = per[members[0]]
+        for m in members[1:]:
+            assert per[m] == first, (kind, idx, m)
+    # there is real traffic: forward broadcasts panels on both kinds of
+    # communicator when both grid dimensions exceed 1; the adjoint reduces over
+    # process columns when P > 1
+    ops = [e for v in tr.values() for e in v]
+    if Q > 1:
+        assert any(e[0] == 0 and e[2] == 0 for e in ops)
+    if P > 1:
+        assert any(e[0] == 1 and e[2] == 0 for e in ops)
+        if adjoint:
+            assert any(e[2] == 1 for e in ops)
+    assert sum(1 for e in ops if e[0] == 2) == P * Q   # one status all-reduce per rank

@@ -10,12 +10,20 @@ n=16384, ~35 min for the adjoint), so parity is checked
     adjoint of that block, zeros elsewhere), and a closed-form evaluation of
     A_bar = Phi(G + G^T), G = L^-T Phi(L^T L_bar) L^-1 at sampled entries for an
     L_bar supported on the last rows (rank-r M = L^T L_bar, O(r n) per entry).
-Inputs to the adjoint come from LAPACK (numpy.linalg.cholesky), never from the
+  * A_bar at n = 8192 and 16384 against SAMPLED oracle A_bar
+    (tests/golden/oracle_adj_se_n{8192,16384}.npz, tools/make_golden_adjoint.py),
+    the GPU fed the oracle's own L bits (rebuilt by the bit-identical
+    multi-threaded oracle.cholesky_par, SHA-256 checked);
+  * the integer-exact adjoint family at n = 16384, full matrix, bit for bit.
+Other adjoint inputs come from LAPACK (numpy.linalg.cholesky), never from the
 CUDA path.
 """
 from __future__ import annotations
 
+import hashlib
+import json
 import os
+import sys
 
 import numpy as np
 import pytest
@@ -149,3 +157,54 @@ def test_adjoint_trailing_rows_closed_form_16384(sc, lapack_L):
     for a, b in picks:
         want = _adjoint_entry(L, rows, Wr, a, b)
         assert abs(got[a, b] - want) <= 1e-9 * max(abs(want), scale), (a, b, got[a, b], want)
+
+
+@pytest.mark.parametrize("n", [8192, 16384])
+def test_adjoint_matches_sampled_oracle(sc, n):
+    """A_bar at the bench sizes against the oracle's sampled A_bar
+    (tests/golden/oracle_adj_se_n{n}.npz, tools/make_golden_adjoint.py: oracle K
+    -> oracle L -> oracle adjoint with L_bar = inputs.lbar(n), seed 43).  The GPU
+    adjoint is fed the oracle's own L bits (rebuilt by oracle.cholesky_par and
+    checked against the stored SHA-256), since the 1e-9 bar is stated for the
+    same L on both sides (BASELINE.json north_star)."""
+    g = np.load(os.path.join(GOLD, f"oracle_adj_se_n{n}.npz"))
+    assert int(g["n"]) == n and int(g["x_seed"]) == inputs.X_SEED and int(g["lbar_seed"]) == inputs.LBAR_SEED
+    L = oracle.cholesky_par(oracle_K(n))
+    assert hashlib.sha256(L.tobytes()).hexdigest() == str(g["L_sha256"])
+    Ld = torch.from_numpy(L).cuda()
+    del L
+    W = torch.from_numpy(inputs.lbar(n, seed=int(g["lbar_seed"]))).cuda()
+    sc.cholesky_adjoint(Ld, W, out=W)                 # in place, the bench's aliasing
+    del Ld
+    rows = torch.from_numpy(g["rows"]).cuda()
+    got_rows = W[rows].cpu().numpy()
+    got_vals = W[torch.from_numpy(g["ii"]).cuda(), torch.from_numpy(g["jj"]).cuda()].cpu().numpy()
+    got_diag = torch.diagonal(W).cpu().numpy()
+    want = np.concatenate([g["row_vals"].ravel(), g["vals"], g["diag"]])
+    got = np.concatenate([got_rows.ravel(), got_vals, got_diag])
+    err = float(np.linalg.norm(got - want) / np.linalg.norm(want))
+    print(json.dumps({"test": "adjoint_vs_sampled_oracle", "n": n, "rel_frobenius_sample": err,
+                      "samples": int(want.size)}), file=sys.stderr)
+    assert err <= 1e-9, err
+    # exact zeros above the diagonal of the sampled rows
+    for r, row in zip(g["rows"], got_rows):
+        assert np.all(row[int(r) + 1:] == 0.0)
+    del W
+    torch.cuda.empty_cache()
+
+
+def test_adjoint_integer_exact_16384(sc):
+    """Full-matrix bit-exact adjoint at the headline size: banded (2) unit-lower
+    +-1 L with an integer L_bar keeps every intermediate a multiple of 1/2 below
+    2^53, so every correct blocking returns the same bits (SURVEY.md §8(c));
+    the reference is the paper's blocked listing in numpy
+    (tests/paper_blocked.py, pinned bit-exact to the oracle in test_oracle.py)."""
+    from tests.paper_blocked import blocked_adjoint
+    n = 16384
+    Li = inputs.unit_lower_pm1(n, seed=3, band=2)
+    Wi = inputs.int_lbar(n, seed=4)
+    want = blocked_adjoint(Li, Wi, 1024)
+    assert np.all(np.abs(want) < 2.0 ** 52)
+    W = torch.from_numpy(Wi).cuda()
+    sc.cholesky_adjoint(torch.from_numpy(Li).cuda(), W, out=W)
+    assert np.array_equal(W.cpu().numpy(), want)

@@ -75,6 +75,25 @@ def test_trsv_in_place_upper_garbage_and_errors(sc):
     assert lib.stan_cl_trsv(0, None, None, None, 0) == 0
 
 
+def grad_term_scale(x, y, a, r, s):
+    """S_theta = sum_{i>=j} |A_bar_ij dK_ij/dtheta| for theta = alpha, rho, sigma:
+    the size of the terms the hyperparameter gradient sums (their cancellation is
+    what makes |g| small), so the rounding error of any summation order is
+    O(eps * n * S_theta) -- the scale the absolute tolerance is tied to (instead
+    of |lp|, VERDICT r01 weak #11).  A_bar from the oracle's pieces."""
+    n = x.shape[0]
+    K = oracle.se_cov(x, a, r, s * s)
+    L = oracle.cholesky(K)
+    z = oracle.trsv(L, y)
+    al = oracle.trsv(L, z, trans=True)
+    Lbar = np.tril(np.outer(al, z)) - np.diag(1.0 / np.diag(L))
+    Ab = np.tril(oracle.cholesky_adjoint(L, Lbar))
+    d = x[:, None] - x[None, :]
+    E = np.exp(d * d * (-0.5 / (r * r)))
+    dK = [2 * a * E, a * a * E * d * d / r ** 3, 2 * s * np.eye(n)]
+    return [float(np.sum(np.abs(Ab * t))) for t in dK]
+
+
 @pytest.mark.parametrize("n", [1, 2, 64, 100, 300, 1000, 2048])
 def test_gp_lpdf_grad_parity(sc, n):
     x = inputs.gp_x(n)
@@ -84,8 +103,11 @@ def test_gp_lpdf_grad_parity(sc, n):
         out, yb = sc.gp_lpdf_grad(dev(x), dev(y), a, r, s)
         out = out.cpu().numpy()
         assert math.isclose(out[0], lp_o, rel_tol=1e-10)
+        S = grad_term_scale(x, y, a, r, s)
         for k in range(3):
-            assert math.isclose(out[1 + k], g_o[k], rel_tol=1e-8, abs_tol=1e-9 * (1 + abs(lp_o)))
+            # relative 1e-8 of the value, or 1e-12 of the summed term magnitudes
+            # (eps * sqrt(n) headroom: 2048 terms per row at 1.1e-16 ~ 5e-15 per term)
+            assert math.isclose(out[1 + k], g_o[k], rel_tol=1e-8, abs_tol=1e-12 * S[k]), (k, out[1 + k], g_o[k], S[k])
         assert rel(yb.cpu().numpy(), yb_o) <= 1e-10
 
 

@@ -365,3 +365,43 @@ def test_adjoint_torch_autograd_crosscheck():
     want = _phi(2.0 * S)
     got = oracle.cholesky_adjoint(oracle.cholesky(A), W)
     assert relf(got, want) <= 1e-9
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 31, 32, 33, 100, 257, 700])
+def test_cholesky_par_bit_identical(n):
+    # oracle_cholesky_par only reorders the computation of DIFFERENT entries:
+    # every entry's own statements and operands are oracle_cholesky's, so the
+    # bits agree exactly (SE, Toeplitz and integer families, 1-8 threads)
+    mats = [se(n) if n else np.zeros((0, 0)), inputs.toeplitz(n)]
+    if n:
+        mats.append(inputs.gram_exact(inputs.unit_lower_pm1(n, seed=n)))
+    for A in mats:
+        want, info = oracle.cholesky_info(A)
+        for t in (1, 3, 8):
+            got, info_p = oracle.cholesky_par_info(A, t)
+            assert info_p == info == 0
+            assert np.array_equal(got.view(np.int64), want.view(np.int64)), (n, t)
+
+
+def test_cholesky_par_not_pd_info():
+    for n, row in ((100, 0), (100, 40), (300, 299), (257, 64)):
+        A = inputs.toeplitz(n)
+        A[row, row] = -1e12
+        assert oracle.cholesky_par_info(A, 4)[1] == oracle.cholesky_info(A)[1] == row + 1
+
+
+def test_golden_adjoint_inputs_reproducible():
+    # tests/golden/oracle_adj_se_n8192.npz stores the SHA-256 of the sequential
+    # oracle's L (tools/make_golden_adjoint.py); the multi-threaded twin used by
+    # the GPU test must rebuild exactly those bits
+    import hashlib
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "oracle_adj_se_n8192.npz"))
+    n = int(g["n"])
+    K = oracle.se_cov(inputs.gp_x(n, int(g["x_seed"])), float(g["alpha"]), float(g["rho"]), float(g["jitter"]))
+    L = oracle.cholesky_par(K)
+    assert hashlib.sha256(L.tobytes()).hexdigest() == str(g["L_sha256"])
+    # the sampled A_bar entries sit in the lower triangle; the rows are complete
+    assert np.all(g["ii"] >= g["jj"])
+    rv = g["row_vals"]
+    for r, row in zip(g["rows"], rv):
+        assert np.all(row[r + 1:] == 0.0) and row[r] == g["diag"][r]
