@@ -52,6 +52,12 @@ def _load():
         lib.oracle_cholesky_adjoint.restype = ctypes.c_int
         lib.oracle_trsv.argtypes = [I64, P, P, ctypes.c_int, P]
         lib.oracle_trsv.restype = ctypes.c_int
+        lib.oracle_tri_inverse.argtypes = [I64, P, P]
+        lib.oracle_tri_inverse.restype = ctypes.c_int
+        lib.oracle_trsm.argtypes = [I64, I64, P, P, ctypes.c_int, P]
+        lib.oracle_trsm.restype = ctypes.c_int
+        lib.oracle_trsm_adjoint.argtypes = [I64, I64, P, P, P, P, P]
+        lib.oracle_trsm_adjoint.restype = ctypes.c_int
         lib.oracle_gp_lpdf_grad.argtypes = [I64, P, P, D, D, D, P, P]
         lib.oracle_gp_lpdf_grad.restype = ctypes.c_int
         _lib = lib
@@ -157,6 +163,46 @@ def trsv(L, b, trans: bool = False) -> np.ndarray:
     if info != 0:
         raise ValueError(f"L[{info - 1}][{info - 1}] is zero or not finite")
     return x
+
+
+def tri_inverse(L) -> np.ndarray:
+    """X = L^-1 for lower-triangular L (oracle.c oracle_tri_inverse)."""
+    L = _c(L)
+    n = L.shape[0]
+    assert L.shape == (n, n)
+    X = np.empty_like(L)
+    info = _load().oracle_tri_inverse(n, _ptr(L), _ptr(X))
+    if info != 0:
+        raise ValueError(f"L[{info - 1}][{info - 1}] is zero or not finite")
+    return X
+
+
+def trsm(L, B, trans: bool = False) -> np.ndarray:
+    """X with L X = B (trans=False) or L^T X = B (trans=True); B n x m (oracle.c)."""
+    L = _c(L)
+    B = _c(B)
+    n = L.shape[0]
+    assert L.shape == (n, n) and B.ndim == 2 and B.shape[0] == n
+    X = np.empty_like(B)
+    info = _load().oracle_trsm(n, B.shape[1], _ptr(L), _ptr(B), int(bool(trans)), _ptr(X))
+    if info != 0:
+        raise ValueError(f"L[{info - 1}][{info - 1}] is zero or not finite")
+    return X
+
+
+def trsm_adjoint(L, C, Cbar) -> tuple[np.ndarray, np.ndarray]:
+    """(L_bar, B_bar) of C = L^-1 B given C and C_bar (oracle.c oracle_trsm_adjoint)."""
+    L = _c(L)
+    C = _c(C)
+    Cbar = _c(Cbar)
+    n, m = C.shape
+    assert L.shape == (n, n) and Cbar.shape == (n, m)
+    Lbar = np.empty_like(L)
+    Bbar = np.empty_like(C)
+    info = _load().oracle_trsm_adjoint(n, m, _ptr(L), _ptr(C), _ptr(Cbar), _ptr(Lbar), _ptr(Bbar))
+    if info != 0:
+        raise ValueError(f"L[{info - 1}][{info - 1}] is zero or not finite")
+    return Lbar, Bbar
 
 
 def gp_lpdf_grad(x, y, alpha: float, rho: float, sigma: float) -> tuple[float, np.ndarray, np.ndarray]:

@@ -27,6 +27,12 @@
  *                               torch autograd cross-check, integer-exact family)
  *   oracle_trsv                pinned (integer-exact round trips, independent
  *                               library solve)
+ *   oracle_tri_inverse         pinned (integer-exact L X = I, exact reciprocal diagonal,
+ *                               2 x 2 closed form, X L = I on SE factors)
+ *   oracle_trsm                pinned (integer-exact round trips both ways, column
+ *                               independence)
+ *   oracle_trsm_adjoint        pinned (n = 1 closed form, finite differences of a
+ *                               random functional of L^-1 B in B and in L)
  *   oracle_gp_lpdf_grad        pinned (n = 1 closed form, independent Gaussian
  *                               log-density, trace-form gradient, finite differences)
  */
@@ -250,6 +256,101 @@ int oracle_trsv(int64_t n, const double* L, const double* b, int trans, double* 
       x[i] = s / L[IDX(i, i)];
     }
   }
+  return 0;
+}
+
+/*
+ * Lower triangular inverse X = L^-1 (§3.2 "the lower
+ * triangular inverse of A"), by its plain definition:
+ * column j of X solves L x = e_j by forward substitution,
+ *   X[j][j] = 1 / L[j][j]
+ *   X[i][j] = -(sum_{k=j}^{i-1} L[i][k] X[k][j]) / L[i][i],   i = j+1 .. n-1
+ * (the paper's divide-and-conquer C3 = -C2 A3 C1 reaches the same matrix up
+ * to rounding).  Sums in ascending k.  Reads only the lower triangle of L;
+ * writes all of X (+0.0 above the diagonal).  Returns 0, or k+1 for the first
+ * diagonal entry that is not finite and nonzero.  X must not alias L.
+ */
+int oracle_tri_inverse(int64_t n, const double* L, double* X) {
+  for (int64_t k = 0; k < n; ++k) {
+    double d = L[IDX(k, k)];
+    if (d == 0.0 || !isfinite(d)) return (int)(k + 1);
+  }
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) X[IDX(i, j)] = 0.0;
+  for (int64_t j = 0; j < n; ++j) {
+    X[IDX(j, j)] = 1.0 / L[IDX(j, j)];
+    for (int64_t i = j + 1; i < n; ++i) {
+      double s = 0.0;
+      for (int64_t k = j; k < i; ++k) {
+        double p = L[IDX(i, k)] * X[IDX(k, j)];
+        s = s + p;
+      }
+      X[IDX(i, j)] = -s / L[IDX(i, i)];
+    }
+  }
+  return 0;
+}
+
+/*
+ * Triangular solve with m right-hand sides, the paper's general solver for
+ * A x = b with triangular A (§3.2; NEXT-2), by substitution,
+ * one column c of B at a time (B, X: n x m row-major):
+ *   trans == 0:  L X = B     X[i][c] = (B[i][c] - sum_{j<i} L[i][j] X[j][c]) / L[i][i],  i ascending
+ *   trans == 1:  L^T X = B   X[i][c] = (B[i][c] - sum_{j>i} L[j][i] X[j][c]) / L[i][i],  i descending
+ * Sums in ascending j.  Reads only the lower triangle of L.  Returns 0, or
+ * k+1 for the first diagonal entry that is not finite and nonzero.  X may
+ * alias B.
+ */
+int oracle_trsm(int64_t n, int64_t m, const double* L, const double* B, int trans, double* X) {
+  for (int64_t k = 0; k < n; ++k) {
+    double d = L[IDX(k, k)];
+    if (d == 0.0 || !isfinite(d)) return (int)(k + 1);
+  }
+  if (X != B)
+    for (int64_t i = 0; i < n; ++i)
+      for (int64_t c = 0; c < m; ++c) X[(size_t)i * (size_t)m + (size_t)c] = B[(size_t)i * (size_t)m + (size_t)c];
+  for (int64_t c = 0; c < m; ++c) {
+    if (!trans) {
+      for (int64_t i = 0; i < n; ++i) {
+        double s = X[(size_t)i * (size_t)m + (size_t)c];
+        for (int64_t j = 0; j < i; ++j) s = s - L[IDX(i, j)] * X[(size_t)j * (size_t)m + (size_t)c];
+        X[(size_t)i * (size_t)m + (size_t)c] = s / L[IDX(i, i)];
+      }
+    } else {
+      for (int64_t i = n - 1; i >= 0; --i) {
+        double s = X[(size_t)i * (size_t)m + (size_t)c];
+        for (int64_t j = i + 1; j < n; ++j) s = s - L[IDX(j, i)] * X[(size_t)j * (size_t)m + (size_t)c];
+        X[(size_t)i * (size_t)m + (size_t)c] = s / L[IDX(i, i)];
+      }
+    }
+  }
+  return 0;
+}
+
+/*
+ * Reverse mode of C = L^-1 B (the triangular solver's chain()
+ * §3.2, read per DESIGN.md reading R17: the listing's "A * adjB = adjC" is the
+ * transposed system A^T adjB = adjC, the derivative of C = A^-1 B):
+ *   B_bar = L^-T C_bar                  (oracle_trsm, trans = 1)
+ *   L_bar = tril(-B_bar C^T)            (only L's lower triangle is an input)
+ *   L_bar[i][j] = -sum_c B_bar[i][c] C[j][c],  i >= j, sums in ascending c
+ * C, C_bar, B_bar: n x m row-major; L, L_bar: n x n (+0.0 above the diagonal
+ * of L_bar).  Returns 0, or k+1 for a bad diagonal of L.  B_bar may alias C_bar.
+ */
+int oracle_trsm_adjoint(int64_t n, int64_t m, const double* L, const double* C, const double* Cbar,
+                        double* Lbar, double* Bbar) {
+  int info = oracle_trsm(n, m, L, Cbar, 1, Bbar);
+  if (info) return info;
+  for (int64_t i = 0; i < n; ++i)
+    for (int64_t j = 0; j < n; ++j) {
+      double s = 0.0;
+      if (j <= i)
+        for (int64_t c = 0; c < m; ++c) {
+          double p = Bbar[(size_t)i * (size_t)m + (size_t)c] * C[(size_t)j * (size_t)m + (size_t)c];
+          s = s + p;
+        }
+      Lbar[IDX(i, j)] = (j <= i) ? -s : 0.0;
+    }
   return 0;
 }
 

@@ -31,7 +31,10 @@
 
 namespace stancl {
 
-enum GemmMode { MODE_FULL = 0, MODE_LOWER = 1, MODE_SPLITK = 2 };
+// MODE_CYC: MODE_FULL restricted to the lower tiles of a 2-D block-cyclic
+// local array (persistent TMA GEMM only; its item map carries the per-block-
+// column prefix table, so plain MODE_FULL launches do not)
+enum GemmMode { MODE_FULL = 0, MODE_LOWER = 1, MODE_SPLITK = 2, MODE_CYC = 3 };
 
 struct GemmArgs {
   const double* A;

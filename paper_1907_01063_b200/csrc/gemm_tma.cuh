@@ -141,27 +141,30 @@ __device__ __forceinline__ double frag(const double* s, int rc, int k) {
 template <class CF, int MODE>
 struct TItemMap {
   int ntn, ntiles, ktiles_full;
-  // block-cyclic mode (GemmArgs::cyc, MODE_FULL): items enumerate, per 256-wide
+  // block-cyclic mode (MODE_CYC): items enumerate, per 256-wide
   // block column j, only its tile rows from the first block row that reaches
-  // the diagonal (2 f_j) down; cyc_pref[j] = first item of block column j
-  static constexpr int kCycMax = (MODE == MODE_FULL) ? 512 : 1;
+  // the diagonal (RB f_j) down; cyc_pref[j] = first item of block column j
+  static constexpr int kCycMax = (MODE == MODE_CYC) ? 512 : 1;  // only MODE_CYC launches carry the table
   int cyc_nb = 0;
   int cyc_pref[kCycMax + 1];
   // item -> tile (tm, tn) in the rectangle (cyc) or row-major (otherwise)
   __device__ __forceinline__ void tile_of(const GemmArgs& p, int tile, int& tm, int& tn) const {
-    if constexpr (MODE == MODE_FULL) {
-      if (p.cyc) {
+    if constexpr (MODE == MODE_CYC) {
+      {
         int lo = 0, hi = cyc_nb;  // largest j with cyc_pref[j] <= tile
         while (hi - lo > 1) {
           const int mid = (lo + hi) >> 1;
           if (cyc_pref[mid] <= tile) lo = mid;
           else hi = mid;
         }
-        const int rows = (cyc_pref[lo + 1] - cyc_pref[lo]) / 4;  // tile rows of block column lo
-        const int first = 2 * (p.M / 256) - rows;                  // = 2 f_j
+        // a 256 x 256 block holds RB x CB tiles of BM x BN
+        constexpr int RB = 256 / CF::BM, CB = 256 / CF::BN;
+        static_assert(RB * CF::BM == 256 && CB * CF::BN == 256, "cyclic tiles must divide the 256-wide blocks");
+        const int rows = (cyc_pref[lo + 1] - cyc_pref[lo]) / CB;  // tile rows of block column lo
+        const int first = RB * (p.M / 256) - rows;                  // = RB f_j
         const int local = tile - cyc_pref[lo];
-        tm = first + local / 4;
-        tn = 4 * lo + (local & 3);
+        tm = first + local / CB;
+        tn = CB * lo + local % CB;
         return;
       }
     }
@@ -173,10 +176,9 @@ struct TItemMap {
   __device__ __forceinline__ bool valid(const GemmArgs& p, int item, bool& masked, int& d) const {
     masked = false;
     d = 0;
-    if constexpr (MODE != MODE_FULL) {
+    if constexpr (MODE != MODE_CYC) {
       return true;
     } else {
-      if (!p.cyc) return true;
       int tm, tn;
       tile_of(p, item, tm, tn);
       const int bi = tm / (256 / CF::BM), bj = tn / (256 / CF::BN);
@@ -393,7 +395,7 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
     bool cmask;
     int dd;
     map.valid(p, item, cmask, dd);  // block-cyclic diagonal block: keep r >= c + dd
-    const bool mask = (MODE == MODE_LOWER) || (MODE == MODE_FULL && (p.lower_only || cmask));
+    const bool mask = (MODE == MODE_LOWER) || ((MODE == MODE_FULL || MODE == MODE_CYC) && (p.lower_only || cmask));
     const bool crosses = mask && (n0 + BN - 1 + dd > m0);
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -446,8 +448,8 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reser
   } else {
     ntiles = (p.M / CF::BM) * map.ntn;
   }
-  if constexpr (MODE == MODE_FULL) {
-    if (p.cyc) {  // valid tile rows per 256-wide block column (BM = 128, BN = 64)
+  if constexpr (MODE == MODE_CYC) {
+    {  // valid tile rows per 256-wide block column
       const int nbc = p.N / 256, nbr = p.M / 256;
       if (nbc > TItemMap<CF, MODE>::kCycMax) return cudaErrorInvalidValue;
       map.cyc_nb = nbc;
@@ -457,7 +459,7 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reser
         // first local block row with global I >= J, relative to the rectangle's first row
         long long f = (J > p.cy_p ? (J - p.cy_p + p.cy_P - 1) / p.cy_P : 0) - p.cy_li;
         f = f < 0 ? 0 : (f > nbr ? nbr : f);
-        map.cyc_pref[j + 1] = map.cyc_pref[j] + 8 * (int)(nbr - f);
+        map.cyc_pref[j + 1] = map.cyc_pref[j] + (256 / CF::BM) * (256 / CF::BN) * (int)(nbr - f);
       }
       ntiles = map.cyc_pref[nbc];
     }

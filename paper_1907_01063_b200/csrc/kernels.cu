@@ -973,7 +973,7 @@ cudaError_t gemm_cyclic_lower(int M, int N, int K, const double* A, int64_t lda,
   g.cy_q = q;
   g.cy_li = li0;
   g.cy_lj = lj0;
-  return launch_tma<tg::CfgT32, true, true, MODE_FULL>(g, 1, st, reserve_sms);
+  return launch_tma<tg::CfgT32, true, true, MODE_CYC>(g, 1, st, reserve_sms);
 }
 
 cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
