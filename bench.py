@@ -167,46 +167,69 @@ def replica_seeds(rank: int) -> tuple[int, int]:
     return inputs.X_SEED + rank, inputs.LBAR_SEED + rank
 
 
-def run_oracle_sample(n: int) -> tuple[float, float]:
-    """Oracle Cholesky + adjoint at order n on one core: (seconds, flops)."""
+def oracle_sample_inputs(n: int, n_s: int):
+    """The bounded oracle sample of the order-n workload: the leading n_s x n_s
+    block of the SAME synthetic problem -- K from x_1..x_{n_s} of the n-point
+    draw (so the oracle's Cholesky-Banachiewicz rows 0..n_s-1 are exactly the
+    first n_s rows of its order-n run) and the leading block of the same L_bar
+    draw (the order-n adjoint of an L_bar supported on that block, restricted to
+    it).  n_s = n when n <= n_s."""
     import oracle
     from paper_1907_01063_b200 import inputs
-    K = oracle.se_cov(inputs.gp_x(n), ALPHA, RHO, JITTER)
-    W = inputs.lbar(n)
+    n_s = min(n, n_s)
+    K = oracle.se_cov(inputs.gp_x(n)[:n_s], ALPHA, RHO, JITTER)
+    W = inputs.lbar_leading(n, n_s)
+    return K, W
+
+
+def run_oracle_sample(n: int, n_s: int) -> tuple[float, float]:
+    """Oracle Cholesky + adjoint of the sample on one core: (seconds, flops)."""
+    import oracle
+    K, W = oracle_sample_inputs(n, n_s)
     t0 = time.perf_counter()
     L = oracle.cholesky(K)
     oracle.cholesky_adjoint(L, W)
-    return time.perf_counter() - t0, float(n) ** 3
+    return time.perf_counter() - t0, float(K.shape[0]) ** 3
 
 
-def cpu_baseline_entry(n_sample: int) -> dict:
-    secs, fl = run_oracle_sample(n_sample)
+def sample_desc(n: int, n_s: int) -> str:
+    m = min(n, n_s)
+    if m == n:
+        return f"the whole order-{n} workload (oracle Cholesky + adjoint), 1 thread"
+    return (f"leading {m} x {m} block of the order-{n} workload (x_1..x_{m} of the same draw, leading block of "
+            f"the same L_bar): the oracle's first {m} rows of L of the order-{n} problem plus the adjoint of "
+            f"that block; {m ** 3 / n ** 3:.2e} of the step's flops, rate = sample flops / sample time, 1 thread")
+
+
+def cpu_baseline_entry(n: int, n_sample: int) -> dict:
+    secs, fl = run_oracle_sample(n, n_sample)
     return {"value": fl / secs / 1e9, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle (oracle/oracle.c, 1 thread, -O2 -ffp-contract=off) Cholesky + adjoint of the "
-                      f"same SE-GP workload at n={n_sample} instead of 16384, one run, {secs:.2f} s; "
-                      f"host {os.cpu_count()} logical cores"}
+            "sample": sample_desc(n, n_sample) + f"; one run, {secs:.2f} s; host {os.cpu_count()} logical cores",
+            "sample_n": min(n, n_sample), "sample_seconds": secs}
 
 
 def bench_reference(args, rank: int, world: int):
     if rank != 0:
         return
-    n_s = args.oracle_n
+    n_s = min(args.n, args.oracle_n)
     for _ in range(args.warmup):
-        run_oracle_sample(n_s)
+        run_oracle_sample(args.n, n_s)
     times = []
     for _ in range(args.steps):
-        s, fl = run_oracle_sample(n_s)
+        s, fl = run_oracle_sample(args.n, n_s)
         times.append(s)
     ms = 1e3 * statistics.mean(times)
     val = float(n_s) ** 3 / (ms / 1e3) / 1e9
+    cfg = config(args.n, world)
+    cfg["sample"] = sample_desc(args.n, n_s)
+    cfg["sample_n"] = n_s
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": config(args.n, world),
+        "config": cfg,
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "oracle",
-                         "sample": f"each step = oracle Cholesky + adjoint at n={n_s} (bounded sample of the "
-                                   f"n={args.n} workload), 1 thread"},
+                         "sample": "each step = " + sample_desc(args.n, n_s)},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -428,7 +451,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
 
     if rank != 0:
         return
-    cpu = None if args.no_cpu_baseline else cpu_baseline_entry(args.oracle_n)
+    cpu = None if args.no_cpu_baseline else cpu_baseline_entry(n, args.oracle_n)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,

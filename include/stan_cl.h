@@ -207,6 +207,51 @@ int stan_cl_dist_sim_cholesky_adjoint(int64_t n, int G, const double* const* L_l
 int stan_cl_trsv(int64_t n, const double* L, const double* b, double* x, int trans);
 
 /*
+ * Lower triangular inverse X = L^-1 (the paper's lower_triangular_inverse,
+ * PAPER.md:207-225 §3.2; NEXT-2).  Method: the paper's batched divide and
+ * conquer -- the 128 x 128 diagonal blocks inverted by substitution, one CTA
+ * per block (the paper's batch_identity + diag_inv), then log2(n/128) doubling
+ * levels, each pair of adjacent inverted blocks [[C1, 0], [A3, C2]] completed
+ * by C3 = -C2 A3 C1 on the FP64 tensor cores (batched 128^3 / 256^3 products,
+ * persistent TMA GEMMs above).
+ *   L  device, n x n, lower triangle read; its diagonal must be finite and > 0
+ *      (the factors the library produces): the first L[k][k] that is not
+ *      returns k+1 (X unspecified)
+ *   X  device, n x n, written in full (strict upper +0.0); must not overlap L
+ *      (STAN_CL_EINVAL).  Synchronous.
+ */
+int stan_cl_lower_triangular_inverse(int64_t n, const double* L, double* X);
+
+/*
+ * Triangular solve with m right-hand sides (the paper's general solver for
+ * A x = b with triangular A, §3.2; NEXT-2):
+ *   trans == 0:  X = L^-1 B        trans != 0:  X = L^-T B
+ * L: n x n (lower triangle read, diagonal finite and > 0, else k+1 as
+ * stan_cl_trsv); B, X: n x m row-major (ld m).  X may alias B (in place);
+ * other overlaps -> STAN_CL_EINVAL.  Method: right-looking blocked
+ * substitution over 256-row blocks (128 below n = 768) with the diagonal
+ * blocks' explicit inverses -- per block S = D_i^-1 X_i (or D_i^-T X_i), then
+ * the rank-256 update of the remaining rows on the FP64 tensor cores.
+ * Synchronous.
+ */
+int stan_cl_trsm(int64_t n, int64_t m, const double* L, const double* B, double* X, int trans);
+
+/*
+ * Reverse mode of C = L^-1 B (the triangular solver's chain(), PAPER.md:231-238;
+ * the listing's "A * adjB = adjC" read as A^T adjB = adjC, R17):
+ *   B_bar = L^-T C_bar;    L_bar = tril(-B_bar C^T)
+ * L, L_bar: n x n (L_bar written in full, strict upper +0.0); C, C_bar, B_bar:
+ * n x m row-major.  B_bar may alias C_bar; every other overlap -> EINVAL.
+ * m == 0: L_bar = 0.  Returns k+1 for a bad diagonal of L as stan_cl_trsm.
+ * Synchronous.
+ */
+int stan_cl_trsm_adjoint(int64_t n, int64_t m, const double* L, const double* C, const double* C_bar,
+                         double* L_bar, double* B_bar);
+/* caller workspace (stan_cl_set_workspace) that suffices for stan_cl_trsm and
+ * stan_cl_trsm_adjoint with n x m right-hand sides */
+size_t stan_cl_trsm_workspace_bytes(int64_t n, int64_t m);
+
+/*
  * Marginal log density of zero-mean GP regression and its gradient -- the
  * per-gradient work of the paper's GP example (§4.2, the model
  * y ~ multi_normal_cholesky(0, chol(K)); NEXT-1):
@@ -272,7 +317,8 @@ int stan_cl_set_adjoint_block_size(int nb);
  * for a misaligned / too small buffer.
  * stan_cl_workspace_bytes(n): bytes that suffice for every single-matrix entry
  * point at order n (cholesky, cholesky_adjoint, their _async and _host forms,
- * trsv, gp_lpdf_grad) with the current block-size settings and 16-byte
+ * trsv, gp_lpdf_grad, lower_triangular_inverse; trsm: see
+ * stan_cl_trsm_workspace_bytes) with the current block-size settings and 16-byte
  * aligned arguments (an unaligned argument takes the padded path: add
  * 2 * 8 * N^2, N = n rounded up to 256).
  * stan_cl_batched_workspace_bytes(batch, n, with_info): the same for the batched

@@ -41,6 +41,10 @@ SIGNATURES = {
     "stan_cl_cholesky_adjoint": (_I, [_I64, _P, _P, _P]),
     "stan_cl_gp_exp_quad_cov": (_I, [_I64, _P, _D, _D, _D, _P]),
     "stan_cl_trsv": (_I, [_I64, _P, _P, _P, _I]),
+    "stan_cl_lower_triangular_inverse": (_I, [_I64, _P, _P]),
+    "stan_cl_trsm": (_I, [_I64, _I64, _P, _P, _P, _I]),
+    "stan_cl_trsm_adjoint": (_I, [_I64, _I64, _P, _P, _P, _P, _P]),
+    "stan_cl_trsm_workspace_bytes": (ctypes.c_size_t, [_I64, _I64]),
     "stan_cl_cholesky_batched": (_I, [_I64, _I64, _P, _P, _P]),
     "stan_cl_cholesky_adjoint_batched": (_I, [_I64, _I64, _P, _P, _P, _P]),
     "stan_cl_gp_lpdf_grad": (_I, [_I64, _P, _P, _D, _D, _D, _P, _P]),
@@ -226,6 +230,69 @@ def trsv(L: torch.Tensor, b: torch.Tensor, trans: bool = False, out: torch.Tenso
     if rc > 0:
         raise ValueError(f"L[{rc - 1}][{rc - 1}] is not finite and > 0")
     return x
+
+
+def lower_triangular_inverse(L: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """X = L^-1, L lower with positive diagonal (stan_cl_lower_triangular_inverse)."""
+    L = _dev_matrix(L, "L")
+    n = L.shape[0]
+    X = _out(out, (n, n), L.device)
+    if X.data_ptr() == L.data_ptr() and n > 0:
+        raise ValueError("lower_triangular_inverse is not in place")
+    with torch.cuda.device(L.device):
+        _bind_stream(L.device)
+        rc = _check("stan_cl_lower_triangular_inverse",
+                    load().stan_cl_lower_triangular_inverse(n, L.data_ptr(), X.data_ptr()))
+    if rc > 0:
+        raise ValueError(f"L[{rc - 1}][{rc - 1}] is not finite and > 0")
+    return X
+
+
+def _dev_rect(t: torch.Tensor, name: str, n: int) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64 or t.dim() != 2 \
+            or t.shape[0] != n:
+        raise ValueError(f"{name} must be a ({n}, m) float64 CUDA tensor")
+    return t.contiguous()
+
+
+def trsm(L: torch.Tensor, B: torch.Tensor, trans: bool = False, out: torch.Tensor | None = None) -> torch.Tensor:
+    """X = L^-1 B (trans=False) or L^-T B (trans=True), B n x m (stan_cl_trsm).
+    ``out`` may be ``B`` (in place)."""
+    if out is not None and out is B and not B.is_contiguous():
+        raise ValueError("in-place trsm needs a contiguous B")
+    L = _dev_matrix(L, "L")
+    n = L.shape[0]
+    B = _dev_rect(B, "B", n)
+    if B.device != L.device:
+        raise ValueError("L and B are on different devices")
+    X = _out(out, tuple(B.shape), L.device)
+    with torch.cuda.device(L.device):
+        _bind_stream(L.device)
+        rc = _check("stan_cl_trsm", load().stan_cl_trsm(n, B.shape[1], L.data_ptr(), B.data_ptr(), X.data_ptr(),
+                                                        int(bool(trans))))
+    if rc > 0:
+        raise ValueError(f"L[{rc - 1}][{rc - 1}] is not finite and > 0")
+    return X
+
+
+def trsm_adjoint(L: torch.Tensor, C: torch.Tensor, Cbar: torch.Tensor) -> tuple[torch.Tensor, torch.Tensor]:
+    """(L_bar, B_bar) of C = L^-1 B given C and C_bar (stan_cl_trsm_adjoint):
+    B_bar = L^-T C_bar, L_bar = tril(-B_bar C^T)."""
+    L = _dev_matrix(L, "L")
+    n = L.shape[0]
+    C = _dev_rect(C, "C", n)
+    Cbar = _dev_rect(Cbar, "Cbar", n)
+    if C.shape != Cbar.shape or C.device != L.device or Cbar.device != L.device:
+        raise ValueError("C and Cbar must match in shape and sit on L's device")
+    Lbar = torch.empty_like(L)
+    Bbar = torch.empty_like(C)
+    with torch.cuda.device(L.device):
+        _bind_stream(L.device)
+        rc = _check("stan_cl_trsm_adjoint", load().stan_cl_trsm_adjoint(
+            n, C.shape[1], L.data_ptr(), C.data_ptr(), Cbar.data_ptr(), Lbar.data_ptr(), Bbar.data_ptr()))
+    if rc > 0:
+        raise ValueError(f"L[{rc - 1}][{rc - 1}] is not finite and > 0")
+    return Lbar, Bbar
 
 
 def gp_lpdf_grad(x: torch.Tensor, y: torch.Tensor, alpha: float, rho: float, sigma: float,

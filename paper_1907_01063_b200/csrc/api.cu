@@ -352,7 +352,8 @@ int panel(double* W, int64_t ld, int64_t c0, int64_t N, int64_t OB, int* status,
 //   main: wait panel k; A[col block k+1] -= L21 L21(k+1)^T     (lookahead column)
 //   side: panel(k+1)                                          (L11 = chol(A11); L21 = A21 L11^-T)
 //   main: A22[k+2.., k+2..] -= L21 L21^T (lower tiles)         (multiply_transpose)
-int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status, const HostOut* out = nullptr) {
+int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status, const HostOut* out = nullptr,
+                   bool zero_upper_main = false) {
   cudaStream_t main = g.stream;
   const int64_t T = N / OB;
   int rc = ensure_side(2 * T + 2);
@@ -364,6 +365,10 @@ int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status, co
   CK(cudaStreamWaitEvent(side, ev[0], 0));
   rc = panel(W, ld, 0, N, OB, status, side);
   if (rc) return rc;
+  // in place: the strict upper triangle of A becomes +0.0 (F4).  Nothing in the
+  // factorisation reads it, and the POTRF tiles write their own upper parts,
+  // so the main stream clears the rest while the first panel runs on the side
+  if (zero_upper_main) CK(zero_upper_offdiag(W, N, ld, main));
   CK(cudaEventRecord(ev[1], side));
   // streamed D2H: the rows of panel k are final once panel k is done
   auto ship = [&](int64_t k) -> int {
@@ -418,9 +423,8 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
   const bool fast = (N == n) && aligned16(A) && aligned16(L);
   if (fast) {
     if (A != L) CK(copy_lower_pad(A, n, n, L, n, n, 1.0, st));
-    rc = factor_inplace(L, n, n, OB, status);
+    rc = factor_inplace(L, n, n, OB, status, nullptr, /*zero_upper_main=*/A == L);
     if (rc) return rc;
-    if (A == L) CK(zero_upper(L, n, n, st));
   } else {
     double* W = nullptr;
     rc = ensure_mat(0, (size_t)N * N * sizeof(double), &W);
@@ -471,9 +475,13 @@ int block_inverses(const double* Lw, int64_t ld, int64_t B, int64_t b0, int64_t 
 // block of Lw / Wm have arrived and the D^-1 covering it is in the workspace
 // (streamed H2D); out (optional): column block j of the result is shipped to the
 // host as soon as it is final (after the step that Phi-s D_bar(j)).
+// src (optional): L_bar itself (ld lds).  Wm is then NOT pre-initialised: the
+// rows of block [j, k) get tril(L_bar) when they enter the sweep, fused with the
+// split-K reduction that first writes them (adj_rows_init; R0 costs no pass).
 int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* status,
                     const AdjPlan& plan, const cudaEvent_t* rows_ready = nullptr,
-                    const HostOut* out = nullptr, const cudaEvent_t* col_done = nullptr) {
+                    const HostOut* out = nullptr, const cudaEvent_t* col_done = nullptr,
+                    const double* src = nullptr, int64_t lds = 0) {
   cudaStream_t st = g.stream;
   const int64_t B = plan.B;
   char* base = (char*)g.ws + al(sizeof(int) * 64);
@@ -514,8 +522,11 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
       int splits, kps;
       splitk_choice(m, k, B, &splits, &kps);
       CK(gemm_splitk_tn((int)B, (int)k, (int)m, splits, kps, Ctmp, B, Lw + k * ld, ld, Pbuf, status, st));
-      CK(splitk_reduce_sub(Pbuf, splits, (int)B, (int)k, Wm + j * ld, ld, status, st));
+      if (src) CK(adj_rows_init(Pbuf, splits, (int)B, k, src, lds, Wm, ld, j, N, status, st));
+      else CK(splitk_reduce_sub(Pbuf, splits, (int)B, (int)k, Wm + j * ld, ld, status, st));
       CK(copy_block(Ctmp, B, Cb, ld, m, B, st));
+    } else if (src) {
+      CK(adj_rows_init(nullptr, 0, (int)B, 0, src, lds, Wm, ld, j, N, status, st));  // rows [j, N): tril(L_bar)
     }
     // D_adj = transpose(D) * D_adj; copy_lower_tri_to_upper_tri
     // (only the lower tiles of P = D^T D_adj are formed, stored mirrored)
@@ -563,9 +574,8 @@ int adjoint_enqueue(int64_t n, const double* L, const double* Lbar, double* Abar
   const int64_t N = plan.N;
   const bool fast = (N == n) && aligned16(L) && aligned16(Lbar) && aligned16(Abar);
   if (fast) {
-    if (Lbar != Abar) CK(copy_lower_pad(Lbar, n, n, Abar, n, n, 0.0, st));
-    else CK(zero_upper(Abar, n, n, st));
-    rc = adjoint_inplace(L, Abar, n, n, status, plan);
+    // A_bar starts as tril(L_bar) row block by row block inside the sweep
+    rc = adjoint_inplace(L, Abar, n, n, status, plan, nullptr, nullptr, nullptr, Lbar, n);
     if (rc) return rc;
   } else {
     double *Lw = nullptr, *Wm = nullptr;
@@ -604,6 +614,142 @@ int vec_scratch(int64_t n, VecScratch* v) {
   v->partial = p + 2 * n;
   v->out = v->partial + gp_hyper_scratch_doubles();
   v->flags = (int*)(p + nd);
+  return STAN_CL_OK;
+}
+
+// ---- NEXT-2: lower triangular inverse, multi-RHS solve and its reverse mode ----
+// Largest doubling level b = 128 * 2^s with a pair [[C1, 0], [A3, C2]] at order N.
+int64_t trinv_top_level(int64_t N) {
+  int64_t b = NB;
+  while (2 * b < N) b *= 2;
+  return b;
+}
+size_t trinv_scratch_doubles(int64_t N) {
+  const int64_t bt = trinv_top_level(N);
+  return std::max<size_t>((size_t)N * 128, (size_t)bt * (size_t)bt);
+}
+
+// X = L^-1 on N x N (N % 128 == 0) working matrices: the
+// diagonal 128-blocks by substitution (tri_inverse_batched, the paper's
+// diag_inv over a batch), then doubling: at level b every pair of adjacent
+// b-blocks [[C1, 0], [A3, C2]] gets C3 = -C2 (A3 C1) (the paper's T = C2 A3,
+// C3 = -T C1 with the association flipped: same product).  Levels 128 and 256
+// run all full pairs as one batched launch per product; larger levels one
+// persistent TMA GEMM per product; a ragged last pair (N not a power-of-two
+// multiple of 128) is a rectangular product.  Xw must be zero on entry.
+int tri_inverse_blocked(const double* Lw, int64_t ldl, double* Xw, int64_t ldx, int64_t N, double* T, int* status,
+                        cudaStream_t st) {
+  CK(tri_inverse_batched(Lw, ldl, (int)(N / NB), Xw, status, st, ldx, NB * ldx + NB, 1, NB * ldl + NB));
+  for (int64_t b = NB; b < N; b *= 2) {
+    const int64_t nf = N / (2 * b), R = N - nf * 2 * b;
+    if (nf > 0 && b <= 2 * NB) {
+      const int64_t sL = 2 * b * ldl + 2 * b, sX = 2 * b * ldx + 2 * b;
+      CK(gemm_small((int)b, false, false, false, Lw + b * ldl, ldl, Xw, ldx, T, b, status, st, 1.0, (int)nf, sL, sX,
+                    b * b));
+      CK(gemm_small((int)b, false, false, false, Xw + b * ldx + b, ldx, T, b, Xw + b * ldx, ldx, status, st, -1.0,
+                    (int)nf, sX, b * b, sX));
+    } else {
+      for (int64_t p = 0; p < nf; ++p) {
+        const int64_t c0 = 2 * b * p, r0 = c0 + b;
+        CK(gemm_full(true, false, (int)b, (int)b, (int)b, 1.0, 0, Lw + r0 * ldl + c0, ldl, Xw + c0 * ldx + c0, ldx,
+                     T, b, status, st, 0, PROF_GP));
+        CK(gemm_full(true, false, (int)b, (int)b, (int)b, -1.0, 0, Xw + r0 * ldx + r0, ldx, T, b,
+                     Xw + r0 * ldx + c0, ldx, status, st, 0, PROF_GP));
+      }
+    }
+    if (R > b) {  // ragged pair: C1 is b x b, C2 is rb x rb
+      const int64_t c0 = nf * 2 * b, r0 = c0 + b, rb = R - b;
+      CK(gemm_full(true, false, (int)rb, (int)b, (int)b, 1.0, 0, Lw + r0 * ldl + c0, ldl, Xw + c0 * ldx + c0, ldx,
+                   T, b, status, st, 0, PROF_GP));
+      CK(gemm_full(true, false, (int)rb, (int)b, (int)rb, -1.0, 0, Xw + r0 * ldx + r0, ldx, T, b,
+                   Xw + r0 * ldx + c0, ldx, status, st, 0, PROF_GP));
+    }
+  }
+  return STAN_CL_OK;
+}
+
+// block of the multi-RHS solve: 256 from n = 768 (as the adjoint), else 128
+int64_t trsm_block(int64_t n) { return n >= 768 ? 2 * NB : NB; }
+size_t trsm_ws_bytes(int64_t n, int64_t m) {
+  const int64_t Bk = trsm_block(n), N = round_up(n, Bk), Mp = round_up(std::max<int64_t>(m, 1), 64);
+  return kHdr + al((size_t)N * Bk * sizeof(double)) + al((size_t)Bk * Mp * sizeof(double)) +
+         al((size_t)(N / Bk + 1) * NB * NB * sizeof(double));
+}
+
+// Wx <- L^-1 Wx (trans = false) or L^-T Wx (trans = true), in place on the
+// N x Mp working matrix (ld ldw), L's working copy Lw (ld ldl), N % Bk == 0:
+// right-looking blocked substitution with explicit diagonal-block inverses
+// (the paper's "general solver ... adds a multiplication of the inverse",
+// PAPER.md:207, applied per block so the inverses stay Bk x Bk):
+//   forward, block i ascending:   S = D_i^-1 X_i;   X_{>i} -= L_{>i,i} S;   X_i = S
+//   trans, block i descending:    S = D_i^-T X_i;   X_{<i} -= L_{i,<i}^T S; X_i = S
+int trsm_blocked(const double* Lw, int64_t ldl, double* Wx, int64_t ldw, int64_t N, int64_t Mp, int64_t Bk,
+                 bool trans, int* status, cudaStream_t st) {
+  char* base = (char*)g.ws + kHdr;
+  double* Dinv = (double*)base;
+  double* S = (double*)(base + al((size_t)N * Bk * sizeof(double)));
+  double* bscr = (double*)((char*)S + al((size_t)Bk * Mp * sizeof(double)));
+  const int64_t nblk = N / Bk;
+  int rc = block_inverses(Lw, ldl, Bk, 0, nblk, Dinv, bscr, status, st);
+  if (rc) return rc;
+  for (int64_t t = 0; t < nblk; ++t) {
+    const int64_t i = trans ? nblk - 1 - t : t, r0 = i * Bk;
+    const double* Di = Dinv + i * Bk * Bk;
+    double* Xi = Wx + r0 * ldw;
+    CK(gemm_full(!trans, false, (int)Bk, (int)Mp, (int)Bk, 1.0, 0, Di, Bk, Xi, ldw, S, Mp, status, st, 0, PROF_GP));
+    if (!trans && r0 + Bk < N)
+      CK(gemm_full(true, false, (int)(N - r0 - Bk), (int)Mp, (int)Bk, -1.0, 1, Lw + (r0 + Bk) * ldl + r0, ldl, S, Mp,
+                   Xi + Bk * ldw, ldw, status, st, 0, PROF_GP));
+    if (trans && r0 > 0)
+      CK(gemm_full(false, false, (int)r0, (int)Mp, (int)Bk, -1.0, 1, Lw + r0 * ldl, ldl, S, Mp, Wx, ldw, status, st, 0,
+                   PROF_GP));
+    CK(copy_block(S, Mp, Xi, ldw, Bk, Mp, st));
+  }
+  return STAN_CL_OK;
+}
+
+// the working copies of a multi-RHS solve: L (N x N, padded with I) and the
+// right-hand sides (N x Mp, zero padded), or the caller's buffers when aligned
+struct TrsmWork {
+  const double* Lw;
+  int64_t ldl;
+  double* Wx;
+  int64_t ldw, N, Mp, Bk;
+  bool direct;  // Wx is the caller's output
+};
+int trsm_prepare(int64_t n, int64_t m, const double* L, const double* B, double* X, TrsmWork* w, int* status,
+                 cudaStream_t st) {
+  w->Bk = trsm_block(n);
+  w->N = round_up(n, w->Bk);
+  w->Mp = round_up(m, 64);
+  int rc = ensure_ws(trsm_ws_bytes(n, m));
+  if (rc) return rc;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  CK(check_diag(L, n, n, status, st));
+  if (w->N == n && aligned16(L)) {
+    w->Lw = L;
+    w->ldl = n;
+  } else {
+    double* Lp = nullptr;
+    if ((rc = ensure_mat(0, (size_t)w->N * w->N * sizeof(double), &Lp))) return rc;
+    CK(copy_lower_pad(L, n, n, Lp, w->N, w->N, 1.0, st));
+    w->Lw = Lp;
+    w->ldl = w->N;
+  }
+  w->direct = (w->N == n && w->Mp == m && aligned16(X) && aligned16(B));
+  if (w->direct) {
+    w->Wx = X;
+    w->ldw = m;
+    if (X != B) CK(cudaMemcpyAsync(X, B, (size_t)n * m * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  } else {
+    double* Wp = nullptr;
+    if ((rc = ensure_mat(1, (size_t)w->N * w->Mp * sizeof(double), &Wp))) return rc;
+    CK(cudaMemsetAsync(Wp, 0, (size_t)w->N * w->Mp * sizeof(double), st));
+    CK(cudaMemcpy2DAsync(Wp, w->Mp * sizeof(double), B, m * sizeof(double), m * sizeof(double), n,
+                         cudaMemcpyDeviceToDevice, st));
+    w->Wx = Wp;
+    w->ldw = w->Mp;
+  }
   return STAN_CL_OK;
 }
 
@@ -745,6 +891,117 @@ int stan_cl_cholesky_adjoint(int64_t n, const double* L, const double* L_bar, do
   CallScope call_;
   int rc = stan_cl_cholesky_adjoint_async(n, L, L_bar, A_bar, nullptr);
   if (rc || n == 0) return rc;
+  return read_status();
+}
+
+int stan_cl_lower_triangular_inverse(int64_t n, const double* L, double* X) {
+  CallScope call_;
+  if (n < 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!L || !X) return STAN_CL_EINVAL;
+  const size_t bytes = (size_t)n * (size_t)n * sizeof(double);
+  if (ranges_overlap(L, X, bytes)) return STAN_CL_EINVAL;
+  const int64_t N = round_up(n, NB);
+  int rc = ensure_ws(kHdr);
+  if (rc) return rc;
+  int* status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  const bool fast = (N == n) && aligned16(L) && aligned16(X);
+  const double* Lw = L;
+  double* Xw = X;
+  if (!fast) {
+    double *Lp = nullptr, *Xp = nullptr;
+    if ((rc = ensure_mat(0, (size_t)N * N * sizeof(double), &Lp))) return rc;
+    if ((rc = ensure_mat(1, (size_t)N * N * sizeof(double), &Xp))) return rc;
+    CK(copy_lower_pad(L, n, n, Lp, N, N, 1.0, st));
+    Lw = Lp;
+    Xw = Xp;
+  }
+  double* T = nullptr;
+  if ((rc = ensure_mat(2, trinv_scratch_doubles(N) * sizeof(double), &T))) return rc;
+  CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+  CK(check_diag(L, n, n, status, st));
+  CK(cudaMemsetAsync(Xw, 0, (size_t)N * N * sizeof(double), st));
+  if ((rc = tri_inverse_blocked(Lw, N, Xw, N, N, T, status, st))) return rc;
+  if (!fast) CK(copy_lower_out(Xw, N, X, n, n, st));
+  return read_status();
+}
+
+int stan_cl_trsm(int64_t n, int64_t m, const double* L, const double* B, double* X, int trans) {
+  CallScope call_;
+  if (n < 0 || m < 0) return STAN_CL_EINVAL;
+  if (n == 0 || m == 0) return STAN_CL_OK;
+  if (!L || !B || !X) return STAN_CL_EINVAL;
+  const size_t xb = (size_t)n * (size_t)m * sizeof(double);
+  if (X != B && ranges_overlap(X, B, xb)) return STAN_CL_EINVAL;
+  if (ranges_overlap2(X, xb, L, (size_t)n * n * sizeof(double))) return STAN_CL_EINVAL;
+  int* status = nullptr;
+  TrsmWork w;
+  int rc = ensure_ws(trsm_ws_bytes(n, m));
+  if (rc) return rc;
+  status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  if ((rc = trsm_prepare(n, m, L, B, X, &w, status, st))) return rc;
+  if ((rc = trsm_blocked(w.Lw, w.ldl, w.Wx, w.ldw, w.N, w.Mp, w.Bk, trans != 0, status, st))) return rc;
+  if (!w.direct)
+    CK(cudaMemcpy2DAsync(X, m * sizeof(double), w.Wx, w.ldw * sizeof(double), m * sizeof(double), n,
+                         cudaMemcpyDeviceToDevice, st));
+  return read_status();
+}
+
+int stan_cl_trsm_adjoint(int64_t n, int64_t m, const double* L, const double* C, const double* C_bar,
+                         double* L_bar, double* B_bar) {
+  CallScope call_;
+  if (n < 0 || m < 0) return STAN_CL_EINVAL;
+  if (n == 0) return STAN_CL_OK;
+  if (!L || !L_bar || (m > 0 && (!C || !C_bar || !B_bar))) return STAN_CL_EINVAL;
+  const size_t xb = (size_t)n * (size_t)m * sizeof(double), lb = (size_t)n * n * sizeof(double);
+  if (m > 0) {
+    if (B_bar != C_bar && ranges_overlap(B_bar, C_bar, xb)) return STAN_CL_EINVAL;
+    if (ranges_overlap2(B_bar, xb, L, lb) || ranges_overlap2(B_bar, xb, C, xb) ||
+        ranges_overlap2(B_bar, xb, L_bar, lb))
+      return STAN_CL_EINVAL;
+    if (ranges_overlap2(L_bar, lb, L, lb) || ranges_overlap2(L_bar, lb, C, xb) || ranges_overlap2(L_bar, lb, C_bar, xb))
+      return STAN_CL_EINVAL;
+  } else if (ranges_overlap(L_bar, L, lb)) {
+    return STAN_CL_EINVAL;
+  }
+  int rc = ensure_ws(trsm_ws_bytes(n, std::max<int64_t>(m, 1)));
+  if (rc) return rc;
+  int* status = (int*)g.ws;
+  cudaStream_t st = g.stream;
+  if (m == 0) {
+    CK(cudaMemsetAsync(status, 0, sizeof(int), st));
+    CK(check_diag(L, n, n, status, st));
+    CK(cudaMemsetAsync(L_bar, 0, lb, st));
+    return read_status();
+  }
+  // B_bar = L^-T C_bar (the solve of the primitive, transposed)
+  TrsmWork w;
+  if ((rc = trsm_prepare(n, m, L, C_bar, B_bar, &w, status, st))) return rc;
+  if ((rc = trsm_blocked(w.Lw, w.ldl, w.Wx, w.ldw, w.N, w.Mp, w.Bk, true, status, st))) return rc;
+  // L_bar = tril(-B_bar C^T): lower tiles only (PAPER.md:236 adjA = -adjB C^T),
+  // into an N x N working matrix when padded; C is staged zero-padded to N x Mp
+  const double* Cw = C;
+  double* Lb = L_bar;
+  const bool direct_l = w.direct && aligned16(C) && aligned16(L_bar);
+  if (!direct_l) {
+    double *Cp = nullptr, *Lp = nullptr;
+    if ((rc = ensure_mat(2, (size_t)w.N * w.Mp * sizeof(double), &Cp))) return rc;
+    if ((rc = ensure_mat(3, (size_t)w.N * w.N * sizeof(double), &Lp))) return rc;
+    CK(cudaMemsetAsync(Cp, 0, (size_t)w.N * w.Mp * sizeof(double), st));
+    CK(cudaMemcpy2DAsync(Cp, w.Mp * sizeof(double), C, m * sizeof(double), m * sizeof(double), n,
+                         cudaMemcpyDeviceToDevice, st));
+    Cw = Cp;
+    Lb = Lp;
+  }
+  const int64_t ldlb = direct_l ? n : w.N, ldc = direct_l ? m : w.Mp;
+  CK(cudaMemsetAsync(Lb, 0, (size_t)w.N * ldlb * sizeof(double), st));
+  CK(gemm_lower_nt((int)w.N, (int)w.Mp, w.Wx, w.ldw, Cw, ldc, Lb, ldlb, status, st));
+  if (!direct_l) CK(copy_lower_out(Lb, w.N, L_bar, n, n, st));
+  if (!w.direct)
+    CK(cudaMemcpy2DAsync(B_bar, m * sizeof(double), w.Wx, w.ldw * sizeof(double), m * sizeof(double), n,
+                         cudaMemcpyDeviceToDevice, st));
   return read_status();
 }
 
@@ -1094,7 +1351,20 @@ size_t stan_cl_workspace_bytes(int64_t n) {
   // the inner cholesky / adjoint when n is not a block multiple
   const size_t pads = std::max((Nf == nn) ? 0 : mat_f, (Na == nn) ? 0 : 2 * mat_a);
   need = std::max(need, adj_ws + 2 * al(nn * nn * sizeof(double)) + vec + pads);
+  // lower_triangular_inverse: padded L and X when n % 128 != 0, doubling scratch
+  const size_t N128 = (size_t)round_up(n, NB);
+  const size_t mat_128 = al(N128 * N128 * sizeof(double));
+  need = std::max(need, kHdr + ((N128 == nn) ? 0 : 2 * mat_128) + al(trinv_scratch_doubles((int64_t)N128) * sizeof(double)));
   return need;
+}
+
+size_t stan_cl_trsm_workspace_bytes(int64_t n, int64_t m) {
+  if (n <= 0) return kHdr;
+  const int64_t Bk = trsm_block(n), N = round_up(n, Bk), Mp = round_up(std::max<int64_t>(m, 1), 64);
+  const size_t ws = al(trsm_ws_bytes(n, std::max<int64_t>(m, 1)));
+  const size_t Lp = al((size_t)N * N * sizeof(double)), Wp = al((size_t)N * Mp * sizeof(double));
+  // trsm_adjoint, padded: L, right-hand sides, C and L_bar working copies
+  return ws + 2 * Lp + 2 * Wp;
 }
 
 size_t stan_cl_batched_workspace_bytes(int64_t batch, int64_t n, int with_info) {

@@ -12,6 +12,7 @@
 //       diagonal blocks), gemm128 (128^3 products of the symbolic
 //       diagonal step), phi_sym,
 //       splitk_reduce_sub (the paper's large-k reduction)
+#include <algorithm>
 #include <atomic>
 #include <cstdio>
 #include <climits>
@@ -1027,6 +1028,72 @@ __global__ void splitk_reduce_sub_kernel(const double* __restrict__ P, int split
     o.y -= s.y;
     *d = o;
   }
+}
+
+// R0 fused into the sweep: rows [j, j+B) of A_bar enter the reverse sweep at
+// step k = j + B, so their initialisation tril(L_bar) is
+// done there, together with the split-K reduction that is the first write to
+// them:
+//   dst[j+r][c] = [c <= j+r] src[j+r][c] - [c < kc] sum_z P[z][r][c],  c < N
+// (src may equal dst; columns >= kc of those rows are the strict upper: +0.0).
+// One CTA row per matrix row (blockIdx.y), double2 columns.
+__global__ void adj_rows_init_kernel(const double* __restrict__ P, int splits, int B, int64_t kc,
+                                     const double* src, int64_t lds, double* dst, int64_t ldd, int64_t j, int64_t N,
+                                     const int* status) {
+  pdl_enter();
+  if (cta_status_set(status)) return;
+  const int r = blockIdx.y;
+  const int64_t gr = j + r;
+  const long long plane = (long long)B * kc;
+  const double* srow = src + gr * lds;
+  double* drow = dst + gr * ldd;
+  const double* prow = P + (long long)r * kc;
+  for (int64_t c2 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c2 < N / 2;
+       c2 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = 2 * c2;
+    double2 v = make_double2(0.0, 0.0);
+    if (c <= gr) {
+      v = *reinterpret_cast<const double2*>(srow + c);
+      if (c + 1 > gr) v.y = 0.0;
+    }
+    if (c < kc) {
+      for (int z = 0; z < splits; ++z) {
+        const double2 q = *reinterpret_cast<const double2*>(prow + z * plane + c);
+        v.x -= q.x;
+        v.y -= q.y;
+      }
+    }
+    *reinterpret_cast<double2*>(drow + c) = v;
+  }
+}
+
+cudaError_t adj_rows_init(const double* P, int splits, int B, int64_t kc, const double* src, int64_t lds, double* dst,
+                          int64_t ldd, int64_t j, int64_t N, const int* status, cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st, 8.0 * B * (splits * (double)kc + 1.5 * N));
+  if (B == 0 || N == 0) return cudaSuccess;
+  const int gx = (int)std::min<int64_t>((N / 2 + 255) / 256, 64);
+  return launch_pdl(adj_rows_init_kernel, dim3(gx, B), 256, 0, st, P, splits, B, kc, src, lds, dst, ldd, j, N, status);
+}
+
+// +0.0 into the strict upper triangle outside the 128 x 128 diagonal tiles
+// (those are written by the POTRF tiles): row r, columns [(r/128 + 1) 128, n)
+__global__ void zero_upper_offdiag_kernel(double* A, int64_t n, int64_t ld) {
+  const int64_t r = blockIdx.y;
+  const int64_t c0 = (r / NB + 1) * NB;
+  double* row = A + r * ld;
+  for (int64_t c = c0 + 2 * (blockIdx.x * (int64_t)blockDim.x + threadIdx.x); c < n;
+       c += 2 * (int64_t)gridDim.x * blockDim.x) {
+    if (c + 1 < n) *reinterpret_cast<double2*>(row + c) = make_double2(0.0, 0.0);
+    else row[c] = 0.0;
+  }
+}
+
+cudaError_t zero_upper_offdiag(double* A, int64_t n, int64_t ld, cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st, 4.0 * n * n);
+  if (n <= NB) return cudaSuccess;
+  const int gx = (int)std::min<int64_t>((n / 2 + 255) / 256, 32);
+  zero_upper_offdiag_kernel<<<dim3(gx, (unsigned)n), 256, 0, st>>>(A, n, ld);
+  return cudaGetLastError();
 }
 
 cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double* dst, int64_t ldd,

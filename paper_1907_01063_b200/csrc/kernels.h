@@ -117,6 +117,14 @@ cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const doubl
 cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double* dst, int64_t ldd,
                               const int* status, cudaStream_t st);
 
+// R0 + the split-K reduction of rows [j, j+B) (first write to them in the sweep):
+// dst[j+r][c] = [c <= j+r] src[j+r][c] - [c < kc] sum_z P[z][r][c] for c < N
+// (P: splits planes of B x kc; src may equal dst; 16-B aligned rows, N, kc even)
+cudaError_t adj_rows_init(const double* P, int splits, int B, int64_t kc, const double* src, int64_t lds, double* dst,
+                          int64_t ldd, int64_t j, int64_t N, const int* status, cudaStream_t st);
+// +0.0 into the strict upper triangle outside the 128 x 128 diagonal tiles
+cudaError_t zero_upper_offdiag(double* A, int64_t n, int64_t ld, cudaStream_t st);
+
 // ---- adjoint diagonal-block helpers (R4, R5) ----
 // (L[b*128.., b*128..])^-1 for b in [0, nblk), lower, by substitution; block b is
 // written with leading dimension ldo at Dinv + (b/per)*ostride + (b%per)*(128*ldo+128)

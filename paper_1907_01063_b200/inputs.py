@@ -76,6 +76,24 @@ def lbar(n: int, seed: int = LBAR_SEED) -> np.ndarray:
     return out
 
 
+def lbar_leading(n: int, m: int, seed: int = LBAR_SEED) -> np.ndarray:
+    """lbar(n, seed)[:m, :m] without drawing the whole n x n matrix (the same
+    row-block stream: only the blocks covering the first m rows are drawn)."""
+    m = min(m, n)
+    g = rng(seed)
+    out = np.empty((m, m), dtype=np.float64)
+    step = max(1, (1 << 24) // max(n, 1))
+    for r0 in range(0, m, step):
+        r1 = min(n, r0 + step)
+        blk = g.standard_normal((r1 - r0, n))
+        ii = np.arange(r0, r1)[:, None]
+        jj = np.arange(n)[None, :]
+        blk[jj > ii] = 0.0
+        take = min(r1, m) - r0
+        out[r0:r0 + take] = blk[:take, :m]
+    return out
+
+
 def toeplitz(n: int) -> np.ndarray:
     """The paper's Cholesky benchmark matrix."""
     i = np.arange(n)
