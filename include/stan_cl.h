@@ -148,7 +148,11 @@ int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_ba
  *                               place; both with leading dimension ld_local
  * Every rank must make the same sequence of calls (collectives inside).
  * Return values as the single-GPU calls (numerical status all-reduced with max);
- * STAN_CL_ENCCL when NCCL cannot be loaded or fails; STAN_CL_EINVAL for a bad
+ * STAN_CL_ENCCL when NCCL cannot be loaded or fails -- including an
+ * asynchronous communicator error or the stream not draining within
+ * STAN_CL_NCCL_TIMEOUT_S seconds (environment; default 1800, 0 = no limit):
+ * the call then aborts every communicator (ncclCommAbort) and returns instead
+ * of hanging, and the grid must be re-initialised; STAN_CL_EINVAL for a bad
  * grid, n % 256 != 0, or ld_local too small.  Library-owned scratch: about
  * (R_p + 1) * 256^2 doubles (+ C_q * 256^2 * (P + 3) for P > 1 / the adjoint).
  */
@@ -283,9 +287,12 @@ int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alp
  * info of each matrix (forward: first failing pivot + 1; adjoint: first
  * L[k][k] not finite and > 0, + 1).  Returns 0 when every matrix succeeded,
  * k > 0 when matrix k-1 is the first that failed, negative on errors
- * (n > 128 -> STAN_CL_EINVAL).  Forward: one CTA per matrix (the diagonal-tile
- * kernel, identity padded); adjoint: the paper's diagonal-block step on
- * 128 x 128 padded copies in chunks of 4096.  Device pointers; synchronous.
+ * (n > 128 -> STAN_CL_EINVAL).  Kernels: n <= 32 one warp per matrix, n <= 64
+ * two warps per matrix (rows in registers; forward bit-identical to the
+ * single-matrix path), 64 < n <= 128 one CTA per matrix (the diagonal-tile
+ * kernel, identity padded) and, for the adjoint, the paper's diagonal-block
+ * step on 128 x 128 padded copies in chunks of 4096.  The single-matrix calls
+ * use the n <= 64 kernels for n <= 64 as well.  Device pointers; synchronous.
  */
 int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* L, int* info);
 int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, const double* L_bar,

@@ -23,7 +23,10 @@
 #include <tuple>
 #include <mutex>
 #include <thread>
+#include <chrono>
 #include <vector>
+
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/stan_cl.h"
 #include "common.cuh"
@@ -102,13 +105,14 @@ inline size_t al(size_t b) { return (b + kAlign - 1) / kAlign * kAlign; }
 struct AdjPlan {
   int64_t N;    // padded order (multiple of B)
   int64_t B;    // adjoint block size: 128 or 256
-  size_t dinv, part, tmp, ctmp, hscr, total;
+  size_t dinv, part, tmp, ctmp, hscr, cs, total;
 };
+constexpr int kNumSms = 148;  // B200 (the persistent GEMMs size their grids from the device)
 
 // split-K factor for W = C_bar^T L[k:N, 0:k] (M = B rows; persistent TMA GEMM,
 // 128 x 64 output tiles, 32-deep slabs): minimise rounds-of-148 x per-item K
 // (+ a fixed per-item cost) plus the reduction's extra reads
-void splitk_choice(int64_t m, int64_t k, int64_t B, int* splits_out, int* kps_out) {
+void splitk_choice(int64_t m, int64_t k, int64_t B, int* splits_out, int* kps_out, int nsm = kNumSms) {
   const int ntiles = (int)((B / 128) * (k / 64));
   const int kmax = (int)(m / 32);
   double best = 1e300;
@@ -117,8 +121,8 @@ void splitk_choice(int64_t m, int64_t k, int64_t B, int* splits_out, int* kps_ou
     const int64_t kps = round_up((m + s - 1) / s, 32);
     const int eff_s = (int)((m + kps - 1) / kps);
     const int64_t items = (int64_t)ntiles * eff_s;
-    const int64_t rounds = (items + 147) / 148;
-    const double t = (double)rounds * (double)(kps + 96) + 3.0 * eff_s * 64 * (double)k * (B / 128) / (148.0 * 64);
+    const int64_t rounds = (items + nsm - 1) / nsm;
+    const double t = (double)rounds * (double)(kps + 96) + 3.0 * eff_s * 64 * (double)k * (B / 128) / (nsm * 64.0);
     if (t < best - 1e-9) {
       best = t;
       bs = s;
@@ -135,6 +139,25 @@ void splitk_choice(int64_t m, int64_t k, int64_t B, int* splits_out, int* kps_ou
 int64_t adj_block(int64_t n) {
   if (g.adj_nb) return g.adj_nb;
   return n >= 768 ? 2 * NB : NB;
+}
+
+// SMs given to the pipelined adjoint's dependency chain at step k (the rest
+// goes to the previous step's bulk update running beside it): proportional to
+// the two sides' DMMA work, at least 64 (the fused diagonal step's 64 CTAs
+// meet at grid barriers and must all be resident), at most 140 while the
+// bulk side has work
+int adj_chain_sms(int64_t N, int64_t B, int64_t k) {
+  const int64_t m = N - k, jprev = k;                            // previous step: j = k
+  const double wc = (double)m * k * B + (double)m * B * B + (double)(B + m) * B * B;
+  const double wm = (double)(B + std::max<int64_t>(m - B, 0)) * (double)std::max<int64_t>(jprev - 2 * B, 0) * B;
+  if (wm <= 0) return kNumSms;
+  static const int fixed = [] {
+    const char* e = getenv("STAN_CL_PIPE_CHAIN_SMS");  // tuning aid: fixed chain share
+    return e ? atoi(e) : 0;
+  }();
+  if (fixed > 0) return std::min(fixed, kNumSms);
+  int r = (int)std::lround(kNumSms * wc / (wc + wm));
+  return std::min(std::max(r, 64), kNumSms - 8);
 }
 
 AdjPlan adj_plan(int64_t n) {
@@ -157,7 +180,9 @@ AdjPlan adj_plan(int64_t n) {
   // scratch of the streamed host path's per-block D^-1 (copy stream): its own
   // region, since the reverse sweep already runs on the main stream meanwhile
   p.hscr = al((size_t)NB * NB * sizeof(double));
-  p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp + p.ctmp + p.hscr;
+  // pipelined sweep: three rotating [S; C_bar D^-1] buffers of (B + N) x B
+  p.cs = 3 * al((size_t)(p.B + p.N) * p.B * sizeof(double));
+  p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp + p.ctmp + p.hscr + p.cs;
   return p;
 }
 
@@ -255,8 +280,11 @@ int ensure_mat(int slot, size_t bytes, double** p) {
 
 // Scope of one public call: with a caller workspace, the outermost call lays
 // its buffers out afresh from the start of that workspace.
+// Also an NVTX range named after the entry point (visible in nsys / ncu
+// --nvtx; header-only NVTX v3, a no-op unless a tool is attached).
 struct CallScope {
-  CallScope() {
+  explicit CallScope(const char* name) {
+    nvtxRangePushA(name);
     if (g.depth++ == 0 && g.user_ws) {
       g.ws = g.user_ws;
       g.ws_cap = kHdr;
@@ -267,7 +295,10 @@ struct CallScope {
       }
     }
   }
-  ~CallScope() { --g.depth; }
+  ~CallScope() {
+    --g.depth;
+    nvtxRangePop();
+  }
 };
 
 // ------------------------------------------------------------------ forward
@@ -415,6 +446,15 @@ int cholesky_enqueue(int64_t n, const double* A, double* L, int* d_info) {
   if (rc) return rc;
   int* status = (int*)g.ws;
   cudaStream_t st = g.stream;
+  if (n <= 64) {
+    // one small matrix: the batched register kernels with batch 1 (one launch,
+    // no padded copies; the same arithmetic as the 128-tile kernel, so L is
+    // bit-identical to the blocked path); the kernel writes the info word
+    if (n <= 32) CK(potrf_batched_w32(A, L, (int)n, 1, status, st));
+    else CK(potrf_batched_w64(A, L, (int)n, 1, status, st));
+    if (d_info) CK(cudaMemcpyAsync(d_info, status, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    return STAN_CL_OK;
+  }
   CK(cudaMemsetAsync(status, 0, sizeof(int), st));
   // outer block: 256 (two-level) when it divides n, else 128 (set_block_size overrides)
   int64_t OB = g.nb;
@@ -554,6 +594,129 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
   return STAN_CL_OK;
 }
 
+// The blocked reverse sweep as a two-stream pipeline (device entry points).
+// Per step s (block [j, k), m = N - k) the dependency chain runs on the
+// high-priority side stream:
+//   C_bar D^-1 -> split-K C_bar^T [B C] -> R0 + reduce -> write-back C_bar ->
+//   fused diagonal step S -> the LOOKAHEAD column of the rank-B update
+//   ([S; C_bar D^-1] R on columns [j - B, j): the next step's C_bar)
+// and the rest of step s's rank-B update (columns [0, j - B), one GEMM for
+// both B_bar -= C_bar R and R_bar -= S R since they share R) runs on the main
+// stream BESIDE the chain of step s + 1, the SMs split between the two
+// persistent kernels in proportion to their DMMA work (adj_chain_sms).  The
+// columns [j - 2B, j - B) are updated first on the main stream and signalled:
+// they are the lookahead column of step s + 1.  Each element of A_bar receives
+// the same updates in the same order as in adjoint_inplace, from the same
+// kernels, so the result is bit-identical to the sequential sweep.
+int adjoint_pipelined(const double* Lw, double* Wm, int64_t N, int64_t ld, int* status, const AdjPlan& plan,
+                      const double* src, int64_t lds, bool two_streams = true) {
+  cudaStream_t main = g.stream;
+  const int64_t B = plan.B, nblk = N / B;
+  int rc = ensure_side((size_t)(3 * nblk + 4));
+  if (rc) return rc;
+  // no programmatic dependent launch here: a dependent kernel's CTAs would sit
+  // resident on SMs the other stream's persistent GEMM is sized to use
+  static const bool pdl_on = getenv("STAN_CL_PIPE_PDL") && atoi(getenv("STAN_CL_PIPE_PDL")) != 0;
+  struct PdlGuard {
+    bool on;
+    explicit PdlGuard(bool o) : on(o) { if (!on) pdl_allow(false); }
+    ~PdlGuard() { if (!on) pdl_allow(true); }
+  } pdl_guard_(pdl_on);
+  static const bool serial = getenv("STAN_CL_NO_LOOKAHEAD") != nullptr;  // debugging aid
+  cudaStream_t chain = (serial || !two_streams) ? main : g.side;
+  char* base = (char*)g.ws + al(sizeof(int) * 64);
+  double* Dinv = (double*)base;
+  double* Pbuf = (double*)(base + plan.dinv);
+  double* T1 = (double*)(base + plan.dinv + plan.part);
+  double* T2 = T1 + B * B;
+  double* T3 = T2 + B * B;
+  char* csb = base + plan.dinv + plan.part + plan.tmp + plan.ctmp + plan.hscr;
+  const size_t csz = al((size_t)(B + N) * B * sizeof(double));
+  rc = block_inverses(Lw, ld, B, 0, nblk, Dinv, Pbuf, status, main);
+  if (rc) return rc;
+  cudaEvent_t* ev = g.events.data();  // ev[0] start; step s: ev[1+3s] chain done, ev[2+3s] first cols, ev[3+3s] rest
+  if (two_streams) {
+    CK(cudaEventRecord(ev[0], main));
+    CK(cudaStreamWaitEvent(chain, ev[0], 0));
+  }
+  int64_t s = 0;
+  for (int64_t k = N; k > 0; k -= B, ++s) {
+    const int64_t j = k - B, m = N - k;
+    const double* D = Lw + j * ld + j;
+    const double* Db = Dinv + (j / B) * B * B;
+    const double* R = Lw + j * ld;  // L(j:k, 0:j)
+    double* Cb = Wm + k * ld + j;   // C_adj = L_adj(k:N, j:k)
+    double* Dbar = Wm + j * ld + j;
+    double* cs = (double*)(csb + (size_t)(s % 3) * csz);  // [S (B x B); C_bar D^-1 (m x B)]
+    const int chain_res = two_streams ? kNumSms - adj_chain_sms(N, B, k) : 0;
+    // the buffer's last reader (two streams only: with one stream the order is
+    // implied, and the events may last have been recorded inside a captured graph)
+    if (two_streams && s >= 3) CK(cudaStreamWaitEvent(chain, ev[3 + 3 * (s - 3)], 0));
+    if (m > 0) {
+      // C_adj = C_adj * lower_triangular_inverse(D)
+      CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, cs + B * B, B, status, chain, 0,
+                   PROF_TRMM, true, chain_res));
+      // [R_adj D_adj] -= C_adj^T [B C], split-K
+      // the split is the sequential sweep's (a function of m, k only), so the
+      // partial sums -- and every bit of the result -- match adjoint_inplace
+      int splits, kps;
+      splitk_choice(m, k, B, &splits, &kps);
+      CK(gemm_splitk_tn((int)B, (int)k, (int)m, splits, kps, cs + B * B, B, Lw + k * ld, ld, Pbuf, status, chain,
+                        chain_res));
+      if (src) CK(adj_rows_init(Pbuf, splits, (int)B, k, src, lds, Wm, ld, j, N, status, chain));
+      else CK(splitk_reduce_sub(Pbuf, splits, (int)B, (int)k, Wm + j * ld, ld, status, chain));
+      CK(copy_block(cs + B * B, B, Cb, ld, m, B, chain));
+    } else if (src) {
+      CK(adj_rows_init(nullptr, 0, (int)B, 0, src, lds, Wm, ld, j, N, status, chain));
+    }
+    // S = D^-T sym(D^T D_adj) D^-1, D_adj = Phi(S)
+    CK(adj_diag_fused((int)B, D, ld, Dbar, ld, Db, T1, T2, T3, cs, (unsigned*)status + 16, status, chain));
+    if (!two_streams) {
+      // one stream: [R_adj; B_adj] -= [S; C_adj] R over all of [0, j) in one launch
+      if (j > 0)
+        CK(gemm_full(true, false, (int)(B + m), (int)j, (int)B, -1.0, 1, cs, B, R, ld, Wm + j * ld, ld, status, main, 0,
+                     PROF_GEMM));
+      continue;
+    }
+    // [R_adj; B_adj] -= [S; C_adj] R on the lookahead column [j - B, j)
+    if (s >= 1) CK(cudaStreamWaitEvent(chain, ev[2 + 3 * (s - 1)], 0));
+    if (j >= B)
+      CK(gemm_full(true, false, (int)(B + m), (int)B, (int)B, -1.0, 1, cs, B, R + (j - B), ld, Wm + j * ld + (j - B),
+                   ld, status, chain, 0, PROF_GEMM, true, chain_res));
+    CK(cudaEventRecord(ev[1 + 3 * s], chain));
+    // main: the rest of the rank-B update beside the next chain step
+    CK(cudaStreamWaitEvent(main, ev[1 + 3 * s], 0));
+    const int main_res = (k - B > 0) ? adj_chain_sms(N, B, k - B) : 0;
+    if (j >= 2 * B)
+      CK(gemm_full(true, false, (int)(B + m), (int)B, (int)B, -1.0, 1, cs, B, R + (j - 2 * B), ld,
+                   Wm + j * ld + (j - 2 * B), ld, status, main, 0, PROF_GEMM, true, main_res));
+    CK(cudaEventRecord(ev[2 + 3 * s], main));
+    if (j > 2 * B)
+      CK(gemm_full(true, false, (int)(B + m), (int)(j - 2 * B), (int)B, -1.0, 1, cs, B, R, ld, Wm + j * ld, ld, status,
+                   main, 0, PROF_GEMM, true, main_res));
+    CK(cudaEventRecord(ev[3 + 3 * s], main));
+  }
+  if (two_streams) CK(cudaStreamWaitEvent(main, ev[1 + 3 * (s - 1)], 0));
+  return STAN_CL_OK;
+}
+
+// adjoint sweep variant (all three give bit-identical results):
+//   0 = adjoint_inplace (separate B_bar / R_bar updates, one stream),
+//   1 = two-stream pipeline, 2 = one stream with the merged [S; C_bar] R update.
+// Default (measured, profiles/r02_adjoint_variants.txt): the pipeline up to
+// N = 2048, where the chain's latency dominates (n = 1024: 0.416 vs 0.451 ms),
+// the merged single stream above, where splitting the SMs between two
+// persistent GEMMs costs more than the chain it hides (n = 16384: 96.8 vs 94.9 ms).
+int adj_pipe_mode(int64_t N = 0) {
+  static const int m = [] {
+    const char* e = getenv("STAN_CL_ADJ_PIPE");
+    return e ? atoi(e) : -1;
+  }();
+  if (m >= 0) return m;
+  return N <= 2048 ? 1 : 2;
+}
+bool adj_pipe_enabled(int64_t N) { return adj_pipe_mode(N) != 0; }
+
 int adjoint_enqueue(int64_t n, const double* L, const double* Lbar, double* Abar, int* d_info) {
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) {
@@ -569,13 +732,23 @@ int adjoint_enqueue(int64_t n, const double* L, const double* Lbar, double* Abar
   if (rc) return rc;
   int* status = (int*)g.ws;
   cudaStream_t st = g.stream;
+  if (n <= 64) {
+    // one small matrix: the batched kernel (the diagonal-block step of
+    // PAPER.md:313-321 on the whole matrix, in registers / shared memory);
+    // it reads everything before writing, so any aliasing is fine
+    if (n <= 32) CK(adjoint_batched_w32(L, Lbar, Abar, (int)n, 1, status, st));
+    else CK(adjoint_batched_w64(L, Lbar, Abar, (int)n, 1, status, st));
+    if (d_info) CK(cudaMemcpyAsync(d_info, status, sizeof(int), cudaMemcpyDeviceToDevice, st));
+    return STAN_CL_OK;
+  }
   CK(cudaMemsetAsync(status, 0, sizeof(int), st));
   CK(check_diag(L, n, n, status, st));
   const int64_t N = plan.N;
   const bool fast = (N == n) && aligned16(L) && aligned16(Lbar) && aligned16(Abar);
   if (fast) {
     // A_bar starts as tril(L_bar) row block by row block inside the sweep
-    rc = adjoint_inplace(L, Abar, n, n, status, plan, nullptr, nullptr, nullptr, Lbar, n);
+    rc = adj_pipe_enabled(n) ? adjoint_pipelined(L, Abar, n, n, status, plan, Lbar, n, adj_pipe_mode(n) == 1)
+                            : adjoint_inplace(L, Abar, n, n, status, plan, nullptr, nullptr, nullptr, Lbar, n);
     if (rc) return rc;
   } else {
     double *Lw = nullptr, *Wm = nullptr;
@@ -585,7 +758,8 @@ int adjoint_enqueue(int64_t n, const double* L, const double* Lbar, double* Abar
     if (rc) return rc;
     CK(copy_lower_pad(L, n, n, Lw, N, N, 1.0, st));
     CK(copy_lower_pad(Lbar, n, n, Wm, N, N, 0.0, st));
-    rc = adjoint_inplace(Lw, Wm, N, N, status, plan);
+    rc = adj_pipe_enabled(N) ? adjoint_pipelined(Lw, Wm, N, N, status, plan, nullptr, 0, adj_pipe_mode(N) == 1)
+                            : adjoint_inplace(Lw, Wm, N, N, status, plan);
     if (rc) return rc;
     CK(copy_lower_out(Wm, N, Abar, n, n, st));
   }
@@ -866,14 +1040,14 @@ int run_cached(const GraphKey& key, F&& enqueue) {
 extern "C" {
 
 int stan_cl_cholesky_async(int64_t n, const double* A, double* L, int* d_info) {
-  CallScope call_;
+  CallScope call_("stan_cl_cholesky_async");
   if (n <= 0) return cholesky_enqueue(n, A, L, d_info);
   return run_cached(GraphKey{0, n, {A, L, d_info, nullptr}, g.nb, 0},
                     [&] { return cholesky_enqueue(n, A, L, d_info); });
 }
 
 int stan_cl_cholesky(int64_t n, const double* A, double* L) {
-  CallScope call_;
+  CallScope call_("stan_cl_cholesky");
   int rc = stan_cl_cholesky_async(n, A, L, nullptr);
   if (rc || n == 0) return rc;
   return read_status();
@@ -881,21 +1055,21 @@ int stan_cl_cholesky(int64_t n, const double* A, double* L) {
 
 int stan_cl_cholesky_adjoint_async(int64_t n, const double* L, const double* L_bar, double* A_bar,
                                    int* d_info) {
-  CallScope call_;
+  CallScope call_("stan_cl_cholesky_adjoint_async");
   if (n <= 0) return adjoint_enqueue(n, L, L_bar, A_bar, d_info);
   return run_cached(GraphKey{1, n, {L, L_bar, A_bar, d_info}, g.adj_nb, 0},
                     [&] { return adjoint_enqueue(n, L, L_bar, A_bar, d_info); });
 }
 
 int stan_cl_cholesky_adjoint(int64_t n, const double* L, const double* L_bar, double* A_bar) {
-  CallScope call_;
+  CallScope call_("stan_cl_cholesky_adjoint");
   int rc = stan_cl_cholesky_adjoint_async(n, L, L_bar, A_bar, nullptr);
   if (rc || n == 0) return rc;
   return read_status();
 }
 
 int stan_cl_lower_triangular_inverse(int64_t n, const double* L, double* X) {
-  CallScope call_;
+  CallScope call_("stan_cl_lower_triangular_inverse");
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!L || !X) return STAN_CL_EINVAL;
@@ -928,7 +1102,7 @@ int stan_cl_lower_triangular_inverse(int64_t n, const double* L, double* X) {
 }
 
 int stan_cl_trsm(int64_t n, int64_t m, const double* L, const double* B, double* X, int trans) {
-  CallScope call_;
+  CallScope call_("stan_cl_trsm");
   if (n < 0 || m < 0) return STAN_CL_EINVAL;
   if (n == 0 || m == 0) return STAN_CL_OK;
   if (!L || !B || !X) return STAN_CL_EINVAL;
@@ -951,7 +1125,7 @@ int stan_cl_trsm(int64_t n, int64_t m, const double* L, const double* B, double*
 
 int stan_cl_trsm_adjoint(int64_t n, int64_t m, const double* L, const double* C, const double* C_bar,
                          double* L_bar, double* B_bar) {
-  CallScope call_;
+  CallScope call_("stan_cl_trsm_adjoint");
   if (n < 0 || m < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!L || !L_bar || (m > 0 && (!C || !C_bar || !B_bar))) return STAN_CL_EINVAL;
@@ -1006,7 +1180,7 @@ int stan_cl_trsm_adjoint(int64_t n, int64_t m, const double* L, const double* C,
 }
 
 int stan_cl_trsv(int64_t n, const double* L, const double* b, double* x, int trans) {
-  CallScope call_;
+  CallScope call_("stan_cl_trsv");
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
   if (!L || !b || !x) return STAN_CL_EINVAL;
@@ -1027,7 +1201,7 @@ int stan_cl_trsv(int64_t n, const double* L, const double* b, double* x, int tra
 
 int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alpha, double rho, double sigma,
                          double* out, double* y_bar) {
-  CallScope call_;
+  CallScope call_("stan_cl_gp_lpdf_grad");
   if (n < 0) return STAN_CL_EINVAL;
   if (n > 0 && (!x || !y || !out)) return STAN_CL_EINVAL;
   if (!(rho != 0.0) || !(rho - rho == 0.0) || !(alpha - alpha == 0.0) || !(sigma - sigma == 0.0))
@@ -1067,7 +1241,7 @@ int stan_cl_gp_lpdf_grad(int64_t n, const double* x, const double* y, double alp
 
 // ---- NEXT-4: batched small matrices ----------------------------------------
 int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* L, int* info) {
-  CallScope call_;
+  CallScope call_("stan_cl_cholesky_batched");
   if (batch < 0 || n < 0 || n > NB) return STAN_CL_EINVAL;
   if (batch == 0 || n == 0) return STAN_CL_OK;
   if (!A || !L) return STAN_CL_EINVAL;
@@ -1085,6 +1259,8 @@ int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* 
   cudaStream_t st = g.stream;
   if (n <= 32) {
     CK(potrf_batched_w32(A, L, (int)n, batch, inf, st));
+  } else if (n <= 64) {
+    CK(potrf_batched_w64(A, L, (int)n, batch, inf, st));
   } else {
     CK(cudaMemsetAsync(inf, 0, sizeof(int) * (size_t)batch, st));
     CK(potrf_batched(A, L, (int)n, batch, inf, st));
@@ -1095,7 +1271,7 @@ int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* 
 
 int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, const double* L_bar,
                                      double* A_bar, int* info) {
-  CallScope call_;
+  CallScope call_("stan_cl_cholesky_adjoint_batched");
   if (batch < 0 || n < 0 || n > NB) return STAN_CL_EINVAL;
   if (batch == 0 || n == 0) return STAN_CL_OK;
   if (!L || !L_bar || !A_bar) return STAN_CL_EINVAL;
@@ -1104,7 +1280,7 @@ int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, 
   if (L_bar != A_bar && ranges_overlap(L_bar, A_bar, bytes)) return STAN_CL_EINVAL;
   int rc = ensure_ws(al(sizeof(int) * 64));
   if (rc) return rc;
-  if (n <= 32) {  // one warp per matrix, no padded copies
+  if (n <= 64) {  // one or two warps per matrix, no padded copies
     int* inf = info;
     if (!inf) {
       double* p = nullptr;
@@ -1112,7 +1288,8 @@ int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, 
       inf = (int*)p;
     }
     cudaStream_t st = g.stream;
-    CK(adjoint_batched_w32(L, L_bar, A_bar, (int)n, batch, inf, st));
+    if (n <= 32) CK(adjoint_batched_w32(L, L_bar, A_bar, (int)n, batch, inf, st));
+    else CK(adjoint_batched_w64(L, L_bar, A_bar, (int)n, batch, inf, st));
     CK(batched_first_fail(inf, batch, (int*)g.ws, st));
     return read_status();
   }
@@ -1230,7 +1407,7 @@ struct HostUpperZero {
 };
 
 int stan_cl_cholesky_host(int64_t n, const double* A, double* L) {
-  CallScope call_;
+  CallScope call_("stan_cl_cholesky_host");
   PdlOff pdl_off_;
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
@@ -1290,7 +1467,7 @@ int adjoint_host_enqueue(int64_t n, const double* L, const double* L_bar, double
 }
 
 int stan_cl_cholesky_adjoint_host(int64_t n, const double* L, const double* L_bar, double* A_bar) {
-  CallScope call_;
+  CallScope call_("stan_cl_cholesky_adjoint_host");
   PdlOff pdl_off_;
   if (n < 0) return STAN_CL_EINVAL;
   if (n == 0) return STAN_CL_OK;
@@ -1370,7 +1547,7 @@ size_t stan_cl_trsm_workspace_bytes(int64_t n, int64_t m) {
 size_t stan_cl_batched_workspace_bytes(int64_t batch, int64_t n, int with_info) {
   if (batch <= 0 || n <= 0) return kHdr;
   const size_t inf = with_info ? 0 : al(sizeof(int) * (size_t)batch);
-  if (n <= 32) return kHdr + inf;
+  if (n <= 64) return kHdr + inf;
   const size_t chunk = (size_t)std::min<int64_t>(batch, 4096);
   return kHdr + al(sizeof(double) * 4 * chunk * (size_t)NB * NB) + inf;
 }
@@ -1532,6 +1709,8 @@ struct NcclApi {
   ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
   ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*commGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;  // optional
+  ncclResult_t (*commAbort)(ncclComm_t) = nullptr;                        // optional
   bool load() {
     if (h) return true;
     const char* env = getenv("STAN_CL_NCCL_LIB");
@@ -1549,6 +1728,8 @@ struct NcclApi {
     reduce = (decltype(reduce))dlsym(h, "ncclReduce");
     allReduce = (decltype(allReduce))dlsym(h, "ncclAllReduce");
     commDestroy = (decltype(commDestroy))dlsym(h, "ncclCommDestroy");
+    commGetAsyncError = (decltype(commGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
+    commAbort = (decltype(commAbort))dlsym(h, "ncclCommAbort");
     return getUniqueId && commInitRank && commSplit && broadcast && reduce && allReduce && commDestroy;
   }
 };
@@ -2103,17 +2284,64 @@ int stan_cl_dist_init(int nranks, int rank, const void* id128, int P, int Q) {
   return STAN_CL_OK;
 }
 
+// abort every communicator of the grid (after an asynchronous NCCL error or a
+// timeout: a peer died or stopped issuing collectives); the grid must be
+// re-initialised with stan_cl_dist_init
+static void dist_abort(const char* why) {
+  snprintf(g.last_err, sizeof(g.last_err), "NCCL: %s; communicators aborted", why);
+  for (ncclComm_t* c : {&g_dist.rowc, &g_dist.colc, &g_dist.comm}) {
+    if (*c) {
+      if (g_nccl.commAbort) g_nccl.commAbort(*c);
+      *c = nullptr;
+    }
+  }
+  g_dist = DistState{};
+}
+
+// wait for the library stream while watching the communicators: returns
+// STAN_CL_ENCCL (after aborting them) on an asynchronous NCCL error or when the
+// stream has not drained within STAN_CL_NCCL_TIMEOUT_S seconds (default 1800;
+// 0 = wait forever), instead of hanging in cudaStreamSynchronize
+static int dist_wait() {
+  static const double timeout_s = [] {
+    const char* e = getenv("STAN_CL_NCCL_TIMEOUT_S");
+    return e ? atof(e) : 1800.0;
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (unsigned it = 0;; ++it) {
+    const cudaError_t e = cudaStreamQuery(g.stream);
+    if (e == cudaSuccess) return STAN_CL_OK;
+    if (e != cudaErrorNotReady) return cuda_fail(e, "dist_wait");
+    if (g_nccl.commGetAsyncError) {
+      for (ncclComm_t c : {g_dist.comm, g_dist.rowc, g_dist.colc}) {
+        ncclResult_t r = ncclSuccess;
+        if (c && g_nccl.commGetAsyncError(c, &r) == ncclSuccess && r != ncclSuccess && r != ncclInProgress) {
+          dist_abort("asynchronous error");
+          return STAN_CL_ENCCL;
+        }
+      }
+    }
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (timeout_s > 0 && el > timeout_s) {
+      dist_abort("timeout waiting for the collectives");
+      return STAN_CL_ENCCL;
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(it < 1000 ? 20 : 500));
+  }
+}
+
 static int dist_status_allreduce(int rc) {
   if (rc) return rc;
   // "did anything fail": status words are 0 or row+1; the max is a failing row
   int* status = (int*)g.ws;
   if (g_nccl.allReduce(status, status, 1, ncclInt32, ncclMax, g_dist.comm, g.stream) != ncclSuccess)
     return STAN_CL_ENCCL;
+  if ((rc = dist_wait())) return rc;
   return read_status();
 }
 
 int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local) {
-  CallScope call_;
+  CallScope call_("stan_cl_dist_cholesky");
   if (!g_dist.comm || (nb != 0 && nb != (int)DB)) return STAN_CL_EINVAL;
   double* Ws[1] = {A_local};
   const int p = g_dist.rank / g_dist.Q, q = g_dist.rank % g_dist.Q;
@@ -2123,7 +2351,7 @@ int stan_cl_dist_cholesky(int64_t n, int nb, double* A_local, int64_t ld_local) 
 
 int stan_cl_dist_cholesky_adjoint(int64_t n, int nb, const double* L_local, double* Lbar_to_Abar_local,
                                   int64_t ld_local) {
-  CallScope call_;
+  CallScope call_("stan_cl_dist_cholesky_adjoint");
   if (!g_dist.comm || (nb != 0 && nb != (int)DB)) return STAN_CL_EINVAL;
   const double* Ls[1] = {L_local};
   double* Ws[1] = {Lbar_to_Abar_local};
@@ -2134,7 +2362,7 @@ int stan_cl_dist_cholesky_adjoint(int64_t n, int nb, const double* L_local, doub
 
 int stan_cl_dist_trace(int64_t n, int P, int Q, int p, int q, int adjoint, const double* L_local,
                        double* A_local, int64_t ld_local, int64_t* out, int64_t max_entries) {
-  CallScope call_;
+  CallScope call_("stan_cl_dist_trace");
   if (P < 1 || Q < 1 || p < 0 || p >= P || q < 0 || q >= Q || max_entries < 0 || (max_entries && !out))
     return STAN_CL_EINVAL;
   std::vector<TraceEntry> tr;
@@ -2176,7 +2404,7 @@ int stan_cl_gp_exp_quad_cov_cols(int64_t n, const double* x, double alpha, doubl
 }
 
 int stan_cl_dist_sim2_cholesky(int64_t n, int P, int Q, double* const* A_locals, int64_t ld_local) {
-  CallScope call_;
+  CallScope call_("stan_cl_dist_sim2_cholesky");
   if (!A_locals || P < 1 || Q < 1) return STAN_CL_EINVAL;
   int rc = dist_run(false, n, P, Q, true, 0, 0, nullptr, A_locals, ld_local);
   return (rc || n == 0) ? rc : read_status();
@@ -2184,7 +2412,7 @@ int stan_cl_dist_sim2_cholesky(int64_t n, int P, int Q, double* const* A_locals,
 
 int stan_cl_dist_sim2_cholesky_adjoint(int64_t n, int P, int Q, const double* const* L_locals,
                                        double* const* W_locals, int64_t ld_local) {
-  CallScope call_;
+  CallScope call_("stan_cl_dist_sim2_cholesky_adjoint");
   if (!L_locals || !W_locals || P < 1 || Q < 1) return STAN_CL_EINVAL;
   int rc = dist_run(true, n, P, Q, true, 0, 0, L_locals, W_locals, ld_local);
   return (rc || n == 0) ? rc : read_status();

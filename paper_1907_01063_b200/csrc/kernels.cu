@@ -741,6 +741,175 @@ __global__ void __launch_bounds__(128) adjoint_w32_kernel(const double* L, const
   }
 }
 
+// ---- NEXT-4, 32 < n <= 64: 64 threads (two warps) per matrix, two matrices
+// per CTA, each half synchronised by its own named barrier ----
+__device__ __forceinline__ void bar_half(int h) { asm volatile("bar.sync %0, 64;" ::"r"(1 + h) : "memory"); }
+
+// forward: thread r holds row r (identity padded to 64) in registers; per
+// column j the owner of row j forms the pivot's correctly rounded sqrt and
+// reciprocal, the rows below divide (Markstein quotient) and publish the
+// column, and every row takes the rank-1 update fma(-l_rj, l_cj, a) -- the
+// arithmetic of the diagonal-tile kernel, so L is bit-identical to the
+// single-matrix path (which pads n <= 64 to one 128 tile).
+template <int J>
+__device__ __forceinline__ void potrf_w64_step(double (&row)[64], int t, int h, double* col, double* piv, int& bad) {
+  if (t == J) {
+    const double d = row[J];
+    double sq, y;
+    scaled_sqrt_rcp(d, sq, y);
+    piv[0] = sq;
+    piv[1] = y;
+    piv[2] = (d > 0.0) ? 0.0 : 1.0;
+  }
+  bar_half(h);
+  const double sq = piv[0], y = piv[1];
+  if (bad < 0 && piv[2] != 0.0) bad = J;
+  if (t == J) row[J] = sq;
+  else if (t > J) row[J] = div_pos(row[J], sq, y);
+  col[t] = row[J];
+  bar_half(h);
+  // unpredicated: rows t <= J only touch their (never written) upper part
+#pragma unroll
+  for (int c = J + 1; c < 64; ++c) row[c] = fma(-row[J], col[c], row[c]);
+  if constexpr (J + 1 < 64) potrf_w64_step<J + 1>(row, t, h, col, piv, bad);
+}
+
+__global__ void __launch_bounds__(128) potrf_w64_kernel(const double* A, double* L, int n, int64_t batch,
+                                                       int* info) {
+  __shared__ double col[2][64];
+  __shared__ double piv[2][4];
+  const int t = threadIdx.x & 63, h = threadIdx.x >> 6;
+  const int64_t b = (int64_t)blockIdx.x * 2 + h;
+  if (b >= batch) return;  // uniform per half (the halves never share a barrier)
+  const double* Ab = A + b * n * n;
+  double row[64];
+#pragma unroll
+  for (int c = 0; c < 64; ++c)
+    row[c] = (t < n) ? ((c <= t && c < n) ? Ab[(int64_t)t * n + c] : 0.0) : (c == t ? 1.0 : 0.0);
+  int bad = -1;
+  potrf_w64_step<0>(row, t, h, col[h], piv[h], bad);
+  double* Lb = L + b * n * n;
+  if (t < n) {
+#pragma unroll
+    for (int c = 0; c < 64; ++c)
+      if (c < n) Lb[(int64_t)t * n + c] = (c <= t) ? row[c] : 0.0;
+  }
+  if (t == 0) info[b] = bad >= 0 ? bad + 1 : 0;
+}
+
+// adjoint: the diagonal-block step on the whole (<= 64, identity/zero padded)
+// matrix as in adjoint_w32_kernel, rows over 64 threads:
+//   P = D^T D_bar; M = sym(tril P); X = D^-1 (columns by substitution);
+//   T = M X; S = X^T T; A_bar = Phi(tril S)
+constexpr int W64P = 65;
+constexpr int W64_SMEM = 3 * 64 * W64P * (int)sizeof(double);
+__global__ void __launch_bounds__(64) adjoint_w64_kernel(const double* L, const double* Lbar, double* Abar, int n,
+                                                        int64_t batch, int* info) {
+  extern __shared__ double smw[];
+  const int t = threadIdx.x;
+  const int64_t b = blockIdx.x;
+  double* D = smw;              // D, later T
+  double* M = D + 64 * W64P;    // D_bar, later M
+  double* X = M + 64 * W64P;    // D^-1
+  __shared__ int badv;
+  const double* Lb = L + b * n * n;
+  const double* Wb = Lbar + b * n * n;
+  if (t == 0) badv = 0x7fffffff;
+  for (int c = 0; c < 64; ++c) {
+    const bool in = t < n && c < n && c <= t;
+    D[t * W64P + c] = in ? Lb[(int64_t)t * n + c] : (t >= n && c == t ? 1.0 : 0.0);
+    M[t * W64P + c] = in ? Wb[(int64_t)t * n + c] : 0.0;
+  }
+  __syncthreads();
+  const double dii = D[t * W64P + t];
+  if (t < n && (!(dii > 0.0) || !isfinite(dii))) atomicMin(&badv, t);
+  // P row t, lower part: P[i][j] = sum_k D[k][i] D_bar[k][j]
+  double acc[64];
+#pragma unroll
+  for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < 64; ++k) {
+    const double dki = D[k * W64P + t];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = fma(dki, M[k * W64P + j], acc[j]);
+  }
+  __syncthreads();
+  // M = sym(tril P)
+#pragma unroll
+  for (int j = 0; j < 64; ++j)
+    if (j <= t) M[t * W64P + j] = acc[j];
+  // X = D^-1, column t: x_t = 1/D_tt, x_i = -(sum_{k=t}^{i-1} D_ik x_k) / D_ii
+  // (x_k kept in the column of X itself: no 64-entry register array)
+  for (int i = 0; i < 64; ++i) {
+    double xi;
+    if (i < t) {
+      xi = 0.0;
+    } else if (i == t) {
+      xi = 1.0 / D[i * W64P + i];
+    } else {
+      double s = 0.0;
+      for (int k = t; k < i; ++k) s = fma(D[i * W64P + k], X[k * W64P + t], s);
+      xi = -s / D[i * W64P + i];
+    }
+    X[i * W64P + t] = xi;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 64; ++j)
+    if (j > t) M[t * W64P + j] = M[j * W64P + t];
+  __syncthreads();
+  // T = M X, row t
+#pragma unroll
+  for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < 64; ++k) {
+    const double mik = M[t * W64P + k];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = fma(mik, X[k * W64P + j], acc[j]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 64; ++j) D[t * W64P + j] = acc[j];  // T over D
+  __syncthreads();
+  // S = X^T T, row t: S[i][j] = sum_k X[k][i] T[k][j];  A_bar = Phi(tril S)
+#pragma unroll
+  for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+#pragma unroll 2
+  for (int k = 0; k < 64; ++k) {
+    const double xki = X[k * W64P + t];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = fma(xki, D[k * W64P + j], acc[j]);
+  }
+  double* Ab = Abar + b * n * n;
+  if (t < n) {
+#pragma unroll
+    for (int j = 0; j < 64; ++j)
+      if (j < n) Ab[(int64_t)t * n + j] = (j < t) ? acc[j] : (j == t ? 0.5 * acc[j] : 0.0);
+  }
+  if (t == 0) info[b] = badv == 0x7fffffff ? 0 : badv + 1;
+}
+
+cudaError_t potrf_batched_w64(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st) {
+  Prof prof_(PROF_POTRF, (double)batch * n * n * n / 3.0, st, 8.0 * batch * n * (n + 1));
+  if (batch == 0) return cudaSuccess;
+  potrf_w64_kernel<<<(unsigned)((batch + 1) / 2), 128, 0, st>>>(A, L, n, batch, info);
+  return cudaGetLastError();
+}
+
+cudaError_t adjoint_batched_w64(const double* L, const double* Lbar, double* Abar, int n, int64_t batch, int* info,
+                                cudaStream_t st) {
+  Prof prof_(PROF_SMALL, (double)batch * 2.0 * n * n * n, st, 24.0 * batch * n * n);
+  if (batch == 0) return cudaSuccess;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(adjoint_w64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, W64_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  adjoint_w64_kernel<<<(unsigned)batch, 64, W64_SMEM, st>>>(L, Lbar, Abar, n, batch, info);
+  return cudaGetLastError();
+}
+
 cudaError_t potrf_batched_w32(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st) {
   Prof prof_(PROF_POTRF, (double)batch * n * n * n / 3.0, st, 8.0 * batch * n * (n + 1));
   if (batch == 0) return cudaSuccess;
@@ -993,11 +1162,11 @@ cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const doub
 
 cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const double* A, int64_t lda,
                            const double* B, int64_t ldb, double* P, const int* status,
-                           cudaStream_t st) {
+                           cudaStream_t st, int reserve_sms) {
   if (M == 0 || N == 0) return cudaSuccess;
   Prof prof_(PROF_SPLITK, 2.0 * M * N * K, st, 8.0 * ((double)M * K + (double)K * N) + 8.0 * splits * (double)M * N);
   GemmArgs p{A, lda, B, ldb, P, N, M, N, K, kps, 1.0, 0, 0, status, cfgsel().pingpong};
-  if (cfgsel().tma_splitk) return launch_tma<tg::CfgT32, false, false, MODE_SPLITK>(p, splits, st);
+  if (cfgsel().tma_splitk) return launch_tma<tg::CfgT32, false, false, MODE_SPLITK>(p, splits, st, reserve_sms);
   switch (cfgsel().splitk) {
     case CFG_MID: return launch_gemm<gemm::CfgMid, false, false, MODE_SPLITK>(p, splits, st);
     case CFG_W8: return launch_gemm<gemm::CfgW8, false, false, MODE_SPLITK>(p, splits, st);
@@ -1056,12 +1225,17 @@ __global__ void adj_rows_init_kernel(const double* __restrict__ P, int splits, i
       v = *reinterpret_cast<const double2*>(srow + c);
       if (c + 1 > gr) v.y = 0.0;
     }
-    if (c < kc) {
-      for (int z = 0; z < splits; ++z) {
+    if (c < kc && splits > 0) {
+      // the partials summed first, in split order, then subtracted: the same
+      // arithmetic as splitk_reduce_sub (results bit-identical to the unfused path)
+      double2 t = *reinterpret_cast<const double2*>(prow + c);
+      for (int z = 1; z < splits; ++z) {
         const double2 q = *reinterpret_cast<const double2*>(prow + z * plane + c);
-        v.x -= q.x;
-        v.y -= q.y;
+        t.x += q.x;
+        t.y += q.y;
       }
+      v.x -= t.x;
+      v.y -= t.y;
     }
     *reinterpret_cast<double2*>(drow + c) = v;
   }
@@ -1105,11 +1279,50 @@ cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double*
 }
 
 // ------------------------------------------------------------- R1/R4 helpers
-// D^-1 of each 128 x 128 diagonal block of L, column c by thread c:
-//   x_c = 1 / D[c][c];  x_i = -(sum_{k=c}^{i-1} D[i][k] x_k) / D[i][i],  i > c
-// (lower_triangular_inverse of PAPER.md:207-225, by substitution per column)
-constexpr int TRI_PACKED = NB * (NB + 1) / 2;  // D lower triangle, row i at i(i+1)/2
-constexpr int TINV_SMEM = (TRI_PACKED + NB * TP) * (int)sizeof(double);
+// D^-1 of each 128 x 128 diagonal block of L (lower_triangular_inverse of
+// PAPER.md:207-225, the paper's own scheme inside one CTA): the four 32 x 32
+// diagonal blocks are inverted by substitution, one warp each with lane c
+// holding column c in registers,
+//   x_c = 1 / D_cc;  x_i = -(sum_{k=c}^{i-1} D_ik x_k) / D_ii,  i > c,
+// then two doubling levels complete the off-diagonal blocks,
+//   [[C1, 0], [A3, C2]]^-1 = [[C1^-1, 0], [-C2^-1 A3 C1^-1, C2^-1]]
+// (32 -> 64 for both pairs, 64 -> 128), the products as FMA dot products in
+// ascending k.  The old one-column-per-thread substitution ran a dependent
+// chain of ~8k FMAs per thread (124 us per launch; this: ~10 us).
+constexpr int TI_XP = NB + 1;                 // pitch of the 128 x 128 inverse
+constexpr int TI_SP = 65;                     // pitch of the staging tiles
+constexpr int TINV_SMEM = (NB * TI_XP + 2 * 64 * TI_SP) * (int)sizeof(double);
+
+// C[M x N] (ldc) = sign * A[M x K] (lda) B[K x N] (ldb) in shared memory by
+// NT threads (thread index u), each an RM x RN register micro-tile, k ascending
+// (A reads are broadcasts within a half-warp; RM + RN loads per RM RN FMAs)
+template <int M, int N, int K, int RM, int RN>
+__device__ __forceinline__ void ti_gemm(const double* A, int lda, const double* B, int ldb, double* C, int ldc,
+                                        double sign, int u) {
+  constexpr int CG = N / RN;  // column groups
+  const int r0 = (u / CG) * RM, c0 = (u % CG) * RN;
+  double acc[RM][RN];
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) acc[i][j] = 0.0;
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    double a[RM], bb[RN];
+#pragma unroll
+    for (int i = 0; i < RM; ++i) a[i] = A[(r0 + i) * lda + k];
+#pragma unroll
+    for (int j = 0; j < RN; ++j) bb[j] = B[k * ldb + c0 + j];
+#pragma unroll
+    for (int i = 0; i < RM; ++i)
+#pragma unroll
+      for (int j = 0; j < RN; ++j) acc[i][j] = fma(a[i], bb[j], acc[i][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < RM; ++i)
+#pragma unroll
+    for (int j = 0; j < RN; ++j) C[(r0 + i) * ldc + c0 + j] = sign * acc[i][j];
+}
 
 __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, int64_t ld,
                                                              double* Dinv, int64_t ldo, int64_t ostride,
@@ -1117,34 +1330,73 @@ __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, in
                                                              const int* status) {
   if (cta_status_set(status)) return;
   extern __shared__ double sm[];
-  double* D = sm;               // packed lower: D[i][k] at i(i+1)/2 + k
-  double* X = sm + TRI_PACKED;  // X[c][i] = (D^-1)[i][c]  (column c of the inverse, contiguous)
-  const int b = blockIdx.x, c = threadIdx.x;
-  // block b: the b-th diagonal block of L, or (istride > 0) diagonal half b % per
-  // of the tile at (b / per) * istride
+  double* X = sm;                   // [128][TI_XP] the inverse (lower; +0.0 above)
+  double* S1 = X + NB * TI_XP;      // [64][TI_SP] staging: diagonal blocks, then A3
+  double* S2 = S1 + 64 * TI_SP;     // [64][TI_SP] T = A3 C1
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = blockIdx.x;
   const double* src = istride > 0 ? L + (long long)(b / per) * istride + (long long)(b % per) * (NB * ld + NB)
                                   : L + (long long)b * NB * ld + (long long)b * NB;
-  for (int idx = c; idx < NB * NB; idx += NB) {
-    const int i = idx >> 7, k = idx & (NB - 1);
-    if (k <= i) D[i * (i + 1) / 2 + k] = src[(long long)i * ld + k];
+  // zero X (the strict upper blocks stay +0.0)
+  for (int idx = tid; idx < NB * TI_XP; idx += NB) X[idx] = 0.0;
+  // (1) stage the four 32 x 32 diagonal blocks: block w at rows 32 (w & 1), columns 32 (w >> 1) of S1
+  for (int idx = tid; idx < 4 * 32 * 32; idx += NB) {
+    const int w = idx >> 10, i = (idx >> 5) & 31, k = idx & 31;
+    const double v = (k <= i) ? src[(long long)(32 * w + i) * ld + 32 * w + k] : 0.0;
+    S1[(32 * (w & 1) + i) * TI_SP + 32 * (w >> 1) + k] = v;
   }
   __syncthreads();
-  double* x = X + c * TP;
-  for (int i = 0; i < c; ++i) x[i] = 0.0;
-  x[c] = 1.0 / D[c * (c + 1) / 2 + c];
-  for (int i = c + 1; i < NB; ++i) {
-    double s = 0.0;
-    const double* di = D + i * (i + 1) / 2;
-    for (int k = c; k < i; ++k) s = fma(di[k], x[k], s);
-    x[i] = -s / di[i];
+  {
+    const double* Dw = S1 + 32 * (warp & 1) * TI_SP + 32 * (warp >> 1);
+    const int c = lane;
+    double x[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k)
+        if (k >= c) s = fma(Dw[i * TI_SP + k], x[k], s);
+      const double di = Dw[i * TI_SP + i];
+      x[i] = (i < c) ? 0.0 : (i == c ? 1.0 / di : -s / di);
+    }
+    double* Xw = X + 32 * warp * TI_XP + 32 * warp;
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (i >= c) Xw[i * TI_XP + c] = x[i];
   }
+  __syncthreads();
+  // (2) 32 -> 64, both pairs: A3 = D[64p + 32 .., 64p ..] (32 x 32) into S1 columns 32 p
+  for (int idx = tid; idx < 2 * 32 * 32; idx += NB) {
+    const int p = idx >> 10, i = (idx >> 5) & 31, k = idx & 31;
+    S1[i * TI_SP + 32 * p + k] = src[(long long)(64 * p + 32 + i) * ld + 64 * p + k];
+  }
+  __syncthreads();
+  // T_p = A3_p C1_p  (C1_p = X[64p.., 64p..])  -> S2 columns 32 p; pair p on threads 64p..
+  {
+    const int p = tid >> 6, u = tid & 63;
+    ti_gemm<32, 32, 32, 4, 4>(S1 + 32 * p, TI_SP, X + 64 * p * TI_XP + 64 * p, TI_XP, S2 + 32 * p, TI_SP, 1.0, u);
+    __syncthreads();
+    // C3_p = -C2_p T_p  (C2_p = X[64p + 32.., 64p + 32..])  -> X[64p + 32.., 64p..]
+    ti_gemm<32, 32, 32, 4, 4>(X + (64 * p + 32) * TI_XP + 64 * p + 32, TI_XP, S2 + 32 * p, TI_SP,
+                              X + (64 * p + 32) * TI_XP + 64 * p, TI_XP, -1.0, u);
+  }
+  __syncthreads();
+  // (3) 64 -> 128: A3 = D[64.., 0..64] into S1; T = A3 C1 -> S2; C3 = -C2 T -> X[64.., 0..64]
+  for (int idx = tid; idx < 64 * 64; idx += NB) {
+    const int i = idx >> 6, k = idx & 63;
+    S1[i * TI_SP + k] = src[(long long)(64 + i) * ld + k];
+  }
+  __syncthreads();
+  ti_gemm<64, 64, 64, 8, 4>(S1, TI_SP, X, TI_XP, S2, TI_SP, 1.0, tid);
+  __syncthreads();
+  ti_gemm<64, 64, 64, 8, 4>(X + 64 * TI_XP + 64, TI_XP, S2, TI_SP, X + 64 * TI_XP, TI_XP, -1.0, tid);
   __syncthreads();
   // block b lands in output group b / per (stride ostride), sub-block b % per
   // (offset ohalf): per = 2 places consecutive 128-blocks on the diagonal of 256 x 256 blocks
   double* dst = Dinv + (long long)(b / per) * ostride + (long long)(b % per) * ohalf;
-  for (int idx = c; idx < NB * NB; idx += NB) {
+  for (int idx = tid; idx < NB * NB; idx += NB) {
     const int i = idx >> 7, k = idx & (NB - 1);
-    dst[(long long)i * ldo + k] = X[k * TP + i];
+    dst[(long long)i * ldo + k] = X[i * TI_XP + k];
   }
 }
 

@@ -112,7 +112,7 @@ cudaError_t gemm_lower_nt(int M, int K, const double* A, int64_t lda, const doub
 // split-K: P[z][M][N] = op(A) op(B) over K range z*kps..; a_kmaj=false, b_kmaj=false only
 cudaError_t gemm_splitk_tn(int M, int N, int K, int splits, int kps, const double* A, int64_t lda,
                            const double* B, int64_t ldb, double* P, const int* status,
-                           cudaStream_t st);
+                           cudaStream_t st, int reserve_sms = 0);
 // dst[r][c] -= sum_{z=0}^{splits-1} P[z][r][c]  (fixed order), r < M, c < N
 cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double* dst, int64_t ldd,
                               const int* status, cudaStream_t st);
@@ -164,6 +164,10 @@ cudaError_t potrf_batched(const double* A, double* L, int n, int64_t batch, int*
 // n <= 32: one warp per matrix (info written, no zeroing needed)
 cudaError_t potrf_batched_w32(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st);
 cudaError_t adjoint_batched_w32(const double* L, const double* Lbar, double* Abar, int n, int64_t batch, int* info,
+                                cudaStream_t st);
+// 32 < n <= 64: two warps per matrix (forward: bit-identical to the tile kernel)
+cudaError_t potrf_batched_w64(const double* A, double* L, int n, int64_t batch, int* info, cudaStream_t st);
+cudaError_t adjoint_batched_w64(const double* L, const double* Lbar, double* Abar, int n, int64_t batch, int* info,
                                 cudaStream_t st);
 // batched.cu: the adjoint of the batched factorization and helpers
 cudaError_t batched_pad(const double* L, const double* Lbar, int n, int64_t batch, double* Lp, double* Wp,

@@ -28,8 +28,8 @@ def relf(a, b):
     return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
 
 
-@pytest.mark.parametrize("batch,n", [(1, 1), (3, 2), (7, 5), (1001, 17), (64, 32), (257, 64), (33, 100),
-                                     (20, 128)])
+@pytest.mark.parametrize("batch,n", [(1, 1), (3, 2), (7, 5), (1001, 17), (64, 32), (5, 33), (99, 48), (257, 64),
+                                     (33, 100), (20, 128)])
 def test_cholesky_batched_parity(sc, batch, n):
     A = se_batch(batch, n)
     L, info = sc.cholesky_batched(torch.from_numpy(A).cuda())
@@ -62,7 +62,8 @@ def test_cholesky_batched_integer_exact_in_place_and_failures(sc):
         assert np.array_equal(got[b], L0[b])
 
 
-@pytest.mark.parametrize("batch,n", [(1, 1), (5, 3), (999, 20), (64, 32), (300, 64), (9, 100), (17, 128)])
+@pytest.mark.parametrize("batch,n", [(1, 1), (5, 3), (999, 20), (64, 32), (7, 33), (101, 50), (300, 64), (9, 100),
+                                     (17, 128)])
 def test_cholesky_adjoint_batched_parity(sc, batch, n):
     A = se_batch(batch, n, seed0=500)
     Ls = np.stack([oracle.cholesky(a) for a in A])
@@ -109,3 +110,33 @@ def test_batched_errors(sc):
     rc = lib.stan_cl_cholesky_adjoint_batched(2, 4, Lb.data_ptr(), Lb.data_ptr(),
                                               torch.empty_like(Lb).data_ptr(), info.data_ptr())
     assert rc == 2 and info.cpu().tolist() == [0, 2]
+
+
+@pytest.mark.parametrize("n", [40, 64])
+def test_batched_w64_failures_and_in_place(sc, n):
+    """32 < n <= 64 (two warps per matrix): per-matrix info of the first failing
+    pivot, bit-exact integer family, in place."""
+    batch = 9
+    L0 = np.stack([inputs.unit_lower_pm1(n, seed=b) for b in range(batch)])
+    A = np.einsum("bij,bkj->bik", L0, L0)
+    A[3, n - 1, n - 1] = -1.0
+    A[7, 10, 10] = -1e9
+    t = torch.from_numpy(A).cuda()
+    info = torch.zeros(batch, dtype=torch.int32, device="cuda")
+    assert sc.load().stan_cl_cholesky_batched(batch, n, t.data_ptr(), t.data_ptr(), info.data_ptr()) == 4
+    info = info.cpu().numpy()
+    assert info[7] == 11 and info[3] == n
+    got = t.cpu().numpy()
+    for b in (0, 1, 2, 4, 5, 6, 8):
+        assert info[b] == 0 and np.array_equal(got[b], L0[b])
+    # adjoint: integer banded family bit for bit, in place over L_bar
+    L1 = inputs.unit_lower_pm1(n, seed=3, band=2)
+    W1 = inputs.int_lbar(n, seed=4)
+    want = oracle.cholesky_adjoint(L1, W1)
+    Lt = torch.from_numpy(np.broadcast_to(L1, (batch, n, n)).copy()).cuda()
+    Wt = torch.from_numpy(np.broadcast_to(W1, (batch, n, n)).copy()).cuda()
+    assert sc.load().stan_cl_cholesky_adjoint_batched(batch, n, Lt.data_ptr(), Wt.data_ptr(), Wt.data_ptr(),
+                                                      None) == 0
+    got = Wt.cpu().numpy()
+    for b in range(batch):
+        assert np.array_equal(got[b], want)
