@@ -298,6 +298,21 @@ int stan_cl_cholesky_batched(int64_t batch, int64_t n, const double* A, double* 
 int stan_cl_cholesky_adjoint_batched(int64_t batch, int64_t n, const double* L, const double* L_bar,
                                      double* A_bar, int* info);
 
+/*
+ * Input checks of the paper's backend (§3.5: check_nan,
+ * check_symmetric, check_diagonal_zeros; NEXT-3), one pass over the n x n
+ * device matrix A (row-major, ld n), synchronous.  checks selects, the return
+ * value reports (bitwise OR):
+ *   1  some entry is NaN
+ *   2  some |A[i][j] - A[j][i]| > tol (absolute tolerance, tol >= 0; a pair with
+ *      a NaN or an infinite difference also counts)
+ *   4  some diagonal entry is zero
+ * Returns >= 0 (the bits found), or STAN_CL_EINVAL for n < 0, unknown bits in
+ * checks, tol < 0 or NaN, or A == NULL with n > 0.  Flags are only ever set,
+ * never cleared, by the CTAs (race-free, as the paper's kernels).
+ */
+int stan_cl_check_matrix(int64_t n, const double* A, int checks, double tol);
+
 /* ---- control ---- */
 int stan_cl_set_stream(void* cuda_stream); /* cudaStream_t; NULL = legacy default stream */
 void* stan_cl_get_stream(void);

@@ -58,6 +58,8 @@ def _load():
         lib.oracle_trsm.restype = ctypes.c_int
         lib.oracle_trsm_adjoint.argtypes = [I64, I64, P, P, P, P, P]
         lib.oracle_trsm_adjoint.restype = ctypes.c_int
+        lib.oracle_check_matrix.argtypes = [I64, P, ctypes.c_int, D]
+        lib.oracle_check_matrix.restype = ctypes.c_int
         lib.oracle_gp_lpdf_grad.argtypes = [I64, P, P, D, D, D, P, P]
         lib.oracle_gp_lpdf_grad.restype = ctypes.c_int
         _lib = lib
@@ -203,6 +205,14 @@ def trsm_adjoint(L, C, Cbar) -> tuple[np.ndarray, np.ndarray]:
     if info != 0:
         raise ValueError(f"L[{info - 1}][{info - 1}] is zero or not finite")
     return Lbar, Bbar
+
+
+def check_matrix(A, checks: int = 7, tol: float = 1e-8) -> int:
+    """Bits: 1 NaN present, 2 not symmetric within tol, 4 zero on the diagonal (oracle.c)."""
+    A = _c(A)
+    n = A.shape[0]
+    assert A.shape == (n, n)
+    return int(_load().oracle_check_matrix(n, _ptr(A), int(checks), float(tol)))
 
 
 def gp_lpdf_grad(x, y, alpha: float, rho: float, sigma: float) -> tuple[float, np.ndarray, np.ndarray]:

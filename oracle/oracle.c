@@ -33,6 +33,7 @@
  *                               independence)
  *   oracle_trsm_adjoint        pinned (n = 1 closed form, finite differences of a
  *                               random functional of L^-1 B in B and in L)
+ *   oracle_check_matrix        pinned (hand-built cases per bit, tolerance edge)
  *   oracle_gp_lpdf_grad        pinned (n = 1 closed form, independent Gaussian
  *                               log-density, trace-form gradient, finite differences)
  */
@@ -352,6 +353,29 @@ int oracle_trsm_adjoint(int64_t n, int64_t m, const double* L, const double* C, 
       Lbar[IDX(i, j)] = (j <= i) ? -s : 0.0;
     }
   return 0;
+}
+
+/*
+ * Input checks of the paper's OpenCL backend (§3.5 "Input
+ * checking": check_nan, check_symmetric, check_diagonal_zeros), by their plain
+ * definitions over the whole n x n matrix:
+ *   bit 0 (1): some A[i][j] is NaN
+ *   bit 1 (2): some |A[i][j] - A[j][i]| > tol (absolute; "within tolerance of
+ *              zero"; a NaN pair also counts, since the comparison is false)
+ *   bit 2 (4): some A[i][i] == 0
+ * checks selects which bits are evaluated; returns the set bits.
+ */
+int oracle_check_matrix(int64_t n, const double* A, int checks, double tol) {
+  int out = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    for (int64_t j = 0; j < n; ++j) {
+      double a = A[IDX(i, j)];
+      if ((checks & 1) && a != a) out |= 1;
+      if ((checks & 2) && !(fabs(a - A[IDX(j, i)]) <= tol)) out |= 2;
+      if ((checks & 4) && i == j && a == 0.0) out |= 4;
+    }
+  }
+  return out;
 }
 
 /*

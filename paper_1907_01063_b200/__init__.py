@@ -41,6 +41,7 @@ SIGNATURES = {
     "stan_cl_cholesky_adjoint": (_I, [_I64, _P, _P, _P]),
     "stan_cl_gp_exp_quad_cov": (_I, [_I64, _P, _D, _D, _D, _P]),
     "stan_cl_trsv": (_I, [_I64, _P, _P, _P, _I]),
+    "stan_cl_check_matrix": (_I, [_I64, _P, _I, _D]),
     "stan_cl_lower_triangular_inverse": (_I, [_I64, _P, _P]),
     "stan_cl_trsm": (_I, [_I64, _I64, _P, _P, _P, _I]),
     "stan_cl_trsm_adjoint": (_I, [_I64, _I64, _P, _P, _P, _P, _P]),
@@ -246,6 +247,19 @@ def lower_triangular_inverse(L: torch.Tensor, out: torch.Tensor | None = None) -
     if rc > 0:
         raise ValueError(f"L[{rc - 1}][{rc - 1}] is not finite and > 0")
     return X
+
+
+CHECK_NAN, CHECK_SYMMETRIC, CHECK_DIAGONAL_ZEROS = 1, 2, 4
+
+
+def check_matrix(A: torch.Tensor, checks: int = 7, tol: float = 1e-8) -> int:
+    """Bits found among 1 (NaN), 2 (not symmetric within tol), 4 (zero diagonal)
+    (stan_cl_check_matrix, PAPER.md:392-394)."""
+    A = _dev_matrix(A, "A")
+    with torch.cuda.device(A.device):
+        _bind_stream(A.device)
+        return _check("stan_cl_check_matrix",
+                      load().stan_cl_check_matrix(A.shape[0], A.data_ptr(), int(checks), float(tol)))
 
 
 def _dev_rect(t: torch.Tensor, name: str, n: int) -> torch.Tensor:

@@ -1032,6 +1032,117 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------- F1 + F2 fused
+// One launch per 128-wide panel (the latency-bound chain of small n): the
+// first CTA to start (atomic ticket 0) factors the diagonal tile with the
+// POTRF tile body and publishes it with a release flag; every other CTA takes
+// 64 panel rows, loads them while the tile is being factored, waits on the
+// flag (acquire), stages L11^T in shared memory and solves X L11^T = A21 by a
+// 128-wide substitution (4 threads per row, 32 columns each in registers;
+// column j finished by its owner with the IEEE quotient, broadcast by shuffle,
+// then the fma(-x_j, l_cj, a) updates of the columns c > j -- the same
+// column-by-column elimination as the two 64-wide substitutions + DMMA cross
+// update it replaces).  No CTA exits early, so the flag is always published;
+// the last CTA out resets the ticket / flag / exit counters (ctr[0..2]) for
+// the next launch.  Removes a launch boundary and the panel rows' L2 round
+// trip from every step of the forward chain.
+constexpr int P128_ROWS = 64;
+constexpr int P128_TP = NB + 1;
+constexpr int P128_SMEM = NB * P128_TP * (int)sizeof(double);  // = POTRF_SMEM
+static_assert(P128_SMEM == POTRF_SMEM, "the two roles share the dynamic shared memory");
+
+__device__ __forceinline__ int ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return (int)v;
+}
+
+__global__ void __launch_bounds__(256, 1) panel128_kernel(double* W, int64_t ld, int64_t k0, int64_t r0,
+                                                          int64_t r1, int* status, unsigned* ctr) {
+  pdl_enter();
+  extern __shared__ double LT[];  // POTRF staging tile, or L11^T: LT[j * P128_TP + l] = L11[l][j]
+  __shared__ double dg[NB], rdg[NB];
+  __shared__ int s_ticket;
+  const int tid = threadIdx.x, lane = tid & 31;
+  if (tid == 0) s_ticket = (int)atomicAdd(ctr, 1u);
+  __syncthreads();
+  const int ticket = s_ticket;
+  double* L11 = W + k0 * ld + k0;
+  if (ticket == 0) {
+    potrf_tile_body(L11, ld, L11, ld, NB, status, k0);
+    __syncthreads();
+    if (tid == 0) {
+      __threadfence();
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ctr + 1), "r"(1u) : "memory");
+    }
+  } else {
+    constexpr int Q = NB / 4;
+    const int r = tid >> 2, p = tid & 3;
+    const long long row = r0 + (long long)(ticket - 1) * P128_ROWS + r;
+    const bool live = row < r1;
+    double* P = W + (live ? row : r0) * ld + k0;
+    double x[Q];
+#pragma unroll
+    for (int q = 0; q < Q; ++q) x[q] = live ? P[p + 4 * q] : 0.0;  // in flight while the tile is factored
+    if (tid == 0)
+      while (ld_acquire_gpu(ctr + 1) == 0) __nanosleep(64);
+    __syncthreads();
+    // L11^T and the diagonal (L2 reads bypassing L1: the tile was just written by another SM)
+    for (int idx = tid; idx < NB * NB; idx += 256) {
+      const int l = idx >> 7, j = idx & (NB - 1);
+      if (j <= l) {
+        const double v = __ldcg(L11 + (long long)l * ld + j);
+        LT[j * P128_TP + l] = v;
+        if (j == l) {
+          dg[j] = v;
+          rdg[j] = rcp_pos(v);
+        }
+      }
+    }
+    __syncthreads();
+    const int owner_base = lane & ~3;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      if (p == (j & 3)) x[j >> 2] = div_pos(x[j >> 2], dg[j], rdg[j]);  // == x / L_jj (common.cuh)
+      const double v = __shfl_sync(0xffffffffu, x[j >> 2], owner_base | (j & 3));
+      const double* lt = LT + j * P128_TP;
+#pragma unroll
+      for (int q = (j >> 2); q < Q; ++q) {
+        if (p + 4 * q > j) x[q] = fma(-v, lt[p + 4 * q], x[q]);
+      }
+    }
+    if (live) {
+#pragma unroll
+      for (int q = 0; q < Q; ++q) P[p + 4 * q] = x[q];
+    }
+  }
+  // the last CTA out re-arms the counters for the next launch
+  __syncthreads();
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 2, 1u) == gridDim.x - 1) {
+      ctr[0] = 0;
+      ctr[1] = 0;
+      ctr[2] = 0;
+      __threadfence();
+    }
+  }
+}
+
+cudaError_t panel128(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, int* status, unsigned* ctr,
+                     cudaStream_t st) {
+  Prof prof_(PROF_POTRF, (double)NB * NB * NB / 3.0 + (double)(r1 - r0) * NB * NB, st,
+             8.0 * NB * (NB + 1) + 16.0 * (r1 - r0) * NB);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(panel128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P128_SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int blocks = 1 + (int)((std::max<int64_t>(r1 - r0, 0) + P128_ROWS - 1) / P128_ROWS);
+  return launch_pdl(panel128_kernel, blocks, 256, P128_SMEM, st, W, ld, k0, r0, r1, status, ctr);
+}
+
 // ------------------------------------------------------------ DMMA GEMM family
 // Tile configuration per call class, tunable with STAN_CL_GEMM_CFG="syrk,gemm,splitk",
 // each one of big (128x128, 8 warps of 64x32, 1 CTA/SM), mid (128x64, 4 warps of
@@ -1735,6 +1846,50 @@ cudaError_t adj_diag_fused(int S, const double* D, int64_t ldl, double* Dbar, in
   } else {
     return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+// Input checks of PAPER.md:392-394 (check_nan, check_symmetric,
+// check_diagonal_zeros) in one pass: CTA (I, J), I >= J, stages the 32 x 32
+// tiles (I, J) and (J, I) in shared memory (both read coalesced) and ORs
+//   1: a NaN in either tile;  2: |A_ij - A_ji| > tol (or a NaN pair);
+//   4: a zero on the diagonal
+// into *flags (bits are only ever set, so concurrent CTAs cannot race).
+__global__ void __launch_bounds__(256) check_matrix_kernel(const double* __restrict__ A, int64_t n, int checks,
+                                                           double tol, int* flags) {
+  __shared__ double ta[32][33], tb[32][33];
+  // blockIdx.x enumerates the lower tile pairs row by row: I (I + 1) / 2 + J
+  const long long t = blockIdx.x;
+  long long I = (long long)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+  while ((I + 1) * (I + 2) / 2 <= t) ++I;
+  while (I * (I + 1) / 2 > t) --I;
+  const long long J = t - I * (I + 1) / 2;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+  for (int r = ty; r < 32; r += 8) {
+    const long long i = I * 32 + r, j = J * 32 + tx;
+    ta[r][tx] = (i < n && j < n) ? A[i * n + j] : 0.0;   // tile (I, J): row i, column j
+    const long long i2 = J * 32 + r, j2 = I * 32 + tx;
+    tb[r][tx] = (i2 < n && j2 < n) ? A[i2 * n + j2] : 0.0;  // tile (J, I)
+  }
+  __syncthreads();
+  int bits = 0;
+  for (int r = ty; r < 32; r += 8) {
+    const long long i = I * 32 + r, j = J * 32 + tx;
+    if (i >= n || j >= n) continue;
+    const double a = ta[r][tx], b = tb[tx][r];  // a = A[i][j], b = A[j][i]
+    if ((checks & 1) && (a != a || b != b)) bits |= 1;
+    if ((checks & 2) && !(fabs(a - b) <= tol)) bits |= 2;
+    if ((checks & 4) && i == j && a == 0.0) bits |= 4;
+  }
+  const int any1 = __syncthreads_or(bits & 1), any2 = __syncthreads_or(bits & 2), any4 = __syncthreads_or(bits & 4);
+  if (threadIdx.x == 0 && (any1 | any2 | any4)) atomicOr(flags, (any1 ? 1 : 0) | (any2 ? 2 : 0) | (any4 ? 4 : 0));
+}
+
+cudaError_t check_matrix(const double* A, int64_t n, int checks, double tol, int* flags, cudaStream_t st) {
+  Prof prof_(PROF_MISC, 0.0, st, 8.0 * n * n);
+  if (n == 0) return cudaSuccess;
+  const long long T = (n + 31) / 32;
+  check_matrix_kernel<<<(unsigned)(T * (T + 1) / 2), 256, 0, st>>>(A, n, checks, tol, flags);
   return cudaGetLastError();
 }
 

@@ -88,6 +88,12 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st);
 
+// F1 + F2 in one launch: chol of the tile at (k0, k0) and rows [r0, r1) of its
+// panel solved against it (ctr: 3 device words, zero before the first launch,
+// left zero by every launch)
+cudaError_t panel128(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, int* status, unsigned* ctr,
+                     cudaStream_t st);
+
 // ---- DMMA GEMM family (F3, R1, R2, R3, R5) ----
 // C[M x N] = beta*C + sign * op(A) op(B)   (see gemm_dmma.cuh)
 //   a_kmaj: A is M x K row-major (else K x M);  b_kmaj: B is N x K (else K x N)
@@ -154,6 +160,9 @@ cudaError_t phi_sym(const double* S, double* Ssym, double* Dbar, int64_t ldd, co
 cudaError_t adj_diag_fused(int S, const double* D, int64_t ldl, double* Dbar, int64_t ldw, const double* Di,
                            double* T1, double* T2, double* T3, double* Ssym, unsigned* ctr, const int* status,
                            cudaStream_t st);
+// *flags |= 1 (NaN), 2 (|A_ij - A_ji| > tol), 4 (zero diagonal) over the n x n
+// matrix; checks selects the bits
+cudaError_t check_matrix(const double* A, int64_t n, int checks, double tol, int* flags, cudaStream_t st);
 // status = first base+k+1 with !(L[k][k] > 0 && finite), k < n
 cudaError_t check_diag(const double* L, int64_t n, int64_t ld, int* status, cudaStream_t st, int64_t base = 0);
 

@@ -196,3 +196,35 @@ def test_binding_rejects_bad_out(sc):
     # a non-contiguous INPUT is fine when it is not also the output (copied)
     L = sc.cholesky(T)
     assert relf(L.cpu().numpy(), oracle.cholesky(se(64))) <= L_TOL
+
+
+@pytest.mark.parametrize("n", [1, 3, 31, 32, 33, 100, 257, 1000])
+def test_check_matrix_vs_oracle(sc, n):
+    """stan_cl_check_matrix against oracle_check_matrix on
+    clean and corrupted SE matrices: every bit, every combination of checks."""
+    K = se(n)
+    cases = [K]
+    g = np.random.default_rng(n)
+    for kind in range(4):
+        A = K.copy()
+        i, j = int(g.integers(0, n)), int(g.integers(0, n))
+        if kind == 0:
+            A[i, j] = np.nan
+        elif kind == 1 and n > 1:
+            A[max(i, j), min(i, j)] += 1e-6 if i != j else 0.0
+            A[n - 1, 0] += 3e-8
+        elif kind == 2:
+            A[i, i] = 0.0
+        else:
+            A[i, i] = -0.0
+            A[j, (j + 1) % n] = np.inf
+        cases.append(A)
+    for A in cases:
+        for checks in (1, 2, 4, 7):
+            for tol in (1e-8, 1e-5):
+                want = oracle.check_matrix(A, checks, tol)
+                assert sc.check_matrix(dev(A), checks, tol) == want, (checks, tol)
+    lib = sc.load()
+    assert lib.stan_cl_check_matrix(-1, None, 1, 0.0) == -1
+    assert lib.stan_cl_check_matrix(0, None, 7, 0.0) == 0
+    assert lib.stan_cl_check_matrix(2, None, 8, 0.0) == -1

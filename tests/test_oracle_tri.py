@@ -124,3 +124,29 @@ def test_trsm_adjoint_finite_differences(n, m):
             fdL[i, j] = (f(L + e, B) - f(L - e, B)) / (2 * e[i, j])
     assert np.linalg.norm(fdL - Lbar) <= 1e-6 * np.linalg.norm(Lbar)
     assert np.all(Lbar[np.triu_indices(n, 1)] == 0.0)
+
+
+# ----------------------------------------------------- input checks (NEXT-3)
+def test_check_matrix_pins():
+    # check_nan, check_symmetric (absolute tolerance), check_diagonal_zeros
+    A = np.array([[4.0, 2.0, 1.0], [2.0, 5.0, 0.5], [1.0, 0.5, 3.0]])
+    assert oracle.check_matrix(A) == 0
+    B = A.copy()
+    B[2, 0] = np.nan
+    assert oracle.check_matrix(B) == 1 | 2              # a NaN pair is also not symmetric
+    assert oracle.check_matrix(B, checks=1) == 1
+    C = A.copy()
+    C[0, 1] += 1e-9                                      # within 1e-8: symmetric
+    assert oracle.check_matrix(C) == 0
+    C[0, 1] += 2e-8                                      # now 3e-8 apart
+    assert oracle.check_matrix(C) == 2
+    assert oracle.check_matrix(C, tol=1e-7) == 0
+    D = A.copy()
+    D[1, 1] = 0.0
+    assert oracle.check_matrix(D) == 4
+    assert oracle.check_matrix(D, checks=3) == 0
+    E = A.copy()
+    E[1, 1] = -0.0                                       # -0.0 == 0: a zero on the diagonal
+    assert oracle.check_matrix(E, checks=4) == 4
+    assert oracle.check_matrix(np.zeros((0, 0))) == 0
+    assert oracle.check_matrix(np.full((1, 1), np.inf)) == 2   # inf - inf is NaN: not within tol
