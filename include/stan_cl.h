@@ -371,6 +371,19 @@ int stan_cl_profile_reset(void);
 int stan_cl_profile_read(int kind, double* ms, double* flops, long long* launches);
 /* summed algorithmic (minimum) HBM bytes of the recorded launches of a class */
 int stan_cl_profile_read_bytes(int kind, double* bytes);
+/*
+ * Launch timeline (tracing).  stan_cl_trace_enable(1) records a
+ * base event on the library stream and from then on brackets EVERY library
+ * launch with CUDA events on its own stream (all classes; a few microseconds
+ * of host overhead per launch); stan_cl_trace_enable(0) stops.
+ * stan_cl_trace_read(out, max): 4 doubles per launch -- profiling class (as
+ * above), stream id (0, 1, ... in order of first use: the library stream, the
+ * lookahead side stream, copy streams), start and end in ms after the base
+ * event; synchronises on the recorded events; returns the number of records
+ * (writes at most max).
+ */
+int stan_cl_trace_enable(int on);
+int stan_cl_trace_read(double* out, int max_records);
 /* release library-owned device workspace; the library stays usable */
 int stan_cl_finalize(void);
 int stan_cl_version(void); /* major*10000 + minor*100 + patch */

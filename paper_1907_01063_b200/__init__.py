@@ -68,6 +68,8 @@ SIGNATURES = {
     "stan_cl_profile_read": (_I, [_I, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
                                   ctypes.POINTER(ctypes.c_longlong)]),
     "stan_cl_profile_read_bytes": (_I, [_I, ctypes.POINTER(ctypes.c_double)]),
+    "stan_cl_trace_enable": (_I, [_I]),
+    "stan_cl_trace_read": (_I, [_P, _I]),
     "stan_cl_finalize": (_I, []),
     "stan_cl_dist_get_unique_id": (_I, [_P]),
     "stan_cl_dist_init": (_I, [_I, _I, _P, _I, _I]),
@@ -638,6 +640,20 @@ def profile_read() -> dict:
         load().stan_cl_profile_read_bytes(k, ctypes.byref(by))
         out[name] = {"ms": ms.value, "flops": fl.value, "bytes": by.value, "launches": cnt.value}
     return out
+
+
+def trace(on: bool = True) -> None:
+    """Start (base event on the current stream) / stop the launch timeline."""
+    _bind_stream(torch.device("cuda", torch.cuda.current_device()))
+    load().stan_cl_trace_enable(int(bool(on)))
+
+
+def trace_read() -> list:
+    """[(class name, stream id, start ms, end ms), ...] of the traced launches."""
+    n = int(load().stan_cl_trace_read(None, 0))
+    buf = (ctypes.c_double * (4 * max(n, 1)))()
+    n = int(load().stan_cl_trace_read(ctypes.cast(buf, ctypes.c_void_p), n))
+    return [(PROFILE_KINDS[int(buf[4 * i])], int(buf[4 * i + 1]), buf[4 * i + 2], buf[4 * i + 3]) for i in range(n)]
 
 
 def workspace_bytes(n: int) -> int:

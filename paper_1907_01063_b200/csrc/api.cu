@@ -361,32 +361,7 @@ int64_t fwd_outer_block(int64_t n) {
 // OB = 256 (two-level blocking): two 128 sub-steps with the second half of the
 // panel updated in between (GEMM, K = 128), so the trailing update outside
 // the panel runs with K = 256.
-// fused POTRF + TRSM panel kernel (panel128): on for the 128-wide outer blocks
-// (the latency-bound sizes); STAN_CL_PANEL_FUSED=0 off, =2 also for the halves
-// of the 256-wide two-level panel
-int panel_fused_mode() {
-  static const int m = [] {
-    const char* e = getenv("STAN_CL_PANEL_FUSED");
-    return e ? atoi(e) : 1;
-  }();
-  return m;
-}
-
 int panel(double* W, int64_t ld, int64_t c0, int64_t N, int64_t OB, int* status, cudaStream_t st) {
-  const int fm = panel_fused_mode();
-  const bool fused = (OB == NB && fm >= 1) || (OB == 2 * NB && fm >= 2);
-  unsigned* pctr = (unsigned*)status + 24;  // ws header words 24..26
-  if (fused) {
-    CK(panel128(W, ld, c0, c0 + NB, N, status, pctr, st));
-    if (OB == 2 * NB) {
-      const int64_t h = c0 + NB;
-      const double* L21 = W + h * ld + c0;
-      CK(gemm_full(true, true, (int)(N - h), NB, NB, -1.0, 1, L21, ld, L21, ld, W + h * ld + h, ld, status, st,
-                   /*lower_only=*/1, PROF_LOOKAHEAD, /*allow_persistent=*/false));
-      CK(panel128(W, ld, h, h + NB, N, status, pctr, st));
-    }
-    return STAN_CL_OK;
-  }
   CK(potrf_tile(W, ld, c0, status, st));
   if (c0 + NB < N) CK(trsm_panel(W, ld, c0, c0 + NB, N, status, st));
   if (OB == 2 * NB) {
@@ -1655,6 +1630,17 @@ int stan_cl_profile_read_bytes(int kind, double* bytes) {
   long long n;
   prof_read(kind, &ms, &fl, &n, bytes);
   return STAN_CL_OK;
+}
+
+int stan_cl_trace_enable(int on) {
+  if (on) trace_start(g.stream);
+  else trace_stop();
+  return STAN_CL_OK;
+}
+
+int stan_cl_trace_read(double* out, int max_records) {
+  if (max_records < 0 || (max_records > 0 && !out)) return STAN_CL_EINVAL;
+  return trace_read(out, max_records);
 }
 
 int stan_cl_finalize(void) {

@@ -140,7 +140,7 @@ __device__ __forceinline__ double frag(const double* s, int rc, int k) {
 
 template <class CF, int MODE>
 struct TItemMap {
-  int ntn, ntiles, ktiles_full;
+  int ntn, ntm, ntiles, ktiles_full;
   // block-cyclic mode (MODE_CYC): items enumerate, per 256-wide
   // block column j, only its tile rows from the first block row that reaches
   // the diagonal (RB f_j) down; cyc_pref[j] = first item of block column j
@@ -167,6 +167,14 @@ struct TItemMap {
         tn = CB * lo + local % CB;
         return;
       }
+    }
+    if constexpr (MODE == MODE_SPLITK) {
+      // column-major over tiles: the M tiles that share one B slab (the long
+      // m x k operand, streamed once per split) are adjacent items, so they run
+      // at the same time on neighbouring CTAs and the second read hits L2
+      tn = tile / ntm;
+      tm = tile - tn * ntm;
+      return;
     }
     tm = tile / ntn;
     tn = tile - tm * ntn;
@@ -439,6 +447,7 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reser
   if (B_KMAJ && !make_kmajor_map(&mb, p.B, p.N, p.K, p.ldb, CF::BN)) return cudaErrorInvalidValue;
   TItemMap<CF, MODE> map;
   map.ntn = p.N / CF::BN;
+  map.ntm = p.M / CF::BM;
   map.ktiles_full = p.K / CF::BKS;
   int ntiles;
   if (MODE == MODE_LOWER) {

@@ -38,9 +38,20 @@ struct ProfRec {
   int kind;
   double flops, bytes;
   cudaEvent_t e0, e1;
+  cudaStream_t st;
+};
+// timeline (stan_cl_trace_*): one record per recorded launch, times relative
+// to a base event recorded when tracing was switched on
+struct TraceRec {
+  int kind, stream;
+  double t0, t1;
 };
 struct ProfState {
   unsigned mask = 0;
+  bool trace = false;
+  cudaEvent_t base = nullptr;
+  std::vector<cudaStream_t> streams;  // stream -> small id, in order of first use
+  std::vector<TraceRec> timeline;
   std::vector<ProfRec> recs;
   std::vector<cudaEvent_t> pool;
   double ms[PROF_KINDS] = {0};
@@ -73,16 +84,56 @@ Prof::Prof(int kind, double flops, cudaStream_t st, double bytes)
 Prof::~Prof() {
   if (e0_) {
     cudaEventRecord(e1_, st_);
-    g_prof.recs.push_back({kind_, flops_, bytes_, e0_, e1_});
+    g_prof.recs.push_back({kind_, flops_, bytes_, e0_, e1_, st_});
   }
 }
 void prof_enable(unsigned mask) { g_prof.mask = mask; }
+void prof_collect();
+void trace_start(cudaStream_t st) {
+  prof_collect();
+  g_prof.timeline.clear();
+  g_prof.streams.clear();
+  if (!g_prof.base) cudaEventCreate(&g_prof.base);
+  cudaEventRecord(g_prof.base, st);
+  g_prof.trace = true;
+  g_prof.mask = ~0u;
+}
+void trace_stop() {
+  prof_collect();
+  g_prof.trace = false;
+  g_prof.mask = 0;
+}
+int trace_read(double* out, int max_records) {
+  prof_collect();
+  const int m = (int)g_prof.timeline.size();
+  for (int i = 0; i < m && i < max_records; ++i) {
+    const TraceRec& t = g_prof.timeline[i];
+    out[4 * i] = t.kind;
+    out[4 * i + 1] = t.stream;
+    out[4 * i + 2] = t.t0;
+    out[4 * i + 3] = t.t1;
+  }
+  return m;
+}
 bool prof_active() { return g_prof.mask != 0; }
 void prof_collect() {
   for (auto& r : g_prof.recs) {
     cudaEventSynchronize(r.e1);
     float ms = 0.f;
     cudaEventElapsedTime(&ms, r.e0, r.e1);
+    if (g_prof.trace && g_prof.base) {
+      float a = 0.f, b = 0.f;
+      cudaEventElapsedTime(&a, g_prof.base, r.e0);
+      cudaEventElapsedTime(&b, g_prof.base, r.e1);
+      int sid = -1;
+      for (size_t i = 0; i < g_prof.streams.size(); ++i)
+        if (g_prof.streams[i] == r.st) sid = (int)i;
+      if (sid < 0) {
+        sid = (int)g_prof.streams.size();
+        g_prof.streams.push_back(r.st);
+      }
+      g_prof.timeline.push_back({r.kind, sid, (double)a, (double)b});
+    }
     g_prof.ms[r.kind] += ms;
     g_prof.flops[r.kind] += r.flops;
     g_prof.bytes[r.kind] += r.bytes;
@@ -1030,117 +1081,6 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
   e = launch_pdl(trsm_panel_kernel, blocks, 256, 0, st, W, ld, k0 + TRSM_W, r0, status);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
-}
-
-// ---------------------------------------------------------- F1 + F2 fused
-// One launch per 128-wide panel (the latency-bound chain of small n): the
-// first CTA to start (atomic ticket 0) factors the diagonal tile with the
-// POTRF tile body and publishes it with a release flag; every other CTA takes
-// 64 panel rows, loads them while the tile is being factored, waits on the
-// flag (acquire), stages L11^T in shared memory and solves X L11^T = A21 by a
-// 128-wide substitution (4 threads per row, 32 columns each in registers;
-// column j finished by its owner with the IEEE quotient, broadcast by shuffle,
-// then the fma(-x_j, l_cj, a) updates of the columns c > j -- the same
-// column-by-column elimination as the two 64-wide substitutions + DMMA cross
-// update it replaces).  No CTA exits early, so the flag is always published;
-// the last CTA out resets the ticket / flag / exit counters (ctr[0..2]) for
-// the next launch.  Removes a launch boundary and the panel rows' L2 round
-// trip from every step of the forward chain.
-constexpr int P128_ROWS = 64;
-constexpr int P128_TP = NB + 1;
-constexpr int P128_SMEM = NB * P128_TP * (int)sizeof(double);  // = POTRF_SMEM
-static_assert(P128_SMEM == POTRF_SMEM, "the two roles share the dynamic shared memory");
-
-__device__ __forceinline__ int ld_acquire_gpu(const unsigned* p) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return (int)v;
-}
-
-__global__ void __launch_bounds__(256, 1) panel128_kernel(double* W, int64_t ld, int64_t k0, int64_t r0,
-                                                          int64_t r1, int* status, unsigned* ctr) {
-  pdl_enter();
-  extern __shared__ double LT[];  // POTRF staging tile, or L11^T: LT[j * P128_TP + l] = L11[l][j]
-  __shared__ double dg[NB], rdg[NB];
-  __shared__ int s_ticket;
-  const int tid = threadIdx.x, lane = tid & 31;
-  if (tid == 0) s_ticket = (int)atomicAdd(ctr, 1u);
-  __syncthreads();
-  const int ticket = s_ticket;
-  double* L11 = W + k0 * ld + k0;
-  if (ticket == 0) {
-    potrf_tile_body(L11, ld, L11, ld, NB, status, k0);
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(ctr + 1), "r"(1u) : "memory");
-    }
-  } else {
-    constexpr int Q = NB / 4;
-    const int r = tid >> 2, p = tid & 3;
-    const long long row = r0 + (long long)(ticket - 1) * P128_ROWS + r;
-    const bool live = row < r1;
-    double* P = W + (live ? row : r0) * ld + k0;
-    double x[Q];
-#pragma unroll
-    for (int q = 0; q < Q; ++q) x[q] = live ? P[p + 4 * q] : 0.0;  // in flight while the tile is factored
-    if (tid == 0)
-      while (ld_acquire_gpu(ctr + 1) == 0) __nanosleep(64);
-    __syncthreads();
-    // L11^T and the diagonal (L2 reads bypassing L1: the tile was just written by another SM)
-    for (int idx = tid; idx < NB * NB; idx += 256) {
-      const int l = idx >> 7, j = idx & (NB - 1);
-      if (j <= l) {
-        const double v = __ldcg(L11 + (long long)l * ld + j);
-        LT[j * P128_TP + l] = v;
-        if (j == l) {
-          dg[j] = v;
-          rdg[j] = rcp_pos(v);
-        }
-      }
-    }
-    __syncthreads();
-    const int owner_base = lane & ~3;
-#pragma unroll
-    for (int j = 0; j < NB; ++j) {
-      if (p == (j & 3)) x[j >> 2] = div_pos(x[j >> 2], dg[j], rdg[j]);  // == x / L_jj (common.cuh)
-      const double v = __shfl_sync(0xffffffffu, x[j >> 2], owner_base | (j & 3));
-      const double* lt = LT + j * P128_TP;
-#pragma unroll
-      for (int q = (j >> 2); q < Q; ++q) {
-        if (p + 4 * q > j) x[q] = fma(-v, lt[p + 4 * q], x[q]);
-      }
-    }
-    if (live) {
-#pragma unroll
-      for (int q = 0; q < Q; ++q) P[p + 4 * q] = x[q];
-    }
-  }
-  // the last CTA out re-arms the counters for the next launch
-  __syncthreads();
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(ctr + 2, 1u) == gridDim.x - 1) {
-      ctr[0] = 0;
-      ctr[1] = 0;
-      ctr[2] = 0;
-      __threadfence();
-    }
-  }
-}
-
-cudaError_t panel128(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, int* status, unsigned* ctr,
-                     cudaStream_t st) {
-  Prof prof_(PROF_POTRF, (double)NB * NB * NB / 3.0 + (double)(r1 - r0) * NB * NB, st,
-             8.0 * NB * (NB + 1) + 16.0 * (r1 - r0) * NB);
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(panel128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P128_SMEM);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int blocks = 1 + (int)((std::max<int64_t>(r1 - r0, 0) + P128_ROWS - 1) / P128_ROWS);
-  return launch_pdl(panel128_kernel, blocks, 256, P128_SMEM, st, W, ld, k0, r0, r1, status, ctr);
 }
 
 // ------------------------------------------------------------ DMMA GEMM family

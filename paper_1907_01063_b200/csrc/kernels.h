@@ -43,6 +43,10 @@ void prof_enable(unsigned mask);  // bit k enables class k
 bool prof_active();
 void prof_reset();
 void prof_read(int kind, double* ms, double* flops, long long* count, double* bytes = nullptr);
+// timeline of every launch from trace_start (base event on st) to trace_stop
+void trace_start(cudaStream_t st);
+void trace_stop();
+int trace_read(double* out, int max_records);  // 4 doubles per launch: kind, stream id, start, end (ms)
 
 // ---- F0: SE covariance (K1) ----
 cudaError_t se_cov(int64_t n, const double* x, double alpha, double rho, double jitter, double* K,
@@ -87,12 +91,6 @@ cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStrea
 // rows [r0, r1) of columns [k0, k0+128): X <- X L11^-T (L11 = W[k0.., k0..]), substitution
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st);
-
-// F1 + F2 in one launch: chol of the tile at (k0, k0) and rows [r0, r1) of its
-// panel solved against it (ctr: 3 device words, zero before the first launch,
-// left zero by every launch)
-cudaError_t panel128(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, int* status, unsigned* ctr,
-                     cudaStream_t st);
 
 // ---- DMMA GEMM family (F3, R1, R2, R3, R5) ----
 // C[M x N] = beta*C + sign * op(A) op(B)   (see gemm_dmma.cuh)

@@ -228,3 +228,25 @@ def test_check_matrix_vs_oracle(sc, n):
     assert lib.stan_cl_check_matrix(-1, None, 1, 0.0) == -1
     assert lib.stan_cl_check_matrix(0, None, 7, 0.0) == 0
     assert lib.stan_cl_check_matrix(2, None, 8, 0.0) == -1
+
+
+def test_trace_timeline(sc):
+    """stan_cl_trace_*: every launch of a call is recorded with its stream and
+    ordered times; the forward uses the library stream and the lookahead side
+    stream; classes match the launch kinds."""
+    n = 2048
+    K = dev(se(n))
+    sc.cholesky(K)                                 # warm
+    before = sc.kernel_launches()
+    sc.trace(True)
+    sc.cholesky(K)
+    torch.cuda.synchronize()
+    recs = sc.trace_read()
+    sc.trace(False)
+    assert len(recs) == sc.kernel_launches() - before
+    assert all(0.0 <= a <= b for _, _, a, b in recs)
+    kinds = {k for k, _, _, _ in recs}
+    assert {"potrf", "trsm", "syrk", "lookahead"} <= kinds
+    assert {s for _, s, _, _ in recs} == {0, 1}
+    sc.cholesky(K)                                 # not traced any more
+    assert len(sc.trace_read()) == len(recs)
