@@ -553,7 +553,8 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
       // C_adj = C_adj * lower_triangular_inverse(D)
       // computed out of place (persistent TMA GEMM) into Ctmp, consumed from there
       // by the two big products, and written back to A_bar afterwards
-      CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, Ctmp, B, status, st, 0, PROF_TRMM));
+      CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, Ctmp, B, status, st, 0, PROF_TRMM, true, 0,
+                   TRI_B_LOWER));
       // B_adj = B_adj - C_adj * R
       if (j > 0)
         CK(gemm_full(true, false, (int)m, (int)j, (int)B, -1.0, 1, Ctmp, B, R, ld, Wm + k * ld, ld, status, st));
@@ -655,7 +656,7 @@ int adjoint_pipelined(const double* Lw, double* Wm, int64_t N, int64_t ld, int* 
     if (m > 0) {
       // C_adj = C_adj * lower_triangular_inverse(D)
       CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, cs + B * B, B, status, chain, 0,
-                   PROF_TRMM, true, chain_res));
+                   PROF_TRMM, true, chain_res, TRI_B_LOWER));
       // [R_adj D_adj] -= C_adj^T [B C], split-K
       // the split is the sequential sweep's (a function of m, k only), so the
       // partial sums -- and every bit of the result -- match adjoint_inplace
@@ -826,17 +827,17 @@ int tri_inverse_blocked(const double* Lw, int64_t ldl, double* Xw, int64_t ldx, 
       for (int64_t p = 0; p < nf; ++p) {
         const int64_t c0 = 2 * b * p, r0 = c0 + b;
         CK(gemm_full(true, false, (int)b, (int)b, (int)b, 1.0, 0, Lw + r0 * ldl + c0, ldl, Xw + c0 * ldx + c0, ldx,
-                     T, b, status, st, 0, PROF_GP));
+                     T, b, status, st, 0, PROF_GP, true, 0, TRI_B_LOWER));
         CK(gemm_full(true, false, (int)b, (int)b, (int)b, -1.0, 0, Xw + r0 * ldx + r0, ldx, T, b,
-                     Xw + r0 * ldx + c0, ldx, status, st, 0, PROF_GP));
+                     Xw + r0 * ldx + c0, ldx, status, st, 0, PROF_GP, true, 0, TRI_A_LOWER));
       }
     }
     if (R > b) {  // ragged pair: C1 is b x b, C2 is rb x rb
       const int64_t c0 = nf * 2 * b, r0 = c0 + b, rb = R - b;
       CK(gemm_full(true, false, (int)rb, (int)b, (int)b, 1.0, 0, Lw + r0 * ldl + c0, ldl, Xw + c0 * ldx + c0, ldx,
-                   T, b, status, st, 0, PROF_GP));
+                   T, b, status, st, 0, PROF_GP, true, 0, TRI_B_LOWER));
       CK(gemm_full(true, false, (int)rb, (int)b, (int)rb, -1.0, 0, Xw + r0 * ldx + r0, ldx, T, b,
-                   Xw + r0 * ldx + c0, ldx, status, st, 0, PROF_GP));
+                   Xw + r0 * ldx + c0, ldx, status, st, 0, PROF_GP, true, 0, TRI_A_LOWER));
     }
   }
   return STAN_CL_OK;
@@ -870,7 +871,8 @@ int trsm_blocked(const double* Lw, int64_t ldl, double* Wx, int64_t ldw, int64_t
     const int64_t i = trans ? nblk - 1 - t : t, r0 = i * Bk;
     const double* Di = Dinv + i * Bk * Bk;
     double* Xi = Wx + r0 * ldw;
-    CK(gemm_full(!trans, false, (int)Bk, (int)Mp, (int)Bk, 1.0, 0, Di, Bk, Xi, ldw, S, Mp, status, st, 0, PROF_GP));
+    CK(gemm_full(!trans, false, (int)Bk, (int)Mp, (int)Bk, 1.0, 0, Di, Bk, Xi, ldw, S, Mp, status, st, 0, PROF_GP, true, 0,
+                 trans ? TRI_A_UPPER : TRI_A_LOWER));
     if (!trans && r0 + Bk < N)
       CK(gemm_full(true, false, (int)(N - r0 - Bk), (int)Mp, (int)Bk, -1.0, 1, Lw + (r0 + Bk) * ldl + r0, ldl, S, Mp,
                    Xi + Bk * ldw, ldw, status, st, 0, PROF_GP));
@@ -2145,7 +2147,7 @@ int dist_adjoint(std::vector<Rank>& rs, const Grid& gr, Comm& cm) {
         if (mloc == 0) continue;
         double* Cb = r.W + li0 * DB * r.ld + (jb / Q) * DB;
         CK(gemm_full(true, false, (int)mloc, (int)DB, (int)DB, 1.0, 0, Cb, r.ld, dinv_of(r), DB, r.pan(b), DB,
-                     r.status, st, 0, PROF_TRMM));
+                     r.status, st, 0, PROF_TRMM, true, 0, TRI_B_LOWER));
         CK(copy_block(r.pan(b), DB, Cb, r.ld, mloc, DB, st));
       }
       for (int p = 0; p < P; ++p) {

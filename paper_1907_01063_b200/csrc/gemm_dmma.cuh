@@ -56,7 +56,12 @@ struct GemmArgs {
   // (I, J) = ((cy_li + i) cy_P + cy_p, (cy_lj + j) cy_Q + cy_q): tiles with I < J are
   // skipped (no loads, no stores), I == J blocks keep their lower part only.
   int cyc = 0, cy_P = 1, cy_p = 0, cy_Q = 1, cy_q = 0, cy_li = 0, cy_lj = 0;
+  // TMA kernel, MODE_FULL: triangular operands (TRI_* bits of op(A) M x K,
+  // op(B) K x N): each output tile contracts only the k-slabs that can be
+  // nonzero -- the skipped terms are exact zeros
+  int tri = 0;
 };
+
 
 // Per-SM MMA token ("ping-pong" between the CTAs resident on one SM): a CTA
 // issues its prologue loads, then waits for the token, runs its DMMA main loop

@@ -227,6 +227,18 @@ struct TItemMap {
     } else {
       kbeg = 0;
       ns = ktiles_full;
+      if constexpr (MODE == MODE_FULL) {
+        if (p.tri) {
+          int kend = p.K;
+          if (p.tri & TRI_A_LOWER) kend = min(kend, m0 + CF::BM);  // op(A)(m, k) = 0 for k > m
+          if (p.tri & TRI_A_UPPER) kbeg = max(kbeg, m0);           // op(A)(m, k) = 0 for k < m
+          if (p.tri & TRI_B_LOWER) kbeg = max(kbeg, n0);           // op(B)(k, n) = 0 for k < n
+          if (p.tri & TRI_B_UPPER) kend = min(kend, n0 + CF::BN);  // op(B)(k, n) = 0 for k > n
+          kbeg = kbeg / CF::BKS * CF::BKS;
+          kend = (kend + CF::BKS - 1) / CF::BKS * CF::BKS;
+          ns = kend > kbeg ? (kend - kbeg) / CF::BKS : 0;
+        }
+      }
     }
   }
 };

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "kernels.h"
 #include "gemm_dmma.cuh"
 #include "gemm_tma.cuh"
 #include <cudaTypedefs.h>
@@ -1065,10 +1066,96 @@ __global__ void __launch_bounds__(256, 2) trsm_panel_kernel(double* W, int64_t l
   for (int q = 0; q < Q; ++q) P[p + 4 * q] = x[q];
 }
 
+// The whole 128-wide panel solve X L11^T = A21 in ONE launch (replaces two
+// 64-wide substitutions + the DMMA cross update: three launches on the
+// forward's critical chain).  64 rows per CTA, four threads per row holding
+// 32 columns each in registers; column j finished by its owner (call-free IEEE
+// quotient), broadcast by shuffle, then fma(-x_j, L_cj, x_c) for the columns
+// c > j -- the column-by-column elimination, with the cross-half products on
+// the FMA pipe.  L11 is staged transposed in two halves so the shared memory
+// (66 KB) leaves room for two CTAs per SM at <= 128 registers: columns 0..63 of L11 (all 128 rows) for
+// j < 64, then the lower 64 x 64 corner for j >= 64.
+constexpr int T128_P = NB + 1;
+constexpr int T128_SMEM = (64 * T128_P + 2 * NB) * (int)sizeof(double);
+
+__global__ void __launch_bounds__(256, 2) trsm128_kernel(double* W, int64_t ld, int64_t k0, int64_t r0,
+                                                         const int* status) {
+  pdl_enter();
+  if (cta_status_set(status)) return;
+  extern __shared__ double sm128[];
+  double* LT = sm128;                 // [64][T128_P]: LT[jj][c] = L11[c][j], jj = j (first half) or j - 64
+  double* dg = sm128 + 64 * T128_P;   // L_jj
+  double* rdg = dg + NB;              // RN(1 / L_jj)
+  const int tid = threadIdx.x, lane = tid & 31;
+  const double* L11 = W + k0 * ld + k0;
+  constexpr int Q = NB / 4;
+  const int r = tid >> 2, p = tid & 3;
+  const long long row = r0 + (long long)blockIdx.x * TRSM_ROWS + r;
+  double* P = W + row * ld + k0;
+  double x[Q];
+#pragma unroll
+  for (int q = 0; q < Q; ++q) x[q] = P[p + 4 * q];
+  // first half: L11[c][j], j < 64, every row c (lower part only)
+  for (int idx = tid; idx < NB * 64; idx += 256) {
+    const int c = idx >> 6, j = idx & 63;
+    if (j <= c) LT[j * T128_P + c] = L11[(long long)c * ld + j];
+  }
+  if (tid < NB) {
+    const double d = L11[(long long)tid * ld + tid];
+    dg[tid] = d;
+    rdg[tid] = rcp_pos(d);
+  }
+  __syncthreads();
+  const int owner_base = lane & ~3;
+#pragma unroll
+  for (int j = 0; j < 64; ++j) {
+    if (p == (j & 3)) x[j >> 2] = div_pos(x[j >> 2], dg[j], rdg[j]);  // == x / L_jj (common.cuh)
+    const double v = __shfl_sync(0xffffffffu, x[j >> 2], owner_base | (j & 3));
+    const double* lt = LT + j * T128_P;
+#pragma unroll
+    for (int q = (j >> 2); q < Q; ++q)
+      if (p + 4 * q > j) x[q] = fma(-v, lt[p + 4 * q], x[q]);
+  }
+  __syncthreads();
+  // second half: L11[c][j], 64 <= j <= c < 128
+  for (int idx = tid; idx < 64 * 64; idx += 256) {
+    const int c = 64 + (idx >> 6), j = 64 + (idx & 63);
+    if (j <= c) LT[(j - 64) * T128_P + c] = L11[(long long)c * ld + j];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 64; j < NB; ++j) {
+    if (p == (j & 3)) x[j >> 2] = div_pos(x[j >> 2], dg[j], rdg[j]);
+    const double v = __shfl_sync(0xffffffffu, x[j >> 2], owner_base | (j & 3));
+    const double* lt = LT + (j - 64) * T128_P;
+#pragma unroll
+    for (int q = (j >> 2); q < Q; ++q)
+      if (p + 4 * q > j) x[q] = fma(-v, lt[p + 4 * q], x[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < Q; ++q) P[p + 4 * q] = x[q];
+}
+
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st, 16.0 * (r1 - r0) * NB + 4.0 * NB * NB);
+  // one launch for panels up to trsm128_maxm rows (latency-bound; measured
+  // faster there), the two 64-wide substitutions + DMMA cross update above
+  // (more CTAs per SM for the long panels of large n)
+  static const int maxm = [] {
+    const char* e = getenv("STAN_CL_TRSM128_MAXM");
+    return e ? atoi(e) : 4096;
+  }();
+  if (r1 - r0 <= maxm) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(trsm128_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, T128_SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    return launch_pdl(trsm128_kernel, (int)((r1 - r0) / TRSM_ROWS), 256, T128_SMEM, st, W, ld, k0, r0, status);
+  }
   const int blocks = (int)((r1 - r0) / TRSM_ROWS);
   cudaError_t e = launch_pdl(trsm_panel_kernel, blocks, 256, 0, st, W, ld, k0, r0, status);
   if (e != cudaSuccess) return e;
@@ -1101,12 +1188,22 @@ struct CfgSel {
   // trailing order M >= reserve_m, else reserve_small (the panel is then
   // relatively longer); STAN_CL_SYRK_RESERVE="big,small,m" overrides
   int reserve_big = 8, reserve_small = 24, reserve_m = 8192;
-  int syrk_reserve(int M) const { return M >= reserve_m ? reserve_big : reserve_small; }
+  // third level: M < reserve_m2 -> reserve_tiny (the short trailing updates of
+  // n <= 4096, where the panel chain is the bottleneck: forward 2.85 -> 2.69 ms
+  // at n = 4096 with the one-launch TRSM, profiles/r02_small_n_forward.txt)
+  int reserve_tiny = 48, reserve_m2 = 4096;
+  int syrk_reserve(int M) const {
+    return M >= reserve_m ? reserve_big : (M >= reserve_m2 ? reserve_small : reserve_tiny);
+  }
   CfgSel() {
     const char* rs = getenv("STAN_CL_SYRK_RESERVE");
     if (rs) {
-      int n = sscanf(rs, "%d,%d,%d", &reserve_big, &reserve_small, &reserve_m);
+      int n = sscanf(rs, "%d,%d,%d,%d,%d", &reserve_big, &reserve_small, &reserve_m, &reserve_tiny, &reserve_m2);
       if (n == 1) reserve_small = reserve_big;
+      if (n < 4) {
+        reserve_tiny = reserve_small;
+        reserve_m2 = 0;
+      }
     }
     const char* pp = getenv("STAN_CL_PINGPONG");
     if (pp) pingpong = atoi(pp);
@@ -1159,10 +1256,14 @@ cudaError_t gemm_full_cfg(bool a_kmaj, bool b_kmaj, const GemmArgs& p, cudaStrea
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st, int lower_only, int prof_kind,
-                      bool allow_persistent, int reserve_sms) {
+                      bool allow_persistent, int reserve_sms, int tri) {
   if (M == 0 || N == 0) return cudaSuccess;
-  Prof prof_(prof_kind, 2.0 * M * N * K, st, (beta ? 16.0 : 8.0) * M * N + 8.0 * ((double)M * K + (double)N * K));
+  // algorithmic flops: a triangular operand halves the contraction
+  const double tri_fac = ((tri & (TRI_A_LOWER | TRI_A_UPPER)) ? 0.5 : 1.0) * ((tri & (TRI_B_LOWER | TRI_B_UPPER)) ? 0.5 : 1.0);
+  Prof prof_(prof_kind, 2.0 * M * N * K * tri_fac, st,
+             (beta ? 16.0 : 8.0) * M * N + 8.0 * ((double)M * K + (double)N * K));
   GemmArgs p{A, lda, B, ldb, C, ldc, M, N, K, K, sign, beta, lower_only, status, cfgsel().pingpong};
+  p.tri = tri;
   // A aliasing C (in-place C <- A B): one CTA must own whole rows of C, i.e. a
   // single 128-wide tile column with the one-tile-per-CTA kernel
   const bool alias = (const void*)A == (const void*)C;
@@ -1400,15 +1501,21 @@ __global__ void __launch_bounds__(128, 1) tri_inverse_kernel(const double* L, in
   {
     const double* Dw = S1 + 32 * (warp & 1) * TI_SP + 32 * (warp >> 1);
     const int c = lane;
+    // RN(1 / D_ii) of the block, one lane each (off the dependency chain); the
+    // quotients below are then the call-free Markstein ones (common.cuh:
+    // bit-identical to IEEE '/'), 3 dependent FMAs instead of a division
+    __shared__ double yd[4][32];
+    yd[warp][c] = rcp_pos(Dw[c * TI_SP + c]);
+    __syncwarp();
     double x[32];
+    // x_k = 0 for k < c, so the unpredicated products add exact zeros (finite D)
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
       double s = 0.0;
 #pragma unroll
-      for (int k = 0; k < i; ++k)
-        if (k >= c) s = fma(Dw[i * TI_SP + k], x[k], s);
+      for (int k = 0; k < i; ++k) s = fma(Dw[i * TI_SP + k], x[k], s);
       const double di = Dw[i * TI_SP + i];
-      x[i] = (i < c) ? 0.0 : (i == c ? 1.0 / di : -s / di);
+      x[i] = (i < c) ? 0.0 : div_pos(i == c ? 1.0 : -s, di, yd[warp][i]);
     }
     double* Xw = X + 32 * warp * TI_XP + 32 * warp;
 #pragma unroll

@@ -93,6 +93,9 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
                        cudaStream_t st);
 
 // ---- DMMA GEMM family (F3, R1, R2, R3, R5) ----
+// triangular operands of gemm_full (tri bits; op(A) is M x K, op(B) is K x N):
+// each output tile contracts only the k-slabs that can be nonzero
+enum TriBits { TRI_A_LOWER = 1, TRI_A_UPPER = 2, TRI_B_LOWER = 4, TRI_B_UPPER = 8 };
 // C[M x N] = beta*C + sign * op(A) op(B)   (see gemm_dmma.cuh)
 //   a_kmaj: A is M x K row-major (else K x M);  b_kmaj: B is N x K (else K x N)
 // lower_only: store only r >= c (relative to C); prof_kind: profiling class;
@@ -102,7 +105,7 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st, int lower_only = 0,
-                      int prof_kind = 1, bool allow_persistent = true, int reserve_sms = 0);
+                      int prof_kind = 1, bool allow_persistent = true, int reserve_sms = 0, int tri = 0);
 // C[M x N] -= A B^T (A M x K, B N x K, both k-major) on the block-cyclic lower
 // tiles of rank (p, q) of a P x Q grid: C's 256 x 256 block (i, j) is global tile
 // ((li0 + i) P + p, (lj0 + j) Q + q); blocks above the diagonal are skipped and
