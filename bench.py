@@ -364,17 +364,20 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     sc.profile_enable(False)
     warm = sc.profile_read()
-    # the dominant kernel of the step: the persistent TMA DMMA GEMM (its
-    # instantiations: SYRK, rank-256 updates, split-K, lookahead column, C_bar D^-1)
-    # when it is where most of the time goes -- the three large classes tie within
-    # ~1% at n = 16384, so the aggregate over the kernel is the stable figure;
-    # otherwise (n <= 64: the register kernels) the single dominant class
+    # the dominant kernel of the step: when the DMMA GEMM classes take most of the
+    # time, the one with the most algorithmic work (deterministic: the SYRK, the
+    # split-K contraction and the rank-256 update each take ~30% of the n = 16384
+    # step and tie within run-to-run noise in event time; the split-K
+    # contraction carries the most flops); otherwise (n <= 64: the register
+    # kernels) the class with the most event time.  Only that class is
+    # event-bracketed inside the timed region (bracketing more launches breaks
+    # the programmatic-dependent-launch overlap: +1.3 ms per step measured).
     dmma_ms = sum(warm[k]["ms"] for k in DMMA_CLASSES)
     if dmma_ms >= 0.5 * sum(v["ms"] for v in warm.values()):
-        dom_kinds = [k for k in DMMA_CLASSES if warm[k]["launches"]]
+        dom_kinds = [max(DMMA_CLASSES, key=lambda k: warm[k]["flops"])]
     else:
         dom_kinds = [max(warm, key=lambda k: warm[k]["ms"])]
-    dom = dom_kinds[0] if len(dom_kinds) == 1 else "gemm_tma"
+    dom = dom_kinds[0]
     barrier()
     torch.cuda.synchronize()
     sampler = ClockSampler(local_rank)
@@ -413,9 +416,7 @@ def bench_ours(args, rank: int, world: int, local_rank: int):
         peak, unit = (FP64_PEAK_TFLOPS, "TFLOP/s") if bound == "tensor" else (FP64_DFMA_PEAK_TFLOPS, "TFLOP/s")
         src = PEAK_SOURCE if bound == "tensor" else "measured: FP64 DFMA loop, profiles/fp64_peak_r01.jsonl"
     tr = traffic_aggregate(dom_kinds)
-    roofline = {"bound": bound, "kernel": dom, "kernel_classes": dom_kinds,
-                "per_class_tflops": {k: (prof[k]["flops"] / (prof[k]["ms"] / 1e3) / 1e12 if prof[k]["ms"] > 0 else None)
-                                     for k in dom_kinds},
+    roofline = {"bound": bound, "kernel": dom, "selection": "DMMA class with the most algorithmic flops per step",
                 "achieved": achieved, "peak": peak,
                 "unit": unit, "frac": achieved / peak,
                 "traffic": tr, "algorithmic_bytes_per_launch": d["bytes"] / nl,

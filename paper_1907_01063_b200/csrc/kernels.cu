@@ -1337,11 +1337,18 @@ __global__ void splitk_reduce_sub_kernel(const double* __restrict__ P, int split
        h += (long long)gridDim.x * blockDim.x) {
     const long long e = 2 * h;
     const long long r = e / N, c = e - r * N;
-    double2 s = *reinterpret_cast<const double2*>(P + e);
-    for (int z = 1; z < splits; ++z) {
-      const double2 v = *reinterpret_cast<const double2*>(P + z * plane + e);
-      s.x += v.x;
-      s.y += v.y;
+    double2 s = __ldcs(reinterpret_cast<const double2*>(P + e));
+    for (int z0 = 1; z0 < splits; z0 += 8) {  // eight planes in flight, added in order
+      double2 q[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (z0 + u < splits) q[u] = __ldcs(reinterpret_cast<const double2*>(P + (z0 + u) * plane + e));
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (z0 + u < splits) {
+          s.x += q[u].x;
+          s.y += q[u].y;
+        }
     }
     double2* d = reinterpret_cast<double2*>(dst + r * ldd + c);
     double2 o = *d;
@@ -1379,12 +1386,20 @@ __global__ void adj_rows_init_kernel(const double* __restrict__ P, int splits, i
     }
     if (c < kc && splits > 0) {
       // the partials summed first, in split order, then subtracted: the same
-      // arithmetic as splitk_reduce_sub (results bit-identical to the unfused path)
-      double2 t = *reinterpret_cast<const double2*>(prow + c);
-      for (int z = 1; z < splits; ++z) {
-        const double2 q = *reinterpret_cast<const double2*>(prow + z * plane + c);
-        t.x += q.x;
-        t.y += q.y;
+      // arithmetic as splitk_reduce_sub (results bit-identical to the unfused
+      // path); the planes are loaded eight at a time ahead of the in-order adds
+      double2 t = __ldcs(reinterpret_cast<const double2*>(prow + c));
+      for (int z0 = 1; z0 < splits; z0 += 8) {
+        double2 q[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (z0 + u < splits) q[u] = __ldcs(reinterpret_cast<const double2*>(prow + (z0 + u) * plane + c));
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (z0 + u < splits) {
+            t.x += q[u].x;
+            t.y += q[u].y;
+          }
       }
       v.x -= t.x;
       v.y -= t.y;

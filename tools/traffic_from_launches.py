@@ -53,8 +53,19 @@ def main(path, out=None):
         rec = recs.setdefault(d["ID"], {"name": d["Kernel Name"]})
         rec[d["Metric Name"]] = float(d["Metric Value"].replace(",", "")) * UNITS[d["Metric Unit"]]
     agg = collections.defaultdict(lambda: {"launches": 0, "ms": 0.0, "dram_bytes": 0.0})
-    for rec in recs.values():
-        c = classify(rec["name"])
+    seq = list(recs.values())
+    classes = [classify(r["name"]) for r in seq]
+    # the adjoint's C_bar D^-1 product and its merged rank-256 update are the same
+    # TMA instantiation; per step the order is C_bar D^-1 -> split-K -> ... ->
+    # update, so a (1, 0, 0) launch whose next GEMM launch is split-K is the former
+    gemm_like = {"adj_gemm", "splitk", "syrk", "lookahead", "panel_gemm"}
+    for i, c in enumerate(classes):
+        if c != "adj_gemm":
+            continue
+        nxt = next((classes[j] for j in range(i + 1, len(classes)) if classes[j] in gemm_like), None)
+        if nxt == "splitk":
+            classes[i] = "trmm"
+    for rec, c in zip(seq, classes):
         a = agg[c]
         a["launches"] += 1
         a["ms"] += rec.get("gpu__time_duration.sum", 0.0)
