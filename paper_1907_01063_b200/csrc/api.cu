@@ -147,17 +147,36 @@ int64_t adj_block(int64_t n) {
 // meet at grid barriers and must all be resident), at most 140 while the
 // bulk side has work
 int adj_chain_sms(int64_t N, int64_t B, int64_t k) {
-  const int64_t m = N - k, jprev = k;                            // previous step: j = k
+  const int64_t m = N - k;
+  // DMMA work (FMAs) of the chain of this step (C_bar D^-1, split-K, lookahead
+  // column) and of the previous step's bulk update beside it (rows j_prev.. =
+  // k.. of B + m - B rows, columns [0, k - B))
   const double wc = (double)m * k * B + (double)m * B * B + (double)(B + m) * B * B;
-  const double wm = (double)(B + std::max<int64_t>(m - B, 0)) * (double)std::max<int64_t>(jprev - 2 * B, 0) * B;
+  const double wm = (double)std::max<int64_t>(m, 0) * (double)std::max<int64_t>(k - B, 0) * B;
   if (wm <= 0) return kNumSms;
   static const int fixed = [] {
     const char* e = getenv("STAN_CL_PIPE_CHAIN_SMS");  // tuning aid: fixed chain share
     return e ? atoi(e) : 0;
   }();
   if (fixed > 0) return std::min(fixed, kNumSms);
-  int r = (int)std::lround(kNumSms * wc / (wc + wm));
-  return std::min(std::max(r, 64), kNumSms - 8);
+  // the chain also carries latency-bound kernels (R0 + reduce, write-back,
+  // fused diagonal step: ~L0 us per step whatever its SM share): balance
+  //   wc / (R rho) + L0  against  wm / ((148 - R) rho),  rho = FMAs per us per SM
+  static const double L0 = [] {
+    const char* e = getenv("STAN_CL_PIPE_L0_US");
+    return e ? atof(e) : 60.0;
+  }();
+  const double rho = 33e12 / 2.0 / kNumSms / 1e6;
+  int best = 64;
+  double bt = 1e300;
+  for (int r = 64; r <= kNumSms - 8; ++r) {
+    const double t = std::max(wc / (r * rho) + L0, wm / ((kNumSms - r) * rho));
+    if (t < bt) {
+      bt = t;
+      best = r;
+    }
+  }
+  return best;
 }
 
 AdjPlan adj_plan(int64_t n) {
@@ -704,17 +723,18 @@ int adjoint_pipelined(const double* Lw, double* Wm, int64_t N, int64_t ld, int* 
 // adjoint sweep variant (all three give bit-identical results):
 //   0 = adjoint_inplace (separate B_bar / R_bar updates, one stream),
 //   1 = two-stream pipeline, 2 = one stream with the merged [S; C_bar] R update.
-// Default (measured, profiles/r02_adjoint_variants.txt): the pipeline up to
-// N = 2048, where the chain's latency dominates (n = 1024: 0.416 vs 0.451 ms),
-// the merged single stream above, where splitting the SMs between two
-// persistent GEMMs costs more than the chain it hides (n = 16384: 96.8 vs 94.9 ms).
+// Default 2: with the round-2 chain kernels (blocked D^-1, fused R0 + reduce)
+// the merged sweep is as fast or faster at every size (n = 1024: 0.328 vs
+// 0.338 ms, 2048: 0.733 vs 0.869 ms, 16384: 94.7 vs 96.7 ms;
+// profiles/r02_adjoint_variants.txt): the pipeline's SM split between two
+// persistent GEMMs costs more than the chain latency it hides.
 int adj_pipe_mode(int64_t N = 0) {
+  (void)N;
   static const int m = [] {
     const char* e = getenv("STAN_CL_ADJ_PIPE");
-    return e ? atoi(e) : -1;
+    return e ? atoi(e) : 2;
   }();
-  if (m >= 0) return m;
-  return N <= 2048 ? 1 : 2;
+  return m;
 }
 bool adj_pipe_enabled(int64_t N) { return adj_pipe_mode(N) != 0; }
 
