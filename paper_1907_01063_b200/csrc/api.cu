@@ -582,9 +582,12 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
       int splits, kps;
       splitk_choice(m, k, B, &splits, &kps);
       CK(gemm_splitk_tn((int)B, (int)k, (int)m, splits, kps, Ctmp, B, Lw + k * ld, ld, Pbuf, status, st));
-      if (src) CK(adj_rows_init(Pbuf, splits, (int)B, k, src, lds, Wm, ld, j, N, status, st));
-      else CK(splitk_reduce_sub(Pbuf, splits, (int)B, (int)k, Wm + j * ld, ld, status, st));
-      CK(copy_block(Ctmp, B, Cb, ld, m, B, st));
+      if (src) {  // R0 + reduce + C_bar write-back in one launch
+        CK(adj_rows_init(Pbuf, splits, (int)B, k, src, lds, Wm, ld, j, N, status, st, Ctmp, B, Cb, ld, m));
+      } else {
+        CK(splitk_reduce_sub(Pbuf, splits, (int)B, (int)k, Wm + j * ld, ld, status, st));
+        CK(copy_block(Ctmp, B, Cb, ld, m, B, st));
+      }
     } else if (src) {
       CK(adj_rows_init(nullptr, 0, (int)B, 0, src, lds, Wm, ld, j, N, status, st));  // rows [j, N): tril(L_bar)
     }
@@ -683,9 +686,12 @@ int adjoint_pipelined(const double* Lw, double* Wm, int64_t N, int64_t ld, int* 
       splitk_choice(m, k, B, &splits, &kps);
       CK(gemm_splitk_tn((int)B, (int)k, (int)m, splits, kps, cs + B * B, B, Lw + k * ld, ld, Pbuf, status, chain,
                         chain_res));
-      if (src) CK(adj_rows_init(Pbuf, splits, (int)B, k, src, lds, Wm, ld, j, N, status, chain));
-      else CK(splitk_reduce_sub(Pbuf, splits, (int)B, (int)k, Wm + j * ld, ld, status, chain));
-      CK(copy_block(cs + B * B, B, Cb, ld, m, B, chain));
+      if (src) {  // R0 + reduce + C_bar write-back in one launch
+        CK(adj_rows_init(Pbuf, splits, (int)B, k, src, lds, Wm, ld, j, N, status, chain, cs + B * B, B, Cb, ld, m));
+      } else {
+        CK(splitk_reduce_sub(Pbuf, splits, (int)B, (int)k, Wm + j * ld, ld, status, chain));
+        CK(copy_block(cs + B * B, B, Cb, ld, m, B, chain));
+      }
     } else if (src) {
       CK(adj_rows_init(nullptr, 0, (int)B, 0, src, lds, Wm, ld, j, N, status, chain));
     }

@@ -1367,27 +1367,36 @@ __global__ void splitk_reduce_sub_kernel(const double* __restrict__ P, int split
 // One CTA row per matrix row (blockIdx.y), double2 columns.
 __global__ void adj_rows_init_kernel(const double* __restrict__ P, int splits, int B, int64_t kc,
                                      const double* src, int64_t lds, double* dst, int64_t ldd, int64_t j, int64_t N,
-                                     const int* status) {
+                                     const int* status, const double* __restrict__ csrc, int64_t cld,
+                                     double* __restrict__ cdst, int64_t cldd, int crows) {
   pdl_enter();
   if (cta_status_set(status)) return;
-  const int r = blockIdx.y;
-  const int64_t gr = j + r;
   const long long plane = (long long)B * kc;
-  const double* srow = src + gr * lds;
-  double* drow = dst + gr * ldd;
-  const double* prow = P + (long long)r * kc;
-  for (int64_t c2 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; c2 < N / 2;
-       c2 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t c = 2 * c2;
+  const int half = (int)(N / 2), chalf = B / 2;
+  const long long n_init = (long long)B * half, n_all = n_init + (long long)crows * chalf;
+  for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < n_all;
+       idx += (long long)gridDim.x * blockDim.x) {
+    if (idx >= n_init) {
+      // the step's C_bar D^-1 back into A_bar (rows k.., columns [j, k)): the
+      // write-back, fused into this launch
+      const int t = (int)(idx - n_init), r = t / chalf, c = 2 * (t - r * chalf);
+      *reinterpret_cast<double2*>(cdst + (long long)r * cldd + c) =
+          *reinterpret_cast<const double2*>(csrc + (long long)r * cld + c);
+      continue;
+    }
+    const int r = (int)(idx / half);
+    const int64_t c = 2 * (int64_t)(idx - (long long)r * half);
+    const int64_t gr = j + r;
     double2 v = make_double2(0.0, 0.0);
     if (c <= gr) {
-      v = *reinterpret_cast<const double2*>(srow + c);
+      v = *reinterpret_cast<const double2*>(src + gr * lds + c);
       if (c + 1 > gr) v.y = 0.0;
     }
     if (c < kc && splits > 0) {
       // the partials summed first, in split order, then subtracted: the same
       // arithmetic as splitk_reduce_sub (results bit-identical to the unfused
       // path); the planes are loaded eight at a time ahead of the in-order adds
+      const double* prow = P + (long long)r * kc;
       double2 t = __ldcs(reinterpret_cast<const double2*>(prow + c));
       for (int z0 = 1; z0 < splits; z0 += 8) {
         double2 q[8];
@@ -1404,16 +1413,19 @@ __global__ void adj_rows_init_kernel(const double* __restrict__ P, int splits, i
       v.x -= t.x;
       v.y -= t.y;
     }
-    *reinterpret_cast<double2*>(drow + c) = v;
+    *reinterpret_cast<double2*>(dst + gr * ldd + c) = v;
   }
 }
 
 cudaError_t adj_rows_init(const double* P, int splits, int B, int64_t kc, const double* src, int64_t lds, double* dst,
-                          int64_t ldd, int64_t j, int64_t N, const int* status, cudaStream_t st) {
-  Prof prof_(PROF_MISC, 0.0, st, 8.0 * B * (splits * (double)kc + 1.5 * N));
+                          int64_t ldd, int64_t j, int64_t N, const int* status, cudaStream_t st, const double* csrc,
+                          int64_t cld, double* cdst, int64_t cldd, int64_t crows) {
+  Prof prof_(PROF_MISC, 0.0, st, 8.0 * B * (splits * (double)kc + 1.5 * N) + 16.0 * crows * B);
   if (B == 0 || N == 0) return cudaSuccess;
-  const int gx = (int)std::min<int64_t>((N / 2 + 255) / 256, 64);
-  return launch_pdl(adj_rows_init_kernel, dim3(gx, B), 256, 0, st, P, splits, B, kc, src, lds, dst, ldd, j, N, status);
+  if (!csrc) crows = 0;
+  const long long work = (long long)B * (N / 2) + crows * (B / 2);
+  return launch_pdl(adj_rows_init_kernel, grid_for(work, 256, 148 * 8), 256, 0, st, P, splits, B, kc, src, lds, dst,
+                    ldd, j, N, status, csrc, cld, cdst, cldd, (int)crows);
 }
 
 // +0.0 into the strict upper triangle outside the 128 x 128 diagonal tiles

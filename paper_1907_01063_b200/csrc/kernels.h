@@ -127,8 +127,11 @@ cudaError_t splitk_reduce_sub(const double* P, int splits, int M, int N, double*
 // R0 + the split-K reduction of rows [j, j+B) (first write to them in the sweep):
 // dst[j+r][c] = [c <= j+r] src[j+r][c] - [c < kc] sum_z P[z][r][c] for c < N
 // (P: splits planes of B x kc; src may equal dst; 16-B aligned rows, N, kc even)
+// (optional, fused) copy csrc[crows x B] (ld cld) -> cdst (ld cldd): the step's C_bar write-back
 cudaError_t adj_rows_init(const double* P, int splits, int B, int64_t kc, const double* src, int64_t lds, double* dst,
-                          int64_t ldd, int64_t j, int64_t N, const int* status, cudaStream_t st);
+                          int64_t ldd, int64_t j, int64_t N, const int* status, cudaStream_t st,
+                          const double* csrc = nullptr, int64_t cld = 0, double* cdst = nullptr, int64_t cldd = 0,
+                          int64_t crows = 0);
 // +0.0 into the strict upper triangle outside the 128 x 128 diagonal tiles
 cudaError_t zero_upper_offdiag(double* A, int64_t n, int64_t ld, cudaStream_t st);
 

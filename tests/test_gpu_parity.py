@@ -382,3 +382,40 @@ def test_graph_replay_same_buffers(sc, n):
         assert sc.cholesky_host(Ah, Lh) == 0
         lo = np.tril_indices(n)
         assert relf(Lh.numpy()[lo], oracle.cholesky(K)[lo]) <= L_BAR_TOL, it
+
+
+def _adjoint_bits_subprocess(env_extra, n):
+    """A_bar of the SE problem at order n from a fresh process with the given
+    environment (the schedule switches are read once per process)."""
+    import os
+    import subprocess
+    import sys
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, '.');"
+        "import oracle, paper_1907_01063_b200 as sc; from paper_1907_01063_b200 import inputs;"
+        f"n = {n}; K = oracle.se_cov(inputs.gp_x(n), 1.0, 1.0, 1e-6); L = oracle.cholesky_par(K);"
+        "W = inputs.lbar(n); A = sc.cholesky_adjoint(torch.from_numpy(L).cuda(), torch.from_numpy(W).cuda());"
+        "np.save(sys.argv[1], A.cpu().numpy())")
+    import tempfile
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "a.npy")
+        env = dict(os.environ, **env_extra)
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", code, out], env=env, cwd=root, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return np.load(out)
+
+
+@pytest.mark.parametrize("n", [1024, 3072])
+def test_adjoint_schedules_bit_identical(n):
+    """The three adjoint schedules (sequential, two-stream pipeline, merged
+    single stream -- STAN_CL_ADJ_PIPE=0/1/2) give the same bits:
+    every element receives the same updates from the same kernels in the same
+    order; and they match the oracle."""
+    got = {m: _adjoint_bits_subprocess({"STAN_CL_ADJ_PIPE": str(m)}, n) for m in (0, 1, 2)}
+    assert np.array_equal(got[0].view(np.int64), got[2].view(np.int64))
+    assert np.array_equal(got[1].view(np.int64), got[2].view(np.int64))
+    K = se(n)
+    want = oracle.cholesky_adjoint(oracle.cholesky_par(K), inputs.lbar(n))
+    assert relf(got[2], want) <= A_BAR_TOL
