@@ -250,3 +250,21 @@ def test_trace_timeline(sc):
     assert {s for _, s, _, _ in recs} == {0, 1}
     sc.cholesky(K)                                 # not traced any more
     assert len(sc.trace_read()) == len(recs)
+
+
+def test_c_api_demo_from_plain_c(sc, tmp_path):
+    """The boundary is usable from plain C (no Python, no torch): build
+    examples/c_api_demo.c with gcc against include/stan_cl.h and libstancl.so
+    and run it (log-det gradient identity, status codes, caller workspace)."""
+    import os
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = str(tmp_path / "c_api_demo")
+    lib_dir = os.path.join(root, "paper_1907_01063_b200")
+    cmd = ["gcc", "-O2", "-std=c99", os.path.join(root, "examples", "c_api_demo.c"), "-I", os.path.join(root, "include"),
+           "-I/usr/local/cuda/include", "-L" + lib_dir, "-lstancl", "-L/usr/local/cuda/lib64", "-lcudart",
+           "-Wl,-rpath," + lib_dir, "-lm", "-o", exe]
+    subprocess.run(cmd, check=True, capture_output=True, timeout=120)
+    r = subprocess.run([exe, "1500"], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, (r.stdout, r.stderr)
+    assert "not-PD info = 1" in r.stdout
