@@ -1136,10 +1136,180 @@ __global__ void __launch_bounds__(256, 2) trsm128_kernel(double* W, int64_t ld, 
   for (int q = 0; q < Q; ++q) P[p + 4 * q] = x[q];
 }
 
+// The 128-wide panel solve X L11^T = A21 as a blocked substitution with the
+// cross-block updates on the FP64 tensor cores (one launch).  The columns are
+// taken in 16-wide blocks b = 0..7 (the column-by-column elimination of
+// PAPER.md:277's solve, grouped):
+//   x_J  = a_J L_JJ^-T                    substitution, ascending j (J = block b)
+//   a_K -= x_J L_KJ^T   for K > J          DMMA.8x8x4, K = 16
+// A warp owns 8 rows; its 8 x 128 slice of the panel lives in registers in the
+// DMMA accumulator layout (lane (g, t): row g, columns 8 nt + 2t, +1 of every
+// 8-column tile nt), so the updates never leave registers.  For the
+// substitution the four lanes of a row gather the block's 16 values through a
+// per-warp shared slot and solve them redundantly: the dependency chain of a
+// column is then 4 FP64 operations in one lane (Markstein quotient + the next
+// column's fma), with no shuffle on it.  L11 is staged once per CTA: the
+// off-diagonal 16 x 16 blocks row-major with pitch 20 (= 4 mod 16: the DMMA
+// B-fragment reads are conflict-free), the diagonal blocks transposed (the
+// substitution reads L_cj for c > j as contiguous broadcasts), RN(1 / L_jj).
+// Every element sees the same operations as the substitution kernels except
+// that the cross-block sums are DMMA-accumulated (rounding order only; the
+// integer-exact families stay bit-exact).
+constexpr int TD_B = 16;                                   // column block
+constexpr int TD_P = 20;                                   // off-diagonal block pitch
+constexpr int TD_WARPS = 4;                                // 32 rows per CTA
+constexpr int TD_ROWS = 8 * TD_WARPS;
+constexpr int TD_NOFF = 28;                                // off-diagonal blocks of the 8 x 8 block triangle
+constexpr int TD_SMEM = (TD_NOFF * TD_B * TD_P + 8 * TD_B * TD_B + NB + TD_WARPS * 8 * TD_P) * (int)sizeof(double);
+
+__device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double b) {
+  // not volatile: a pure function of its operands, so ptxas may interleave the
+  // cross-block updates with the next block's substitution
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+__host__ __device__ constexpr int td_off(int bi, int bj) { return (bi - 1) * bi / 2 + bj; }  // bj < bi
+
+template <int B>
+__device__ __forceinline__ void trsm_dmma_block(double (&acc)[16][2], const double* Lo, const double* DT,
+                                                const double* rdg, double* Xs, double* P, int g, int t) {
+  // (1) gather block B's 16 columns of row g into every lane of the row
+  double* xr = Xs + g * TD_P;
+  *reinterpret_cast<double2*>(xr + 2 * t) = make_double2(acc[2 * B][0], acc[2 * B][1]);
+  *reinterpret_cast<double2*>(xr + 8 + 2 * t) = make_double2(acc[2 * B + 1][0], acc[2 * B + 1][1]);
+  __syncwarp();
+  double x[16];
+#pragma unroll
+  for (int c = 0; c < 16; c += 2) {
+    const double2 v = *reinterpret_cast<const double2*>(xr + c);
+    x[c] = v.x;
+    x[c + 1] = v.y;
+  }
+  // (2) substitution, ascending j (DT[j][c] = L[16B + c][16B + j])
+  const double* D = DT + B * TD_B * TD_B;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    x[j] = div_pos(x[j], D[j * TD_B + j], rdg[16 * B + j]);
+#pragma unroll
+    for (int c = j + 1; c < 16; ++c) x[c] = fma(-x[j], D[j * TD_B + c], x[c]);
+  }
+  __syncwarp();
+  if (t == 0) {
+#pragma unroll
+    for (int c = 0; c < 16; c += 2) *reinterpret_cast<double2*>(xr + c) = make_double2(x[c], x[c + 1]);
+  }
+  __syncwarp();
+  // (3) the solved block to global (accumulator positions)
+  {
+    const double2 v0 = *reinterpret_cast<const double2*>(xr + 2 * t);
+    const double2 v1 = *reinterpret_cast<const double2*>(xr + 8 + 2 * t);
+    *reinterpret_cast<double2*>(P + 16 * B + 2 * t) = v0;
+    *reinterpret_cast<double2*>(P + 16 * B + 8 + 2 * t) = v1;
+  }
+  if constexpr (B < 7) {
+    // (4) a_K -= x_J L_KJ^T for the later tiles, nearest first (the next
+    // block's columns are on the critical path)
+    double a[4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) a[kc] = -xr[4 * kc + t];  // A[g][k] = -x_g[4 kc + k] (exact)
+#pragma unroll
+    for (int nt = 2 * B + 2; nt < 16; ++nt) {
+      const double* Lb = Lo + td_off(nt >> 1, B) * TD_B * TD_P + (8 * (nt & 1) + g) * TD_P + t;
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) dmma_nv(acc[nt][0], acc[nt][1], a[kc], Lb[4 * kc]);  // B[k][n] = L[n][4kc + k]
+    }
+    __syncwarp();  // Xs is rewritten by the next block's gather
+    trsm_dmma_block<B + 1>(acc, Lo, DT, rdg, Xs, P, g, t);
+  }
+}
+
+__global__ void __launch_bounds__(32 * TD_WARPS, 2) trsm_dmma_kernel(double* W, int64_t ld, int64_t k0, int64_t r0,
+                                                                    const int* status) {
+  pdl_enter();
+  if (cta_status_set(status)) return;
+  extern __shared__ double smtd[];
+  double* Lo = smtd;                                  // 28 off-diagonal blocks [16][TD_P]
+  double* DT = Lo + TD_NOFF * TD_B * TD_P;            // 8 diagonal blocks, transposed [16][16]
+  double* rdg = DT + 8 * TD_B * TD_B;                 // RN(1 / L_jj)
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, g = lane >> 2, t = lane & 3;
+  const long long row = r0 + (long long)blockIdx.x * TD_ROWS + warp * 8 + g;
+  double* P = W + row * ld + k0;
+  double acc[16][2];
+#pragma unroll
+  for (int nt = 0; nt < 16; ++nt) {
+    const double2 v = *reinterpret_cast<const double2*>(P + 8 * nt + 2 * t);
+    acc[nt][0] = v.x;
+    acc[nt][1] = v.y;
+  }
+  // stage L11: (a) the 448 off-diagonal 16-wide row segments (128 B each, all
+  // loads of a thread in flight), (b) one row of the diagonal blocks per thread,
+  // stored transposed, and RN(1 / L_rr)
+  static_assert(32 * TD_WARPS == NB, "one diagonal-block row per thread");
+  const double* L11 = W + k0 * ld + k0;
+  {
+    constexpr int SEGS = TD_NOFF * TD_B, PER = (SEGS + NB - 1) / NB;
+    double2 v[PER][8];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int sg = tid + u * NB;
+      if (sg < SEGS) {
+        int bi = 1, q = sg >> 4;
+        while (q >= bi) q -= bi++;  // segment block (bi, q), q < bi
+        const double2* src = reinterpret_cast<const double2*>(L11 + (long long)(16 * bi + (sg & 15)) * ld + 16 * q);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[u][e] = src[e];
+      }
+    }
+    const int r = tid, bi = r >> 4, rr = r & 15;
+    const double2* dsrc = reinterpret_cast<const double2*>(L11 + (long long)r * ld + 16 * bi);
+    double2 d[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) d[e] = dsrc[e];  // (entries right of the diagonal are staged, never read)
+    const double drr = L11[(long long)r * ld + r];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int sg = tid + u * NB;
+      if (sg < SEGS) {
+        double2* dst = reinterpret_cast<double2*>(Lo + (sg >> 4) * TD_B * TD_P + (sg & 15) * TD_P);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dst[e] = v[u][e];
+      }
+    }
+    double* D = DT + bi * TD_B * TD_B + rr;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      D[(2 * e) * TD_B] = d[e].x;
+      D[(2 * e + 1) * TD_B] = d[e].y;
+    }
+    rdg[r] = rcp_pos(drr);
+  }
+  __syncthreads();  // (the strict upper halves of the DT blocks are never read)
+  trsm_dmma_block<0>(acc, Lo, DT, rdg, smtd + (TD_NOFF * TD_B * TD_P + 8 * TD_B * TD_B + NB) + warp * 8 * TD_P, P, g, t);
+}
+
+static int trsm_impl() {
+  static const int v = [] {
+    const char* e = getenv("STAN_CL_TRSM_IMPL");  // 0 = substitution kernels (round 1/2), 1 = DMMA-blocked
+    return e ? atoi(e) : 1;
+  }();
+  return v;
+}
+
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st, 16.0 * (r1 - r0) * NB + 4.0 * NB * NB);
+  if (trsm_impl() == 1 && (r1 - r0) % TD_ROWS == 0) {
+    static bool attr = false;
+    if (!attr) {
+      cudaError_t e = cudaFuncSetAttribute(trsm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TD_SMEM);
+      if (e != cudaSuccess) return e;
+      attr = true;
+    }
+    return launch_pdl(trsm_dmma_kernel, (int)((r1 - r0) / TD_ROWS), 32 * TD_WARPS, TD_SMEM, st, W, ld, k0, r0,
+                      status);
+  }
   // one launch for panels up to trsm128_maxm rows (latency-bound; measured
   // faster there), the two 64-wide substitutions + DMMA cross update above
   // (more CTAs per SM for the long panels of large n)
