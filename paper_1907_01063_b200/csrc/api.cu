@@ -431,6 +431,45 @@ int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status, co
     return STAN_CL_OK;
   };
   if ((rc = ship(0))) return rc;
+  // Lookahead on the side stream: the lookahead column update runs there too, so the chain
+  // LA(k) -> POTRF(k+1) -> TRSM(k+1) -> LA(k+1) is one stream with PDL
+  // boundaries instead of two cross-stream event hops per step.  LA(k+1)
+  // waits for SYRK(k) (main), which applied panel k to column block k+2.
+  //   side: [wait SYRK(k-1)] LA(k); panel(k+1)     main: [wait panel k] SYRK(k)
+  // Depth 2 (STAN_CL_LA_SIDE=2): SYRK(k) also leaves column block k+2 alone
+  // and LA(k+1) applies panels k and k+1 to it in one K = 2 OB product, so the
+  // side chain only waits for SYRK(k-1), a step further back.
+  static const int la_mode = [] {
+    const char* e = getenv("STAN_CL_LA_SIDE");  // 1 / 2 = depth, 0 = never, unset = auto
+    return e ? atoi(e) : -1;
+  }();
+  // auto (tools/quick_time.py, profiles/r02_forward_schedules.txt): LA on the main
+  // stream below 3072, depth 1 below 6144, depth 2 above (n = 16384: 49.5 -> 48.6 ms)
+  const int la_depth = side == main ? 0 : (la_mode >= 0 ? la_mode : (N >= 6144 ? 2 : (N >= 3072 ? 1 : 0)));
+  if (la_depth > 0) {
+    for (int64_t k = 0; k < T; ++k) {
+      CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
+      if (k == T - 1) break;
+      const int64_t c0 = k * OB, r1 = (k + 1) * OB, r2 = r1 + OB;
+      // LA(k): column block k+1 -= the panels not yet applied to it
+      const int64_t ka = (la_depth == 2 && k > 0) ? 2 * OB : OB, ca = c0 + OB - ka;
+      if (k >= la_depth) CK(cudaStreamWaitEvent(side, ev[2 + 2 * (k - la_depth)], 0));
+      const double* L21 = W + r1 * ld + ca;
+      CK(gemm_full(true, true, (int)(N - r1), (int)OB, (int)ka, -1.0, 1, L21, ld, L21, ld, W + r1 * ld + r1, ld,
+                   status, side, /*lower_only=*/1, PROF_LOOKAHEAD));
+      rc = panel(W, ld, r1, N, OB, status, side);
+      if (rc) return rc;
+      CK(cudaEventRecord(ev[1 + 2 * (k + 1)], side));
+      if ((rc = ship(k + 1))) return rc;
+      const int64_t rs = r2 + (la_depth == 2 ? OB : 0);  // SYRK(k) covers rows / columns >= rs
+      if (rs < N) {
+        const double* L31 = W + rs * ld + c0;
+        CK(gemm_lower_nt((int)(N - rs), (int)OB, L31, ld, L31, ld, W + rs * ld + rs, ld, status, main));
+      }
+      CK(cudaEventRecord(ev[2 + 2 * k], main));
+    }
+    return STAN_CL_OK;
+  }
   for (int64_t k = 0; k < T; ++k) {
     CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
     if (k == T - 1) break;

@@ -384,6 +384,50 @@ def test_graph_replay_same_buffers(sc, n):
         assert relf(Lh.numpy()[lo], oracle.cholesky(K)[lo]) <= L_BAR_TOL, it
 
 
+def _forward_subprocess(env_extra, n, nb, exact=False):
+    """L of the SE problem (or of the integer-exact family) at order n from a
+    fresh process with the given environment."""
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    make = (f"L0 = inputs.unit_lower_pm1(n, seed=11); K = inputs.gram_exact(L0)" if exact
+            else "K = oracle.se_cov(inputs.gp_x(n), 1.0, 1.0, 1e-6)")
+    code = (
+        "import sys, numpy as np, torch; sys.path.insert(0, '.');"
+        "import oracle, paper_1907_01063_b200 as sc; from paper_1907_01063_b200 import inputs;"
+        f"n = {n}; {make}; lib = sc.load(); assert lib.stan_cl_set_block_size({nb}) == 0;"
+        "L = sc.cholesky(torch.from_numpy(K).cuda());"
+        "np.save(sys.argv[1], L.cpu().numpy())")
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "l.npy")
+        env = dict(os.environ, **env_extra)
+        root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        r = subprocess.run([sys.executable, "-c", code, out], env=env, cwd=root, capture_output=True, text=True,
+                           timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        return np.load(out)
+
+
+@pytest.mark.parametrize("n,nb", [(1024, 128), (2048, 256), (3000, 128)])
+def test_forward_schedules(n, nb):
+    """The forward's lookahead schedules (STAN_CL_LA_SIDE = 0: lookahead column
+    on the main stream; 1: on the side stream; 2: depth 2, the column block
+    k+2 taking panels k and k+1 in one product) at 128- and 256-wide outer
+    blocks: each within the L tolerance of the oracle, the integer-exact family
+    bit for bit."""
+    K = se(n)
+    want = oracle.cholesky(K)
+    lo = np.tril_indices(n)
+    L0 = inputs.unit_lower_pm1(n, seed=11)
+    for m in ("0", "1", "2"):
+        env = {"STAN_CL_LA_SIDE": m}
+        got = _forward_subprocess(env, n, nb)
+        assert relf(got[lo], want[lo]) <= L_BAR_TOL, m
+        assert np.all(np.triu(got, 1) == 0)
+        assert np.array_equal(_forward_subprocess(env, n, nb, exact=True), L0), m
+
+
 def _adjoint_bits_subprocess(env_extra, n):
     """A_bar of the SE problem at order n from a fresh process with the given
     environment (the schedule switches are read once per process)."""

@@ -52,7 +52,15 @@ def main():
     print("# class            stream  launches    busy ms")
     for (k, s), (c, ms) in sorted(by.items(), key=lambda x: -x[1][1]):
         print(f"  {k:16s} {s:6d} {c:9d} {ms:10.3f}")
-    if which == "forward":
+    if os.environ.get("TIMELINE_RAW"):
+        # every launch in start order: stream, class, start, duration, gap after the previous launch on its stream
+        last = {}
+        print("# stream class            start_ms   dur_us  gap_us")
+        for k, s, a, b in sorted(recs, key=lambda r: r[2]):
+            g = (a - last[s]) * 1e3 if s in last else float("nan")
+            last[s] = b
+            print(f"  {s:5d}  {k:14s} {a:9.4f} {1e3 * (b - a):8.1f} {g:7.1f}")
+    if which == "forward" and any(r[0] == "lookahead" and r[1] == 0 for r in recs):
         # chain: POTRF launches mark the steps
         pot = [r for r in recs if r[0] == "potrf"]
         la = [r for r in recs if r[0] == "lookahead" and r[1] == 0]
