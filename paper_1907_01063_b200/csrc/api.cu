@@ -701,6 +701,15 @@ int adjoint_pipelined(const double* Lw, double* Wm, int64_t N, int64_t ld, int* 
     CK(cudaEventRecord(ev[0], main));
     CK(cudaStreamWaitEvent(chain, ev[0], 0));
   }
+  // one stream: the merged update of step s and C_bar D^-1 of step s+1 share a
+  // persistent launch (the update's column block [j - B, j) -- the next C_bar --
+  // goes first and is counted; adj_update_fused_trmm).  STAN_CL_ADJ_FUSE=0: separate launches.
+  static const bool fuse_env = !getenv("STAN_CL_ADJ_FUSE") || atoi(getenv("STAN_CL_ADJ_FUSE")) != 0;
+  const bool fuse = fuse_env && !two_streams;
+  int* dep_cnt = status + 32;
+  int cnt_base = 0;
+  bool cdinv_ready = false;  // C_bar D^-1 of this step already computed by the previous launch
+  if (fuse) CK(cudaMemsetAsync(dep_cnt, 0, sizeof(int), main));
   int64_t s = 0;
   for (int64_t k = N; k > 0; k -= B, ++s) {
     const int64_t j = k - B, m = N - k;
@@ -716,8 +725,9 @@ int adjoint_pipelined(const double* Lw, double* Wm, int64_t N, int64_t ld, int* 
     if (two_streams && s >= 3) CK(cudaStreamWaitEvent(chain, ev[3 + 3 * (s - 3)], 0));
     if (m > 0) {
       // C_adj = C_adj * lower_triangular_inverse(D)
-      CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, cs + B * B, B, status, chain, 0,
-                   PROF_TRMM, true, chain_res, TRI_B_LOWER));
+      if (!cdinv_ready)
+        CK(gemm_full(true, false, (int)m, (int)B, (int)B, 1.0, 0, Cb, ld, Db, B, cs + B * B, B, status, chain, 0,
+                     PROF_TRMM, true, chain_res, TRI_B_LOWER));
       // [R_adj D_adj] -= C_adj^T [B C], split-K
       // the split is the sequential sweep's (a function of m, k only), so the
       // partial sums -- and every bit of the result -- match adjoint_inplace
@@ -738,9 +748,20 @@ int adjoint_pipelined(const double* Lw, double* Wm, int64_t N, int64_t ld, int* 
     CK(adj_diag_fused((int)B, D, ld, Dbar, ld, Db, T1, T2, T3, cs, (unsigned*)status + 16, status, chain));
     if (!two_streams) {
       // one stream: [R_adj; B_adj] -= [S; C_adj] R over all of [0, j) in one launch
-      if (j > 0)
+      cdinv_ready = false;
+      if (j > 0 && fuse) {
+        // + C_bar' D'^-1 of step s+1 (C_bar' = rows [j, N) of column block [j - B, j))
+        double* cs1 = (double*)(csb + (size_t)((s + 1) % 3) * csz);
+        int dep = 0;
+        CK(adj_update_fused_trmm((int)(B + m), (int)j, (int)B, cs, B, R, ld, Wm + j * ld, ld, (int)(m + B),
+                                 Wm + j * ld + (j - B), ld, Dinv + ((j - B) / B) * B * B, B, cs1 + B * B, B,
+                                 (int)(B / 64), dep_cnt, cnt_base, &dep, status, main));
+        cnt_base += dep;
+        cdinv_ready = true;
+      } else if (j > 0) {
         CK(gemm_full(true, false, (int)(B + m), (int)j, (int)B, -1.0, 1, cs, B, R, ld, Wm + j * ld, ld, status, main, 0,
                      PROF_GEMM));
+      }
       continue;
     }
     // [R_adj; B_adj] -= [S; C_adj] R on the lookahead column [j - B, j)

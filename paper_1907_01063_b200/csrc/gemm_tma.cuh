@@ -141,6 +141,9 @@ __device__ __forceinline__ double frag(const double* s, int rc, int k) {
 template <class CF, int MODE>
 struct TItemMap {
   int ntn, ntm, ntiles, ktiles_full;
+  // MODE_FULL: enumerate the last first_cols tile columns first (a fused
+  // launch's dependency tiles, TFuse), then the rest row-major
+  int first_cols = 0;
   // block-cyclic mode (MODE_CYC): items enumerate, per 256-wide
   // block column j, only its tile rows from the first block row that reaches
   // the diagonal (RB f_j) down; cyc_pref[j] = first item of block column j
@@ -175,6 +178,34 @@ struct TItemMap {
       tn = tile / ntm;
       tm = tile - tn * ntm;
       return;
+    }
+    if constexpr (MODE == MODE_FULL) {
+      if (first_cols > 0) {
+        const int d = ntm * first_cols;
+        if (tile < d) {
+          tm = tile / first_cols;
+          tn = ntn - first_cols + (tile - tm * first_cols);
+        } else {
+          const int t2 = tile - d, w = ntn - first_cols;
+          tm = t2 / w;
+          tn = t2 - tm * w;
+        }
+        return;
+      }
+      // a triangular operand makes the items' K extents unequal: enumerate
+      // longest first (tiles are dealt to the CTAs round-robin, so the long
+      // items land in the first round and the short ones fill the second)
+      if (p.tri & (TRI_B_LOWER | TRI_B_UPPER)) {
+        tn = tile / ntm;
+        tm = tile - tn * ntm;
+        if (p.tri & TRI_B_UPPER) tn = ntn - 1 - tn;  // K = n0 + BN: longest at the right
+        return;
+      }
+      if (p.tri & TRI_A_LOWER) {  // K = m0 + BM: longest at the bottom
+        tm = ntm - 1 - tile / ntn;
+        tn = tile - (ntm - 1 - tm) * ntn;
+        return;
+      }
     }
     tm = tile / ntn;
     tn = tile - tm * ntn;
@@ -243,6 +274,30 @@ struct TItemMap {
   }
 };
 
+// Two GEMM problems in one persistent launch (MODE_FULL, same layouts, B not
+// k-major): items [0, n1) are problem 1 (p, map), [n1, nitems) problem 2
+// (p2, map2, A through the second tensor map).  Problem 2 may read what
+// problem 1 writes: the first `dep` items of problem 1 each add 1 to *cnt when
+// their tile is stored (release), and problem 2's producer waits until *cnt >=
+// target (acquire, then a generic -> async proxy fence) before its first TMA
+// load.  Problem-2 items come last in every CTA's list and all CTAs of the
+// persistent grid are resident, so the wait always ends.
+template <class CF>
+struct TFuse {
+  GemmArgs p2;
+  TItemMap<CF, MODE_FULL> map2;
+  int n1 = 0x7fffffff;
+  int* cnt = nullptr;
+  int dep = 0;
+  int target = 0;
+};
+
+__device__ __forceinline__ int ld_acquire_gpu(const int* a) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+
 template <int ROWS, bool KMAJ, int BKS>
 __device__ __forceinline__ void produce_slab(double* dst, const CUtensorMap* map, const double* g, long long ld,
                                              int row0, int k0, int lane, uint64_t* bar) {
@@ -256,10 +311,12 @@ __device__ __forceinline__ void produce_slab(double* dst, const CUtensorMap* map
   }
 }
 
-template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
+template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE, bool FUSE>
 __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    GemmArgs p, int nitems, TItemMap<CF, MODE> map) {
+                    const __grid_constant__ GemmArgs p, int nitems, TItemMap<CF, MODE> map,
+                    const __grid_constant__ CUtensorMap tmA2,
+                    const __grid_constant__ TFuse<CF> fz) {
   using namespace tg;
   constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, NCONS = CF::NCONS;
   constexpr int MI = CF::MI, NI = CF::NI;
@@ -299,18 +356,34 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
       if (B_KMAJ) prefetch_tmap(&tmB);
     }
     int it = 0;
+    bool waited = false;
     for (int item = map.next_valid(p, blockIdx.x, gridDim.x, nitems); item < nitems;
          item = map.next_valid(p, item + gridDim.x, gridDim.x, nitems)) {
       int m0, n0, kbeg, ns, z;
-      map.get(p, item, m0, n0, kbeg, ns, z);
+      const bool two = FUSE && item >= fz.n1;
+      const GemmArgs& q = two ? fz.p2 : p;
+      if (two) {
+        fz.map2.get(q, item - fz.n1, m0, n0, kbeg, ns, z);
+        if (!waited && fz.cnt) {
+          if (lane == 0) {
+            while (ld_acquire_gpu(fz.cnt) < fz.target) __nanosleep(100);
+            asm volatile("fence.proxy.async.global;\n" ::: "memory");
+          }
+          __syncwarp();
+          waited = true;
+        }
+      } else {
+        map.get(p, item, m0, n0, kbeg, ns, z);
+      }
+      const CUtensorMap* ta = two ? &tmA2 : &tmA;
       for (int s = 0; s < ns; ++s, ++it) {
         const int slot = it % STAGES, round = it / STAGES;
         if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
         if (lane == 0) mbar_arrive_expect_tx(&full[slot], SA::TX + SB::TX);
         __syncwarp();
         const int k0 = kbeg + s * BKS;
-        produce_slab<BM, A_KMAJ, BKS>(sA + slot * (SA::BYTES / 8), &tmA, p.A, p.lda, m0, k0, lane, &full[slot]);
-        produce_slab<BN, B_KMAJ, BKS>(sB + slot * (SB::BYTES / 8), &tmB, p.B, p.ldb, n0, k0, lane, &full[slot]);
+        produce_slab<BM, A_KMAJ, BKS>(sA + slot * (SA::BYTES / 8), ta, q.A, q.lda, m0, k0, lane, &full[slot]);
+        produce_slab<BN, B_KMAJ, BKS>(sB + slot * (SB::BYTES / 8), &tmB, q.B, q.ldb, n0, k0, lane, &full[slot]);
       }
     }
     return;
@@ -319,24 +392,38 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
   // -------------------------------------------------------------- consumers
   const int wm = warp / CF::WARPS_N, wn = warp % CF::WARPS_N;
   const int g = lane >> 2, t = lane & 3;
-  const bool need_c = (MODE != MODE_SPLITK) && p.beta != 0;
-  const unsigned long long smask = (p.sign < 0) ? 0x8000000000000000ull : 0ull;
   double2* myC = reinterpret_cast<double2*>(sC) + (size_t)warp * MI * NI * 32 + lane;
-  auto load_c = [&](int m0, int n0) {
+  auto load_c = [&](const GemmArgs& q, int m0, int n0) {
 #pragma unroll
     for (int i = 0; i < MI; ++i)
 #pragma unroll
       for (int j = 0; j < NI; ++j) {
         const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
-        cp_async16(myC + (i * NI + j) * 32, p.C + (long long)r * p.ldc + c);
+        cp_async16(myC + (i * NI + j) * 32, q.C + (long long)r * q.ldc + c);
       }
     cp_async_commit();
   };
+  const GemmArgs* const P1 = &p;  // __grid_constant__: addresses of the parameters themselves
+  const GemmArgs* const P2 = &fz.p2;
+  auto resolve = [&](int item, int& m0, int& n0, int& kbeg, int& ns, int& z) -> const GemmArgs* {
+    if (FUSE && item >= fz.n1) {
+      fz.map2.get(fz.p2, item - fz.n1, m0, n0, kbeg, ns, z);
+      return P2;
+    }
+    map.get(p, item, m0, n0, kbeg, ns, z);
+    return P1;
+  };
+  auto needs_c = [&](const GemmArgs& q) { return (MODE != MODE_SPLITK) && q.beta != 0; };
   int m0, n0, kbeg, ns, z;
   const int first = map.next_valid(p, blockIdx.x, gridDim.x, nitems);
   if (first >= nitems) return;
-  map.get(p, first, m0, n0, kbeg, ns, z);
-  if (CF::CPREF && need_c) load_c(m0, n0);
+  const GemmArgs* q = resolve(first, m0, n0, kbeg, ns, z);
+  // the current item's problem (a compile-time reference to p unless fused)
+  auto QQ = [&]() -> const GemmArgs& {
+    if constexpr (FUSE) return *q;
+    else return p;
+  };
+  if (CF::CPREF && needs_c(QQ())) load_c(QQ(), m0, n0);
   int kap[4];
 #pragma unroll
   for (int s = 0; s < 4; ++s) kap[s] = kappa(s, t);
@@ -344,6 +431,8 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
   double acc[MI][NI][2];
   for (int item = first; item < nitems;) {
     const int nxt_item = map.next_valid(p, item + gridDim.x, gridDim.x, nitems);
+    const bool need_c = needs_c(QQ());
+    const unsigned long long smask = (QQ().sign < 0) ? 0x8000000000000000ull : 0ull;
     if (need_c && CF::CPREF) {
       cp_async_wait<0>();
 #pragma unroll
@@ -360,7 +449,7 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
 #pragma unroll
         for (int j = 0; j < NI; ++j) {
           const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
-          const double2 v = *reinterpret_cast<const double2*>(p.C + (long long)r * p.ldc + c);
+          const double2 v = *reinterpret_cast<const double2*>(QQ().C + (long long)r * QQ().ldc + c);
           acc[i][j][0] = xor_sign(v.x, smask);
           acc[i][j][1] = xor_sign(v.y, smask);
         }
@@ -390,32 +479,29 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
-      if (CF::CPREF && need_c && s == 0) {
+      if (CF::CPREF && s == 0 && nxt_item < nitems) {
         // prefetch the next item's C into the private slots only now: the DMMAs
         // above consumed acc (loaded from these slots), and asm-volatile order
         // keeps this cp.async behind them, so the refill cannot overtake the read
-        const int nxt = nxt_item;
-        if (nxt < nitems) {
-          int m1, n1, kb1, ns1, z1;
-          map.get(p, nxt, m1, n1, kb1, ns1, z1);
-          load_c(m1, n1);
-        }
+        int m1, n1, kb1, ns1, z1;
+        const GemmArgs* q1 = resolve(nxt_item, m1, n1, kb1, ns1, z1);
+        if (needs_c(FUSE ? *q1 : p)) load_c(FUSE ? *q1 : p, m1, n1);
       }
     }
     // epilogue: registers -> global
     double* Cout;
     long long ldo;
     if constexpr (MODE == MODE_SPLITK) {
-      Cout = p.C + (long long)z * p.M * p.N;
-      ldo = p.N;
+      Cout = QQ().C + (long long)z * QQ().M * QQ().N;
+      ldo = QQ().N;
     } else {
-      Cout = p.C;
-      ldo = p.ldc;
+      Cout = QQ().C;
+      ldo = QQ().ldc;
     }
-    bool cmask;
-    int dd;
-    map.valid(p, item, cmask, dd);  // block-cyclic diagonal block: keep r >= c + dd
-    const bool mask = (MODE == MODE_LOWER) || ((MODE == MODE_FULL || MODE == MODE_CYC) && (p.lower_only || cmask));
+    bool cmask = false;
+    int dd = 0;
+    if (!FUSE || item < fz.n1) map.valid(p, item, cmask, dd);  // block-cyclic diagonal block: keep r >= c + dd
+    const bool mask = (MODE == MODE_LOWER) || ((MODE == MODE_FULL || MODE == MODE_CYC) && (QQ().lower_only || cmask));
     const bool crosses = mask && (n0 + BN - 1 + dd > m0);
 #pragma unroll
     for (int i = 0; i < MI; ++i)
@@ -431,7 +517,16 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
           *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
         }
       }
-    if (nxt_item < nitems) map.get(p, nxt_item, m0, n0, kbeg, ns, z);
+    if (FUSE && item < fz.dep && fz.cnt) {
+      // a dependency tile of the fused problem 2: every consumer's stores, then
+      // one release increment
+      asm volatile("bar.sync 1, %0;\n" ::"n"(NCONS) : "memory");
+      if (tid == 0) {
+        __threadfence();
+        atomicAdd(fz.cnt, 1);
+      }
+    }
+    if (nxt_item < nitems) q = resolve(nxt_item, m0, n0, kbeg, ns, z);
     item = nxt_item;
   }
 }
@@ -442,22 +537,8 @@ int tma_num_sms();
 bool make_kmajor_map(CUtensorMap* map, const double* X, long long rows, long long K, long long ld,
                      int box_rows);
 
-template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
-cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reserve_sms = 0) {
-  using SM = tg::Smem<CF, A_KMAJ, B_KMAJ>;
-  auto kern = gemm_tma_kernel<CF, A_KMAJ, B_KMAJ, MODE>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  CUtensorMap ma, mb;
-  memset(&ma, 0, sizeof(ma));
-  memset(&mb, 0, sizeof(mb));
-  if (A_KMAJ && !make_kmajor_map(&ma, p.A, p.M, p.K, p.lda, CF::BM)) return cudaErrorInvalidValue;
-  if (B_KMAJ && !make_kmajor_map(&mb, p.B, p.N, p.K, p.ldb, CF::BN)) return cudaErrorInvalidValue;
-  TItemMap<CF, MODE> map;
+template <class CF, int MODE>
+int tma_item_map(const GemmArgs& p, TItemMap<CF, MODE>& map) {
   map.ntn = p.N / CF::BN;
   map.ntm = p.M / CF::BM;
   map.ktiles_full = p.K / CF::BKS;
@@ -472,7 +553,7 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reser
   if constexpr (MODE == MODE_CYC) {
     {  // valid tile rows per 256-wide block column
       const int nbc = p.N / 256, nbr = p.M / 256;
-      if (nbc > TItemMap<CF, MODE>::kCycMax) return cudaErrorInvalidValue;
+      if (nbc > TItemMap<CF, MODE>::kCycMax) return -1;
       map.cyc_nb = nbc;
       map.cyc_pref[0] = 0;
       for (int j = 0; j < nbc; ++j) {
@@ -486,12 +567,59 @@ cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reser
     }
   }
   map.ntiles = ntiles;
-  const int nitems = ntiles * (MODE == MODE_SPLITK ? splits : 1);
+  return ntiles;
+}
+
+template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
+cudaError_t launch_tma_impl(const GemmArgs& p, int splits, cudaStream_t st, int reserve_sms, const GemmArgs* p2,
+                            int first_cols, int* cnt, int cnt_base) {
+  using SM = tg::Smem<CF, A_KMAJ, B_KMAJ>;
+  auto kern = gemm_tma_kernel<CF, A_KMAJ, B_KMAJ, MODE, false>;
+  if constexpr (MODE == MODE_FULL && !B_KMAJ) {  // the only fused shape (adj_update_fused_trmm)
+    if (p2) kern = gemm_tma_kernel<CF, A_KMAJ, B_KMAJ, MODE, true>;
+  }
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[p2 ? 1 : 0]) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set[p2 ? 1 : 0] = true;
+  }
+  CUtensorMap ma, mb, ma2;
+  memset(&ma, 0, sizeof(ma));
+  memset(&mb, 0, sizeof(mb));
+  memset(&ma2, 0, sizeof(ma2));
+  if (A_KMAJ && !make_kmajor_map(&ma, p.A, p.M, p.K, p.lda, CF::BM)) return cudaErrorInvalidValue;
+  if (B_KMAJ && !make_kmajor_map(&mb, p.B, p.N, p.K, p.ldb, CF::BN)) return cudaErrorInvalidValue;
+  TItemMap<CF, MODE> map;
+  const int ntiles = tma_item_map<CF, MODE>(p, map);
+  if (ntiles < 0) return cudaErrorInvalidValue;
+  int nitems = ntiles * (MODE == MODE_SPLITK ? splits : 1);
+  TFuse<CF> fz;
+  if constexpr (MODE == MODE_FULL) {
+    if (p2) {
+      // problem 1's last first_cols tile columns first (counted), then problem 2
+      if (B_KMAJ || first_cols <= 0 || first_cols > map.ntn) return cudaErrorInvalidValue;
+      map.first_cols = first_cols;
+      fz.p2 = *p2;
+      const int n2 = tma_item_map<CF, MODE_FULL>(*p2, fz.map2);
+      if (A_KMAJ && !make_kmajor_map(&ma2, p2->A, p2->M, p2->K, p2->lda, CF::BM)) return cudaErrorInvalidValue;
+      fz.n1 = nitems;
+      fz.cnt = cnt;
+      fz.dep = map.ntm * first_cols;
+      fz.target = cnt_base + fz.dep;  // *cnt counts monotonically across launches
+      nitems += n2;
+    }
+  }
   if (nitems == 0) return cudaSuccess;
   // reserve_sms: SMs left free for kernels on other streams
   const int nsm = (tma_num_sms() - (reserve_sms > 0 && reserve_sms < tma_num_sms() ? reserve_sms : 0)) * CF::MINB;
   const int grid = nitems < nsm ? nitems : nsm;
-  return launch_pdl(kern, grid, CF::NCONS + 32, SM::TOTAL, st, ma, mb, p, nitems, map);
+  return launch_pdl(kern, grid, CF::NCONS + 32, SM::TOTAL, st, ma, mb, p, nitems, map, ma2, fz);
+}
+
+template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
+cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reserve_sms = 0) {
+  return launch_tma_impl<CF, A_KMAJ, B_KMAJ, MODE>(p, splits, st, reserve_sms, nullptr, 0, nullptr, 0);
 }
 
 }  // namespace stancl

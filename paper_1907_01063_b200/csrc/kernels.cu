@@ -1450,6 +1450,27 @@ cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign
   }
 }
 
+// The adjoint's merged update of step s fused with the panel product of step
+// s+1 in one persistent launch (gemm_tma.cuh TFuse):
+//   problem 1: C1[M1 x N1] -= A1[M1 x K] B1[K x N1]   (A1 k-major; [R_bar; B_bar] -= [S; C_bar D^-1] R)
+//   problem 2: C2[M2 x K]   = A2[M2 x K] B2[K x K]     (B2 lower triangular; C_bar' D'^-1)
+// Problem 1's last first_cols tile columns (the next step's C_bar') come first
+// and are counted on *cnt; problem 2 starts loading once *cnt reaches
+// cnt_base + their count (returned through *dep_out).
+cudaError_t adj_update_fused_trmm(int M1, int N1, int K, const double* A1, int64_t lda1, const double* B1,
+                                  int64_t ldb1, double* C1, int64_t ldc1, int M2, const double* A2, int64_t lda2,
+                                  const double* B2, int64_t ldb2, double* C2, int64_t ldc2, int first_cols, int* cnt,
+                                  int cnt_base, int* dep_out, const int* status, cudaStream_t st) {
+  using CF = tg::CfgT32;
+  GemmArgs p1{A1, lda1, B1, ldb1, C1, ldc1, M1, N1, K, K, -1.0, 1, 0, status, cfgsel().pingpong};
+  GemmArgs p2{A2, lda2, B2, ldb2, C2, ldc2, M2, K, K, K, 1.0, 0, 0, status, cfgsel().pingpong};
+  p2.tri = TRI_B_LOWER;
+  Prof prof_(PROF_GEMM, 2.0 * M1 * N1 * K + 1.0 * M2 * K * K, st,
+             16.0 * M1 * N1 + 8.0 * ((double)M1 * K + (double)N1 * K) + 16.0 * M2 * K + 8.0 * K * K);
+  *dep_out = (M1 / CF::BM) * first_cols;
+  return launch_tma_impl<CF, true, false, MODE_FULL>(p1, 1, st, 0, &p2, first_cols, cnt, cnt_base);
+}
+
 cudaError_t gemm_cyclic_lower(int M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,
                               double* C, int64_t ldc, int P, int p, int Q, int q, int li0, int lj0, const int* status,
                               cudaStream_t st, int reserve_sms) {

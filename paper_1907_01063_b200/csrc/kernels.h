@@ -102,6 +102,12 @@ enum TriBits { TRI_A_LOWER = 1, TRI_A_UPPER = 2, TRI_B_LOWER = 4, TRI_B_UPPER = 
 // allow_persistent = false keeps the one-tile-per-CTA kernel (for work issued on
 // the lookahead side stream, which must not hold SMs the trailing update needs);
 // reserve_sms: the persistent kernel leaves that many SMs free for other streams
+// [R_bar; B_bar] -= [S; C_bar D^-1] R of step s with C_bar' D'^-1 of step s+1 in
+// one persistent launch (kernels.cu; gemm_tma.cuh TFuse)
+cudaError_t adj_update_fused_trmm(int M1, int N1, int K, const double* A1, int64_t lda1, const double* B1,
+                                  int64_t ldb1, double* C1, int64_t ldc1, int M2, const double* A2, int64_t lda2,
+                                  const double* B2, int64_t ldb2, double* C2, int64_t ldc2, int first_cols, int* cnt,
+                                  int cnt_base, int* dep_out, const int* status, cudaStream_t st);
 cudaError_t gemm_full(bool a_kmaj, bool b_kmaj, int M, int N, int K, double sign, int beta,
                       const double* A, int64_t lda, const double* B, int64_t ldb, double* C,
                       int64_t ldc, const int* status, cudaStream_t st, int lower_only = 0,
