@@ -418,12 +418,7 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
   const int first = map.next_valid(p, blockIdx.x, gridDim.x, nitems);
   if (first >= nitems) return;
   const GemmArgs* q = resolve(first, m0, n0, kbeg, ns, z);
-  // the current item's problem (a compile-time reference to p unless fused)
-  auto QQ = [&]() -> const GemmArgs& {
-    if constexpr (FUSE) return *q;
-    else return p;
-  };
-  if (CF::CPREF && needs_c(QQ())) load_c(QQ(), m0, n0);
+  if (CF::CPREF && needs_c((FUSE ? *q : p))) load_c((FUSE ? *q : p), m0, n0);
   int kap[4];
 #pragma unroll
   for (int s = 0; s < 4; ++s) kap[s] = kappa(s, t);
@@ -431,8 +426,8 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
   double acc[MI][NI][2];
   for (int item = first; item < nitems;) {
     const int nxt_item = map.next_valid(p, item + gridDim.x, gridDim.x, nitems);
-    const bool need_c = needs_c(QQ());
-    const unsigned long long smask = (QQ().sign < 0) ? 0x8000000000000000ull : 0ull;
+    const bool need_c = needs_c((FUSE ? *q : p));
+    const unsigned long long smask = ((FUSE ? *q : p).sign < 0) ? 0x8000000000000000ull : 0ull;
     if (need_c && CF::CPREF) {
       cp_async_wait<0>();
 #pragma unroll
@@ -449,7 +444,7 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
 #pragma unroll
         for (int j = 0; j < NI; ++j) {
           const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
-          const double2 v = *reinterpret_cast<const double2*>(QQ().C + (long long)r * QQ().ldc + c);
+          const double2 v = *reinterpret_cast<const double2*>((FUSE ? *q : p).C + (long long)r * (FUSE ? *q : p).ldc + c);
           acc[i][j][0] = xor_sign(v.x, smask);
           acc[i][j][1] = xor_sign(v.y, smask);
         }
@@ -492,16 +487,16 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
     double* Cout;
     long long ldo;
     if constexpr (MODE == MODE_SPLITK) {
-      Cout = QQ().C + (long long)z * QQ().M * QQ().N;
-      ldo = QQ().N;
+      Cout = (FUSE ? *q : p).C + (long long)z * (FUSE ? *q : p).M * (FUSE ? *q : p).N;
+      ldo = (FUSE ? *q : p).N;
     } else {
-      Cout = QQ().C;
-      ldo = QQ().ldc;
+      Cout = (FUSE ? *q : p).C;
+      ldo = (FUSE ? *q : p).ldc;
     }
     bool cmask = false;
     int dd = 0;
     if (!FUSE || item < fz.n1) map.valid(p, item, cmask, dd);  // block-cyclic diagonal block: keep r >= c + dd
-    const bool mask = (MODE == MODE_LOWER) || ((MODE == MODE_FULL || MODE == MODE_CYC) && (QQ().lower_only || cmask));
+    const bool mask = (MODE == MODE_LOWER) || ((MODE == MODE_FULL || MODE == MODE_CYC) && ((FUSE ? *q : p).lower_only || cmask));
     const bool crosses = mask && (n0 + BN - 1 + dd > m0);
 #pragma unroll
     for (int i = 0; i < MI; ++i)
