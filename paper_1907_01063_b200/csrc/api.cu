@@ -39,6 +39,7 @@ namespace {
 struct State {
   cudaStream_t stream = nullptr;  // nullptr = legacy default stream
   cudaStream_t side = nullptr;    // library-owned high-priority stream (panel lookahead)
+  cudaStream_t aux = nullptr;     // library-owned stream: the lookahead rows below the diagonal tile
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the *_host entry points
   std::vector<cudaEvent_t> events;
   std::vector<cudaEvent_t> xev;  // per-block events of the streamed host transfers
@@ -443,9 +444,121 @@ int factor_inplace(double* W, int64_t N, int64_t ld, int64_t OB, int* status, co
     const char* e = getenv("STAN_CL_LA_SIDE");  // 1 / 2 = depth, 0 = never, unset = auto
     return e ? atoi(e) : -1;
   }();
-  // auto (tools/quick_time.py, profiles/r02_forward_schedules.txt): LA on the main
-  // stream below 3072, depth 1 below 6144, depth 2 above (n = 16384: 49.5 -> 48.6 ms)
-  const int la_depth = side == main ? 0 : (la_mode >= 0 ? la_mode : (N >= 6144 ? 2 : (N >= 3072 ? 1 : 0)));
+  // auto (tools/quick_time.py): 128-wide steps (n < 6144) the split schedule below
+  // (forward -10..12% at n = 1024 ... 4096 against LA on either stream); 256-wide
+  // steps the split schedule below 12288 (6144: 4.95 -> 4.47 ms, 8192: 8.56 -> 8.00)
+  // and depth 2 above (n = 16384: 49.5 -> 48.6 ms against LA on the main stream;
+  // split: 49.4 -- its third-stream GEMMs are big there and take SMs from the SYRK)
+  int la_depth = side == main ? 0 : (la_mode >= 0 ? la_mode : (OB == NB ? 3 : (N < 12288 ? 4 : 2)));
+  if (la_depth == 3 && OB != NB) la_depth = 4;  // the split schedules: 3 for 128-wide steps, 4 for 256
+  if (la_depth == 4 && OB != 2 * NB) la_depth = 3;
+  // Split lookahead (la_depth 3, 128-wide steps): POTRF(k+1) needs only the
+  // diagonal tile of column block k+1, so the side stream updates that tile
+  // alone on ten CTAs (diag_tile_update) and goes straight on to POTRF; the rows
+  // below it (needed by TRSM(k+1) only) are updated on a third stream beside
+  // the POTRF and joined before the TRSM.
+  //   side: [wait SYRK(k-1)] LAdiag(k); POTRF(k+1); [wait LArest(k)] TRSM(k+1)
+  //   aux:  [wait panel k, SYRK(k-1)] LArest(k)       main: [wait panel k] SYRK(k)
+  if (la_depth == 3 && OB == NB) {
+    if (!g.aux) CK(cudaStreamCreateWithFlags(&g.aux, cudaStreamNonBlocking));
+    rc = ensure_side(3 * T + 2);
+    if (rc) return rc;
+    ev = g.events.data();
+    cudaEvent_t* ev_rest = ev + 2 * T + 2;
+    for (int64_t k = 0; k < T; ++k) {
+      CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
+      if (k == T - 1) break;
+      const int64_t c0 = k * OB, r1 = (k + 1) * OB, r2 = r1 + OB;
+      const double* L21 = W + r1 * ld + c0;
+      if (k > 0) CK(cudaStreamWaitEvent(side, ev[2 + 2 * (k - 1)], 0));
+      CK(diag_tile_update(L21, ld, W + r1 * ld + r1, ld, (int)OB, status, side));
+      if (r2 < N) {
+        CK(cudaStreamWaitEvent(g.aux, ev[1 + 2 * k], 0));
+        if (k > 0) CK(cudaStreamWaitEvent(g.aux, ev[2 + 2 * (k - 1)], 0));
+        const double* L31 = W + r2 * ld + c0;
+        CK(gemm_full(true, true, (int)(N - r2), (int)OB, (int)OB, -1.0, 1, L31, ld, L21, ld, W + r2 * ld + r1, ld,
+                     status, g.aux, /*lower_only=*/0, PROF_LOOKAHEAD));
+        CK(cudaEventRecord(ev_rest[k], g.aux));
+      }
+      CK(potrf_tile(W, ld, r1, status, side));
+      if (r2 < N) {
+        CK(cudaStreamWaitEvent(side, ev_rest[k], 0));
+        CK(trsm_panel(W, ld, r1, r2, N, status, side));
+      }
+      CK(cudaEventRecord(ev[1 + 2 * (k + 1)], side));
+      if ((rc = ship(k + 1))) return rc;
+      if (r2 < N) {
+        const double* L31 = W + r2 * ld + c0;
+        CK(gemm_lower_nt((int)(N - r2), (int)OB, L31, ld, L31, ld, W + r2 * ld + r2, ld, status, main));
+      }
+      CK(cudaEventRecord(ev[2 + 2 * k], main));
+    }
+    return STAN_CL_OK;
+  }
+  // Split lookahead for 256-wide steps (la_depth 4; depth-2 dependencies):
+  // the next panel's first POTRF needs only its 128 x 128 diagonal tile, the
+  // second POTRF only the in-panel update of ITS diagonal tile, so both are
+  // updated alone on ten CTAs on the side stream and the remaining rows on the
+  // third stream, joined before each TRSM:
+  //   side: [wait SYRK(k-2)] LAdiag; POTRF(h0); [wait A] TRSM(h0); [wait B] INdiag; POTRF(h1); [wait C] TRSM(h1)
+  //   aux:  [wait panel k, SYRK(k-2)] A = LA rows >= h1 of cols [h0, h1);  B = LA rows >= h1 of cols [h1, r2)
+  //         [wait TRSM(h0)] C = in-panel update rows >= h1 + 128 of cols [h1, r2)
+  if (la_depth == 4 && OB == 2 * NB) {
+    if (!g.aux) CK(cudaStreamCreateWithFlags(&g.aux, cudaStreamNonBlocking));
+    rc = ensure_side(6 * T + 2);
+    if (rc) return rc;
+    ev = g.events.data();
+    cudaEvent_t* evx = ev + 2 * T + 2;  // per step: A, B, TRSM(h0), C
+    for (int64_t k = 0; k < T; ++k) {
+      CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
+      if (k == T - 1) break;
+      const int64_t c0 = k * OB, r1 = (k + 1) * OB, h1 = r1 + NB, r2 = r1 + OB;
+      const int64_t ka = k > 0 ? 2 * OB : OB, ca = c0 + OB - ka;  // LA(k) applies panels k-1, k
+      cudaEvent_t* e4 = evx + 4 * k;
+      if (k >= 2) CK(cudaStreamWaitEvent(side, ev[2 + 2 * (k - 2)], 0));
+      CK(diag_tile_update(W + r1 * ld + ca, ld, W + r1 * ld + r1, ld, (int)ka, status, side));
+      // aux: the rest of LA(k) (rows >= h1), first and second half columns
+      CK(cudaStreamWaitEvent(g.aux, ev[1 + 2 * k], 0));
+      if (k >= 2) CK(cudaStreamWaitEvent(g.aux, ev[2 + 2 * (k - 2)], 0));
+      const double* Ar = W + h1 * ld + ca;
+      CK(gemm_full(true, true, (int)(N - h1), (int)NB, (int)ka, -1.0, 1, Ar, ld, W + r1 * ld + ca, ld,
+                   W + h1 * ld + r1, ld, status, g.aux, /*lower_only=*/0, PROF_LOOKAHEAD));
+      CK(cudaEventRecord(e4[0], g.aux));
+      CK(gemm_full(true, true, (int)(N - h1), (int)NB, (int)ka, -1.0, 1, Ar, ld, Ar, ld, W + h1 * ld + h1, ld,
+                   status, g.aux, /*lower_only=*/1, PROF_LOOKAHEAD));
+      CK(cudaEventRecord(e4[1], g.aux));
+      // side: first half of panel k+1
+      CK(potrf_tile(W, ld, r1, status, side));
+      CK(cudaStreamWaitEvent(side, e4[0], 0));
+      CK(trsm_panel(W, ld, r1, h1, N, status, side));
+      CK(cudaEventRecord(e4[2], side));
+      // in-panel update of the second half: its diagonal tile on the side stream,
+      // the rows below on aux
+      CK(cudaStreamWaitEvent(side, e4[1], 0));
+      const double* Lh = W + h1 * ld + r1;  // L(rows >= h1, first-half columns)
+      CK(diag_tile_update(Lh, ld, W + h1 * ld + h1, ld, (int)NB, status, side));
+      if (h1 + NB < N) {
+        CK(cudaStreamWaitEvent(g.aux, e4[2], 0));
+        CK(gemm_full(true, true, (int)(N - h1 - NB), (int)NB, (int)NB, -1.0, 1, Lh + NB * ld, ld, Lh, ld,
+                     W + (h1 + NB) * ld + h1, ld, status, g.aux, /*lower_only=*/0, PROF_LOOKAHEAD));
+        CK(cudaEventRecord(e4[3], g.aux));
+      }
+      CK(potrf_tile(W, ld, h1, status, side));
+      if (h1 + NB < N) {
+        CK(cudaStreamWaitEvent(side, e4[3], 0));
+        CK(trsm_panel(W, ld, h1, h1 + NB, N, status, side));
+      }
+      CK(cudaEventRecord(ev[1 + 2 * (k + 1)], side));
+      if ((rc = ship(k + 1))) return rc;
+      const int64_t rs = r2 + OB;  // depth 2: SYRK(k) covers rows / columns >= r2 + OB
+      if (rs < N) {
+        const double* L31 = W + rs * ld + c0;
+        CK(gemm_lower_nt((int)(N - rs), (int)OB, L31, ld, L31, ld, W + rs * ld + rs, ld, status, main));
+      }
+      CK(cudaEventRecord(ev[2 + 2 * k], main));
+    }
+    return STAN_CL_OK;
+  }
   if (la_depth > 0) {
     for (int64_t k = 0; k < T; ++k) {
       CK(cudaStreamWaitEvent(main, ev[1 + 2 * k], 0));
@@ -1770,6 +1883,10 @@ int stan_cl_finalize(void) {
   if (g.side) {
     cudaStreamDestroy(g.side);
     g.side = nullptr;
+  }
+  if (g.aux) {
+    cudaStreamDestroy(g.aux);
+    g.aux = nullptr;
   }
   return STAN_CL_OK;
 }

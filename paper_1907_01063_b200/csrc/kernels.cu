@@ -1288,6 +1288,81 @@ __global__ void __launch_bounds__(32 * TD_WARPS, 2) trsm_dmma_kernel(double* W, 
   trsm_dmma_block<0>(acc, Lo, DT, rdg, smtd + (TD_NOFF * TD_B * TD_P + 8 * TD_B * TD_B + NB) + warp * 8 * TD_P, P, g, t);
 }
 
+// The lookahead update of ONE diagonal tile, split finely so the next POTRF
+// (which needs only this tile) is not held up by a 128 x 64 x K GEMM item
+// (~8 us of DMMA work on one SM): C[128 x 128 lower] -= A A^T, A = 128 x K
+// (row-major, lda).  Ten CTAs, one per 32 x 32 block of the lower triangle;
+// the four warps of a CTA take a quarter of K each (all fragment loads of a
+// warp in flight from L2), the partial 32 x 32 products are added through
+// shared memory in warp order and subtracted from C.
+constexpr int DT_KMAX = 512;  // K / 4 per warp <= 128
+__global__ void __launch_bounds__(128) diag_tile_update_kernel(const double* __restrict__ A, int64_t lda,
+                                                               double* C, int64_t ldc, int K, const int* status) {
+  pdl_enter();
+  if (cta_status_set(status)) return;
+  __shared__ double red[4][32][33];
+  const int b = blockIdx.x;
+  int bi = 0, q = b;
+  while (q > bi) q -= ++bi;  // block (bi, q), q <= bi
+  const int bj = q;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  const int kq = K / 4, k0 = warp * kq;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // this thread's share of C, loaded up front (in flight with the operands)
+  double cv[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = tid + 128 * u, r = e >> 5, c = e & 31;
+    cv[u] = (32 * bj + c <= 32 * bi + r) ? __ldcg(C + (long long)(32 * bi + r) * ldc + 32 * bj + c) : 0.0;
+  }
+  const double* Ar = A + (long long)(32 * bi + g) * lda + k0 + t;
+  const double* Br = A + (long long)(32 * bj + g) * lda + k0 + t;
+#pragma unroll 2
+  for (int k = 0; k < kq; k += 16) {  // 4 k4 steps per round, 32 loads in flight
+    double a[4][4], bb[4][4];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        a[s][i] = __ldcg(Ar + (long long)(8 * i) * lda + k + 4 * s);
+        bb[s][i] = __ldcg(Br + (long long)(8 * i) * lda + k + 4 * s);
+      }
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[s][i], bb[s][j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      red[warp][8 * i + g][8 * j + 2 * t] = acc[i][j][0];
+      red[warp][8 * i + g][8 * j + 2 * t + 1] = acc[i][j][1];
+    }
+  __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 8; ++u) {
+    const int e = tid + 128 * u, r = e >> 5, c = e & 31;
+    const int gr = 32 * bi + r, gc = 32 * bj + c;
+    if (gc > gr) continue;
+    const double sum = ((red[0][r][c] + red[1][r][c]) + red[2][r][c]) + red[3][r][c];
+    C[(long long)gr * ldc + gc] = cv[u] - sum;
+  }
+}
+
+cudaError_t diag_tile_update(const double* A, int64_t lda, double* C, int64_t ldc, int K, const int* status,
+                             cudaStream_t st) {
+  Prof prof_(PROF_LOOKAHEAD, (double)K * NB * (NB + 1.0), st, 16.0 * NB * NB + 8.0 * NB * K);
+  if (K % 64 != 0 || K > DT_KMAX) return cudaErrorInvalidValue;
+  return launch_pdl(diag_tile_update_kernel, 10, 128, 0, st, A, lda, C, ldc, K, status);
+}
+
 static int trsm_impl() {
   static const int v = [] {
     const char* e = getenv("STAN_CL_TRSM_IMPL");  // 0 = substitution kernels (round 1/2), 1 = DMMA-blocked

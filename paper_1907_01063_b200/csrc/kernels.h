@@ -88,6 +88,10 @@ cudaError_t init_pad(double* W, int64_t n, int64_t N, double diag_pad, cudaStrea
 // ---- F1/F2: diagonal tile POTRF (K2) and panel TRSM (K3), NB = 128 ----
 // factor W[k0:k0+128, k0:k0+128] in place (lower); on failure status = k0 + j + 1
 cudaError_t potrf_tile(double* W, int64_t ld, int64_t k0, int* status, cudaStream_t st);
+// C[128 x 128, lower] -= A A^T (A 128 x K, K a multiple of 64 up to 512): the
+// lookahead update of the next diagonal tile alone, on ten CTAs (kernels.cu)
+cudaError_t diag_tile_update(const double* A, int64_t lda, double* C, int64_t ldc, int K, const int* status,
+                             cudaStream_t st);
 // rows [r0, r1) of columns [k0, k0+128): X <- X L11^-T (L11 = W[k0.., k0..]), substitution
 cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1, const int* status,
                        cudaStream_t st);

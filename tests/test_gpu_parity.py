@@ -413,14 +413,15 @@ def _forward_subprocess(env_extra, n, nb, exact=False):
 def test_forward_schedules(n, nb):
     """The forward's lookahead schedules (STAN_CL_LA_SIDE = 0: lookahead column
     on the main stream; 1: on the side stream; 2: depth 2, the column block
-    k+2 taking panels k and k+1 in one product) at 128- and 256-wide outer
+    k+2 taking panels k and k+1 in one product; 3: split, the next diagonal
+    tile alone on the side stream, the rows below on a third stream) at 128- and 256-wide outer
     blocks: each within the L tolerance of the oracle, the integer-exact family
     bit for bit."""
     K = se(n)
     want = oracle.cholesky(K)
     lo = np.tril_indices(n)
     L0 = inputs.unit_lower_pm1(n, seed=11)
-    for m in ("0", "1", "2"):
+    for m in ("0", "1", "2", "3"):
         env = {"STAN_CL_LA_SIDE": m}
         got = _forward_subprocess(env, n, nb)
         assert relf(got[lo], want[lo]) <= L_BAR_TOL, m
