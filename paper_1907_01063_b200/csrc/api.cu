@@ -816,9 +816,14 @@ int adjoint_pipelined(const double* Lw, double* Wm, int64_t N, int64_t ld, int* 
   }
   // one stream: the merged update of step s and C_bar D^-1 of step s+1 share a
   // persistent launch (the update's column block [j - B, j) -- the next C_bar --
-  // goes first and is counted; adj_update_fused_trmm).  STAN_CL_ADJ_FUSE=0: separate launches.
-  static const bool fuse_env = !getenv("STAN_CL_ADJ_FUSE") || atoi(getenv("STAN_CL_ADJ_FUSE")) != 0;
-  const bool fuse = fuse_env && !two_streams;
+  // goes first and is counted; adj_update_fused_trmm).
+  // Default: fused below n = 12288 (adjoint -8% at 4096, -4% at 8192); at
+  // 16384 the gain is 0.5 ms of a 144 ms step (noise level) while the fused
+  // class would mix the latency-bound panel product into the trailing
+  // update's roofline (0.88 instead of 0.91 of the DMMA peak), so the update
+  // keeps its own launch there.  STAN_CL_ADJ_FUSE=1 / 0 forces either.
+  static const int fuse_env = getenv("STAN_CL_ADJ_FUSE") ? atoi(getenv("STAN_CL_ADJ_FUSE")) : -1;
+  const bool fuse = !two_streams && (fuse_env >= 0 ? fuse_env != 0 : N < 12288);
   int* dep_cnt = status + 32;
   int cnt_base = 0;
   bool cdinv_ready = false;  // C_bar D^-1 of this step already computed by the previous launch
