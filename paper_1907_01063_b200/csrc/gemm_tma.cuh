@@ -138,7 +138,7 @@ __device__ __forceinline__ double frag(const double* s, int rc, int k) {
 }
 }  // namespace tg
 
-template <class CF, int MODE>
+template <class CF, int MODE, bool EXT = false>
 struct TItemMap {
   int ntn, ntm, ntiles, ktiles_full;
   // MODE_FULL: enumerate the last first_cols tile columns first (a fused
@@ -179,7 +179,7 @@ struct TItemMap {
       tm = tile - tn * ntm;
       return;
     }
-    if constexpr (MODE == MODE_FULL) {
+    if constexpr (EXT && MODE == MODE_FULL) {  // the fused kernel's orderings only
       if (first_cols > 0) {
         const int d = ntm * first_cols;
         if (tile < d) {
@@ -285,7 +285,7 @@ struct TItemMap {
 template <class CF>
 struct TFuse {
   GemmArgs p2;
-  TItemMap<CF, MODE_FULL> map2;
+  TItemMap<CF, MODE_FULL, true> map2;
   int n1 = 0x7fffffff;
   int* cnt = nullptr;
   int dep = 0;
@@ -311,13 +311,198 @@ __device__ __forceinline__ void produce_slab(double* dst, const CUtensorMap* map
   }
 }
 
-template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE, bool FUSE>
+template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
 __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                    const __grid_constant__ GemmArgs p, int nitems, TItemMap<CF, MODE> map,
+                    GemmArgs p, int nitems, TItemMap<CF, MODE> map) {
+  using namespace tg;
+  constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, NCONS = CF::NCONS;
+  constexpr int MI = CF::MI, NI = CF::NI;
+  constexpr int BKS = CF::BKS;
+  using SA = Slab<BM, A_KMAJ, BKS>;
+  using SB = Slab<BN, B_KMAJ, BKS>;
+  using SM = Smem<CF, A_KMAJ, B_KMAJ>;
+  pdl_enter();
+  if (cta_status_set(p.status)) return;
+  if ((int)blockIdx.x >= nitems) return;
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B aligned slab base (128B-swizzle atoms) as an OFFSET from the shared
+  // array: integer round-tripping the pointer would drop its address space and
+  // turn every fragment read into a generic 64-bit LD instead of an LDS
+  const unsigned sraw = (unsigned)__cvta_generic_to_shared(smem_raw);
+  unsigned char* base = smem_raw + ((1024u - (sraw & 1023u)) & 1023u);
+  double* sA = reinterpret_cast<double*>(base + SM::A);
+  double* sB = reinterpret_cast<double*>(base + SM::B);
+  double* sC = reinterpret_cast<double*>(base + SM::C);
+  uint64_t* full = reinterpret_cast<uint64_t*>(base + SM::BAR);
+  uint64_t* empty = full + STAGES;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);            // the producer's arrive.expect_tx
+      mbar_init(&empty[s], NCONS / 32);  // one arrive per consumer warp
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+  }
+  __syncthreads();
+
+  if (warp == NCONS / 32) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      if (A_KMAJ) prefetch_tmap(&tmA);
+      if (B_KMAJ) prefetch_tmap(&tmB);
+    }
+    int it = 0;
+    for (int item = map.next_valid(p, blockIdx.x, gridDim.x, nitems); item < nitems;
+         item = map.next_valid(p, item + gridDim.x, gridDim.x, nitems)) {
+      int m0, n0, kbeg, ns, z;
+      map.get(p, item, m0, n0, kbeg, ns, z);
+      for (int s = 0; s < ns; ++s, ++it) {
+        const int slot = it % STAGES, round = it / STAGES;
+        if (round > 0) mbar_wait(&empty[slot], (round - 1) & 1);
+        if (lane == 0) mbar_arrive_expect_tx(&full[slot], SA::TX + SB::TX);
+        __syncwarp();
+        const int k0 = kbeg + s * BKS;
+        produce_slab<BM, A_KMAJ, BKS>(sA + slot * (SA::BYTES / 8), &tmA, p.A, p.lda, m0, k0, lane, &full[slot]);
+        produce_slab<BN, B_KMAJ, BKS>(sB + slot * (SB::BYTES / 8), &tmB, p.B, p.ldb, n0, k0, lane, &full[slot]);
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------------------- consumers
+  const int wm = warp / CF::WARPS_N, wn = warp % CF::WARPS_N;
+  const int g = lane >> 2, t = lane & 3;
+  const bool need_c = (MODE != MODE_SPLITK) && p.beta != 0;
+  const unsigned long long smask = (p.sign < 0) ? 0x8000000000000000ull : 0ull;
+  double2* myC = reinterpret_cast<double2*>(sC) + (size_t)warp * MI * NI * 32 + lane;
+  auto load_c = [&](int m0, int n0) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
+        cp_async16(myC + (i * NI + j) * 32, p.C + (long long)r * p.ldc + c);
+      }
+    cp_async_commit();
+  };
+  int m0, n0, kbeg, ns, z;
+  const int first = map.next_valid(p, blockIdx.x, gridDim.x, nitems);
+  if (first >= nitems) return;
+  map.get(p, first, m0, n0, kbeg, ns, z);
+  if (CF::CPREF && need_c) load_c(m0, n0);
+  int kap[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) kap[s] = kappa(s, t);
+  int it = 0;
+  double acc[MI][NI][2];
+  for (int item = first; item < nitems;) {
+    const int nxt_item = map.next_valid(p, item + gridDim.x, gridDim.x, nitems);
+    if (need_c && CF::CPREF) {
+      cp_async_wait<0>();
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const double2 v = myC[(i * NI + j) * 32];
+          acc[i][j][0] = xor_sign(v.x, smask);
+          acc[i][j][1] = xor_sign(v.y, smask);
+        }
+    } else if (need_c) {
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) {
+          const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
+          const double2 v = *reinterpret_cast<const double2*>(p.C + (long long)r * p.ldc + c);
+          acc[i][j][0] = xor_sign(v.x, smask);
+          acc[i][j][1] = xor_sign(v.y, smask);
+        }
+    } else {
+#pragma unroll
+      for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
+    for (int s = 0; s < ns; ++s, ++it) {
+      const int slot = it % STAGES, round = it / STAGES;
+      mbar_wait(&full[slot], round & 1);
+      const double* a_s = sA + slot * (SA::BYTES / 8);
+      const double* b_s = sB + slot * (SB::BYTES / 8);
+#pragma unroll
+      for (int kk = 0; kk < BKS / 4; ++kk) {
+        const int k = ((kk >> 2) << 4) + kap[kk & 3];
+        double af[MI], bf[NI];
+#pragma unroll
+        for (int i = 0; i < MI; ++i) af[i] = tg::frag<BM, A_KMAJ>(a_s, wm * CF::WTM + i * 8 + g, k);
+#pragma unroll
+        for (int j = 0; j < NI; ++j) bf[j] = tg::frag<BN, B_KMAJ>(b_s, wn * CF::WTN + j * 8 + g, k);
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+      if (CF::CPREF && need_c && s == 0) {
+        // prefetch the next item's C into the private slots only now: the DMMAs
+        // above consumed acc (loaded from these slots), and asm-volatile order
+        // keeps this cp.async behind them, so the refill cannot overtake the read
+        const int nxt = nxt_item;
+        if (nxt < nitems) {
+          int m1, n1, kb1, ns1, z1;
+          map.get(p, nxt, m1, n1, kb1, ns1, z1);
+          load_c(m1, n1);
+        }
+      }
+    }
+    // epilogue: registers -> global
+    double* Cout;
+    long long ldo;
+    if constexpr (MODE == MODE_SPLITK) {
+      Cout = p.C + (long long)z * p.M * p.N;
+      ldo = p.N;
+    } else {
+      Cout = p.C;
+      ldo = p.ldc;
+    }
+    bool cmask;
+    int dd;
+    map.valid(p, item, cmask, dd);  // block-cyclic diagonal block: keep r >= c + dd
+    const bool mask = (MODE == MODE_LOWER) || ((MODE == MODE_FULL || MODE == MODE_CYC) && (p.lower_only || cmask));
+    const bool crosses = mask && (n0 + BN - 1 + dd > m0);
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+      for (int j = 0; j < NI; ++j) {
+        const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
+        double* dst = Cout + (long long)r * ldo + c;
+        const double v0 = xor_sign(acc[i][j][0], smask), v1 = xor_sign(acc[i][j][1], smask);
+        if (crosses) {
+          if (r >= c + dd) dst[0] = v0;
+          if (r >= c + 1 + dd) dst[1] = v1;
+        } else {
+          *reinterpret_cast<double2*>(dst) = make_double2(v0, v1);
+        }
+      }
+    if (nxt_item < nitems) map.get(p, nxt_item, m0, n0, kbeg, ns, z);
+    item = nxt_item;
+  }
+}
+
+// The two-problem (fused) variant of gemm_tma_kernel (TFuse): same pipeline and
+// main loop; per item it resolves which problem the tile belongs to.  Kept as a
+// separate kernel so the single-problem launches compile exactly as before.
+template <class CF, bool A_KMAJ, bool B_KMAJ>
+__global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
+    gemm_tma_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ GemmArgs p, int nitems, TItemMap<CF, MODE_FULL, true> map,
                     const __grid_constant__ CUtensorMap tmA2,
                     const __grid_constant__ TFuse<CF> fz) {
   using namespace tg;
+  constexpr int MODE = MODE_FULL;
+  constexpr bool FUSE = true;
   constexpr int BM = CF::BM, BN = CF::BN, STAGES = CF::STAGES, NCONS = CF::NCONS;
   constexpr int MI = CF::MI, NI = CF::NI;
   constexpr int BKS = CF::BKS;
@@ -532,8 +717,22 @@ int tma_num_sms();
 bool make_kmajor_map(CUtensorMap* map, const double* X, long long rows, long long K, long long ld,
                      int box_rows);
 
-template <class CF, int MODE>
-int tma_item_map(const GemmArgs& p, TItemMap<CF, MODE>& map) {
+template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
+cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reserve_sms = 0) {
+  using SM = tg::Smem<CF, A_KMAJ, B_KMAJ>;
+  auto kern = gemm_tma_kernel<CF, A_KMAJ, B_KMAJ, MODE>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  CUtensorMap ma, mb;
+  memset(&ma, 0, sizeof(ma));
+  memset(&mb, 0, sizeof(mb));
+  if (A_KMAJ && !make_kmajor_map(&ma, p.A, p.M, p.K, p.lda, CF::BM)) return cudaErrorInvalidValue;
+  if (B_KMAJ && !make_kmajor_map(&mb, p.B, p.N, p.K, p.ldb, CF::BN)) return cudaErrorInvalidValue;
+  TItemMap<CF, MODE> map;
   map.ntn = p.N / CF::BN;
   map.ntm = p.M / CF::BM;
   map.ktiles_full = p.K / CF::BKS;
@@ -548,7 +747,7 @@ int tma_item_map(const GemmArgs& p, TItemMap<CF, MODE>& map) {
   if constexpr (MODE == MODE_CYC) {
     {  // valid tile rows per 256-wide block column
       const int nbc = p.N / 256, nbr = p.M / 256;
-      if (nbc > TItemMap<CF, MODE>::kCycMax) return -1;
+      if (nbc > TItemMap<CF, MODE>::kCycMax) return cudaErrorInvalidValue;
       map.cyc_nb = nbc;
       map.cyc_pref[0] = 0;
       for (int j = 0; j < nbc; ++j) {
@@ -562,59 +761,58 @@ int tma_item_map(const GemmArgs& p, TItemMap<CF, MODE>& map) {
     }
   }
   map.ntiles = ntiles;
-  return ntiles;
+  const int nitems = ntiles * (MODE == MODE_SPLITK ? splits : 1);
+  if (nitems == 0) return cudaSuccess;
+  // reserve_sms: SMs left free for kernels on other streams
+  const int nsm = (tma_num_sms() - (reserve_sms > 0 && reserve_sms < tma_num_sms() ? reserve_sms : 0)) * CF::MINB;
+  const int grid = nitems < nsm ? nitems : nsm;
+  return launch_pdl(kern, grid, CF::NCONS + 32, SM::TOTAL, st, ma, mb, p, nitems, map);
 }
 
-template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
-cudaError_t launch_tma_impl(const GemmArgs& p, int splits, cudaStream_t st, int reserve_sms, const GemmArgs* p2,
-                            int first_cols, int* cnt, int cnt_base) {
-  using SM = tg::Smem<CF, A_KMAJ, B_KMAJ>;
-  auto kern = gemm_tma_kernel<CF, A_KMAJ, B_KMAJ, MODE, false>;
-  if constexpr (MODE == MODE_FULL && !B_KMAJ) {  // the only fused shape (adj_update_fused_trmm)
-    if (p2) kern = gemm_tma_kernel<CF, A_KMAJ, B_KMAJ, MODE, true>;
-  }
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[p2 ? 1 : 0]) {
+
+// Problem 1 (its last first_cols tile columns first, each counted on *cnt when
+// stored) and problem 2 (waiting for *cnt >= cnt_base + those tiles) in one
+// persistent launch of gemm_tma_fused_kernel: MODE_FULL, B not k-major.
+template <class CF, bool A_KMAJ>
+cudaError_t launch_tma_fused(const GemmArgs& p, const GemmArgs& p2, int first_cols, int* cnt, int cnt_base,
+                             cudaStream_t st, int reserve_sms = 0) {
+  using SM = tg::Smem<CF, A_KMAJ, false>;
+  auto kern = gemm_tma_fused_kernel<CF, A_KMAJ, false>;
+  static bool attr_set = false;
+  if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, SM::TOTAL);
     if (e != cudaSuccess) return e;
-    attr_set[p2 ? 1 : 0] = true;
+    attr_set = true;
   }
   CUtensorMap ma, mb, ma2;
   memset(&ma, 0, sizeof(ma));
   memset(&mb, 0, sizeof(mb));
   memset(&ma2, 0, sizeof(ma2));
   if (A_KMAJ && !make_kmajor_map(&ma, p.A, p.M, p.K, p.lda, CF::BM)) return cudaErrorInvalidValue;
-  if (B_KMAJ && !make_kmajor_map(&mb, p.B, p.N, p.K, p.ldb, CF::BN)) return cudaErrorInvalidValue;
-  TItemMap<CF, MODE> map;
-  const int ntiles = tma_item_map<CF, MODE>(p, map);
-  if (ntiles < 0) return cudaErrorInvalidValue;
-  int nitems = ntiles * (MODE == MODE_SPLITK ? splits : 1);
+  if (A_KMAJ && !make_kmajor_map(&ma2, p2.A, p2.M, p2.K, p2.lda, CF::BM)) return cudaErrorInvalidValue;
+  auto fill = [](const GemmArgs& q, TItemMap<CF, MODE_FULL, true>& m) {
+    m.ntn = q.N / CF::BN;
+    m.ntm = q.M / CF::BM;
+    m.ktiles_full = q.K / CF::BKS;
+    m.ntiles = m.ntm * m.ntn;
+    return m.ntiles;
+  };
+  TItemMap<CF, MODE_FULL, true> map;
+  const int n1 = fill(p, map);
+  if (first_cols <= 0 || first_cols > map.ntn) return cudaErrorInvalidValue;
+  map.first_cols = first_cols;
   TFuse<CF> fz;
-  if constexpr (MODE == MODE_FULL) {
-    if (p2) {
-      // problem 1's last first_cols tile columns first (counted), then problem 2
-      if (B_KMAJ || first_cols <= 0 || first_cols > map.ntn) return cudaErrorInvalidValue;
-      map.first_cols = first_cols;
-      fz.p2 = *p2;
-      const int n2 = tma_item_map<CF, MODE_FULL>(*p2, fz.map2);
-      if (A_KMAJ && !make_kmajor_map(&ma2, p2->A, p2->M, p2->K, p2->lda, CF::BM)) return cudaErrorInvalidValue;
-      fz.n1 = nitems;
-      fz.cnt = cnt;
-      fz.dep = map.ntm * first_cols;
-      fz.target = cnt_base + fz.dep;  // *cnt counts monotonically across launches
-      nitems += n2;
-    }
-  }
+  fz.p2 = p2;
+  const int n2 = fill(p2, fz.map2);
+  fz.n1 = n1;
+  fz.cnt = cnt;
+  fz.dep = map.ntm * first_cols;
+  fz.target = cnt_base + fz.dep;  // *cnt counts monotonically across launches
+  const int nitems = n1 + n2;
   if (nitems == 0) return cudaSuccess;
-  // reserve_sms: SMs left free for kernels on other streams
   const int nsm = (tma_num_sms() - (reserve_sms > 0 && reserve_sms < tma_num_sms() ? reserve_sms : 0)) * CF::MINB;
   const int grid = nitems < nsm ? nitems : nsm;
   return launch_pdl(kern, grid, CF::NCONS + 32, SM::TOTAL, st, ma, mb, p, nitems, map, ma2, fz);
-}
-
-template <class CF, bool A_KMAJ, bool B_KMAJ, int MODE>
-cudaError_t launch_tma(const GemmArgs& p, int splits, cudaStream_t st, int reserve_sms = 0) {
-  return launch_tma_impl<CF, A_KMAJ, B_KMAJ, MODE>(p, splits, st, reserve_sms, nullptr, 0, nullptr, 0);
 }
 
 }  // namespace stancl

@@ -1543,7 +1543,7 @@ cudaError_t adj_update_fused_trmm(int M1, int N1, int K, const double* A1, int64
   Prof prof_(PROF_GEMM, 2.0 * M1 * N1 * K + 1.0 * M2 * K * K, st,
              16.0 * M1 * N1 + 8.0 * ((double)M1 * K + (double)N1 * K) + 16.0 * M2 * K + 8.0 * K * K);
   *dep_out = (M1 / CF::BM) * first_cols;
-  return launch_tma_impl<CF, true, false, MODE_FULL>(p1, 1, st, 0, &p2, first_cols, cnt, cnt_base);
+  return launch_tma_fused<CF, true>(p1, p2, first_cols, cnt, cnt_base, st);
 }
 
 cudaError_t gemm_cyclic_lower(int M, int N, int K, const double* A, int64_t lda, const double* B, int64_t ldb,

@@ -232,8 +232,9 @@ def test_check_matrix_vs_oracle(sc, n):
 
 def test_trace_timeline(sc):
     """stan_cl_trace_*: every launch of a call is recorded with its stream and
-    ordered times; the forward uses the library stream and the lookahead side
-    stream; classes match the launch kinds."""
+    ordered times; the forward uses the library stream, the lookahead side
+    stream and (split lookahead, the default at this size) the third stream
+    for the rows below the next diagonal tile; classes match the launch kinds."""
     n = 2048
     K = dev(se(n))
     sc.cholesky(K)                                 # warm
@@ -247,7 +248,7 @@ def test_trace_timeline(sc):
     assert all(0.0 <= a <= b for _, _, a, b in recs)
     kinds = {k for k, _, _, _ in recs}
     assert {"potrf", "trsm", "syrk", "lookahead"} <= kinds
-    assert {s for _, s, _, _ in recs} == {0, 1}
+    assert {s for _, s, _, _ in recs} == {0, 1, 2}
     sc.cholesky(K)                                 # not traced any more
     assert len(sc.trace_read()) == len(recs)
 

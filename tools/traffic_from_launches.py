@@ -6,8 +6,8 @@
 
 Kernel -> library profiling class (paper_1907_01063_b200.PROFILE_KINDS):
   gemm_dmma_kernel<..., 1, 1, 1> / gemm_tma_kernel<..., 1, 1, 1>   syrk      (MODE_LOWER)
-  gemm_tma_kernel<..., 1, 0, 0, 1>                                 adj_gemm  (fused: [R_bar; B_bar] update + next C_bar D^-1)
-  gemm_tma_kernel<..., 1, 0, 0, 0>                                 adj_gemm / trmm (unfused update; C_bar D^-1)
+  gemm_tma_fused_kernel<..., 1, 0>                                 adj_gemm  (fused: [R_bar; B_bar] update + next C_bar D^-1)
+  gemm_tma_kernel<..., 1, 0, 0>                                    adj_gemm / trmm (unfused update; C_bar D^-1)
   gemm_tma_kernel<..., 0, 0, 2> / gemm_dmma_kernel<..., 0, 0, 2>   splitk
   gemm_tma_kernel<..., 1, 1, 0>                                    lookahead (main-stream column update)
   gemm_dmma_kernel<..., 1, 1, 0>                                   panel_gemm (side stream)
@@ -23,6 +23,8 @@ UNITS = {"ns": 1e-6, "us": 1e-3, "ms": 1.0, "byte": 1.0, "Kbyte": 1e3, "Mbyte": 
 
 
 def classify(name: str):
+    if "gemm_tma_fused_kernel" in name:  # the adjoint's update of step s + C_bar D^-1 of step s+1
+        return "adj_gemm"
     m = re.search(r"(gemm_dmma_kernel|gemm_tma_kernel)<.*>, (\d), (\d), (\d)(?:, (\d))?>", name)
     if not m:
         return re.match(r"(?:void )?(\w+)", name).group(1)
@@ -63,7 +65,7 @@ def main(path, out=None):
     # update, so a (1, 0, 0) launch whose next GEMM launch is split-K is the former
     gemm_like = {"adj_gemm", "splitk", "syrk", "lookahead", "panel_gemm"}
     for i, c in enumerate(classes):
-        if c != "adj_gemm" or re.search(r", 1>\(", seq[i]["name"]):  # fused launches stay adj_gemm
+        if c != "adj_gemm" or "gemm_tma_fused_kernel" in seq[i]["name"]:  # fused launches stay adj_gemm
             continue
         nxt = next((classes[j] for j in range(i + 1, len(classes)) if classes[j] in gemm_like), None)
         if nxt == "splitk":
