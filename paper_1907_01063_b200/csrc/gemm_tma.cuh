@@ -425,23 +425,29 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
 #pragma unroll
         for (int j = 0; j < NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
+    // lower-triangular outputs: a warp whose whole 32 x 32 sub-tile lies above the
+    // diagonal (the upper half of a diagonal block's tiles) only keeps the slab
+    // protocol; its sub-partition's DMMA pipe then serves the other warp alone
+    const bool idle = MODE == MODE_LOWER && (m0 + wm * CF::WTM + CF::WTM - 1 < n0 + wn * CF::WTN);
     for (int s = 0; s < ns; ++s, ++it) {
       const int slot = it % STAGES, round = it / STAGES;
       mbar_wait(&full[slot], round & 1);
       const double* a_s = sA + slot * (SA::BYTES / 8);
       const double* b_s = sB + slot * (SB::BYTES / 8);
+      if (!idle) {
 #pragma unroll
-      for (int kk = 0; kk < BKS / 4; ++kk) {
-        const int k = ((kk >> 2) << 4) + kap[kk & 3];
-        double af[MI], bf[NI];
+        for (int kk = 0; kk < BKS / 4; ++kk) {
+          const int k = ((kk >> 2) << 4) + kap[kk & 3];
+          double af[MI], bf[NI];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) af[i] = tg::frag<BM, A_KMAJ>(a_s, wm * CF::WTM + i * 8 + g, k);
+          for (int i = 0; i < MI; ++i) af[i] = tg::frag<BM, A_KMAJ>(a_s, wm * CF::WTM + i * 8 + g, k);
 #pragma unroll
-        for (int j = 0; j < NI; ++j) bf[j] = tg::frag<BN, B_KMAJ>(b_s, wn * CF::WTN + j * 8 + g, k);
+          for (int j = 0; j < NI; ++j) bf[j] = tg::frag<BN, B_KMAJ>(b_s, wn * CF::WTN + j * 8 + g, k);
 #pragma unroll
-        for (int i = 0; i < MI; ++i)
+          for (int i = 0; i < MI; ++i)
 #pragma unroll
-          for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+            for (int j = 0; j < NI; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[slot]);
@@ -473,7 +479,7 @@ __global__ void __launch_bounds__(CF::NCONS + 32, CF::MINB)
     const bool mask = (MODE == MODE_LOWER) || ((MODE == MODE_FULL || MODE == MODE_CYC) && (p.lower_only || cmask));
     const bool crosses = mask && (n0 + BN - 1 + dd > m0);
 #pragma unroll
-    for (int i = 0; i < MI; ++i)
+    for (int i = 0; i < (idle ? 0 : MI); ++i)
 #pragma unroll
       for (int j = 0; j < NI; ++j) {
         const int r = m0 + wm * CF::WTM + i * 8 + g, c = n0 + wn * CF::WTN + j * 8 + 2 * t;
