@@ -1136,11 +1136,13 @@ __global__ void __launch_bounds__(256, 2) trsm128_kernel(double* W, int64_t ld, 
   for (int q = 0; q < Q; ++q) P[p + 4 * q] = x[q];
 }
 
-// The 128-wide panel solve X L11^T = A21 as a blocked substitution with the
-// cross-block updates on the FP64 tensor cores (one launch).  The columns are
-// taken in 16-wide blocks b = 0..7 (the column-by-column elimination of
-// PAPER.md:277's solve, grouped):
-//   x_J  = a_J L_JJ^-T                    substitution, ascending j (J = block b)
+// The 128-wide panel solve X L11^T = A21 blocked by 16 columns, all of it on
+// the FP64 tensor cores (one launch).  The columns are taken in 16-wide blocks
+// b = 0..7:
+//   x_J  = a_J L_JJ^-T                    INV: DMMA with the CTA's 16 x 16 inverse
+//                                         (PAPER.md:277's explicit inverse, at
+//                                         16-column granularity: DESIGN.md R11);
+//                                         else substitution, ascending j
 //   a_K -= x_J L_KJ^T   for K > J          DMMA.8x8x4, K = 16
 // A warp owns 8 rows; its 8 x 128 slice of the panel lives in registers in the
 // DMMA accumulator layout (lane (g, t): row g, columns 8 nt + 2t, +1 of every
@@ -1161,6 +1163,7 @@ constexpr int TD_WARPS = 4;                                // 32 rows per CTA
 constexpr int TD_ROWS = 8 * TD_WARPS;
 constexpr int TD_NOFF = 28;                                // off-diagonal blocks of the 8 x 8 block triangle
 constexpr int TD_SMEM = (TD_NOFF * TD_B * TD_P + 8 * TD_B * TD_B + NB + TD_WARPS * 8 * TD_P) * (int)sizeof(double);
+constexpr int TD_SMEM_INV = TD_SMEM + 8 * TD_B * TD_P * (int)sizeof(double);  // + the diagonal-block inverses
 
 __device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double b) {
   // not volatile: a pure function of its operands, so ptxas may interleave the
@@ -1171,9 +1174,51 @@ __device__ __forceinline__ void dmma_nv(double& c0, double& c1, double a, double
 }
 __host__ __device__ constexpr int td_off(int bi, int bj) { return (bi - 1) * bi / 2 + bj; }  // bj < bi
 
-template <int B>
+template <int B, bool INV>
 __device__ __forceinline__ void trsm_dmma_block(double (&acc)[16][2], const double* Lo, const double* DT,
-                                                const double* rdg, double* Xs, double* P, int g, int t) {
+                                                const double* rdg, double* Xs, double* P, int g, int t,
+                                                const double* LinvT) {
+  if constexpr (INV) {
+    // x_J = a_J (L_JJ^-1)^T on the tensor cores (the 16 x 16 diagonal-block
+    // inverses are computed once per CTA): no serial substitution chain
+    double* xr = Xs + g * TD_P;
+    *reinterpret_cast<double2*>(xr + 2 * t) = make_double2(acc[2 * B][0], acc[2 * B][1]);
+    *reinterpret_cast<double2*>(xr + 8 + 2 * t) = make_double2(acc[2 * B + 1][0], acc[2 * B + 1][1]);
+    __syncwarp();
+    double a[4];
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) a[kc] = xr[4 * kc + t];
+    const double* M = LinvT + B * TD_B * TD_P;  // M[n][k] = L_JJ^-1[n][k]
+    double x0[2] = {0.0, 0.0}, x1[2] = {0.0, 0.0};
+#pragma unroll
+    for (int kc = 0; kc < 4; ++kc) {
+      if (kc < 2) dmma_nv(x0[0], x0[1], a[kc], M[g * TD_P + 4 * kc + t]);  // columns 0..7: k <= 7 only
+      dmma_nv(x1[0], x1[1], a[kc], M[(8 + g) * TD_P + 4 * kc + t]);
+    }
+    acc[2 * B][0] = x0[0];
+    acc[2 * B][1] = x0[1];
+    acc[2 * B + 1][0] = x1[0];
+    acc[2 * B + 1][1] = x1[1];
+    *reinterpret_cast<double2*>(P + 16 * B + 2 * t) = make_double2(x0[0], x0[1]);
+    *reinterpret_cast<double2*>(P + 16 * B + 8 + 2 * t) = make_double2(x1[0], x1[1]);
+    if constexpr (B < 7) {
+      __syncwarp();
+      *reinterpret_cast<double2*>(xr + 2 * t) = make_double2(x0[0], x0[1]);
+      *reinterpret_cast<double2*>(xr + 8 + 2 * t) = make_double2(x1[0], x1[1]);
+      __syncwarp();
+#pragma unroll
+      for (int kc = 0; kc < 4; ++kc) a[kc] = -xr[4 * kc + t];
+#pragma unroll
+      for (int nt = 2 * B + 2; nt < 16; ++nt) {
+        const double* Lb = Lo + td_off(nt >> 1, B) * TD_B * TD_P + (8 * (nt & 1) + g) * TD_P + t;
+#pragma unroll
+        for (int kc = 0; kc < 4; ++kc) dmma_nv(acc[nt][0], acc[nt][1], a[kc], Lb[4 * kc]);
+      }
+      __syncwarp();
+      trsm_dmma_block<B + 1, INV>(acc, Lo, DT, rdg, Xs, P, g, t, LinvT);
+    }
+    return;
+  }
   // (1) gather block B's 16 columns of row g into every lane of the row
   double* xr = Xs + g * TD_P;
   *reinterpret_cast<double2*>(xr + 2 * t) = make_double2(acc[2 * B][0], acc[2 * B][1]);
@@ -1220,10 +1265,11 @@ __device__ __forceinline__ void trsm_dmma_block(double (&acc)[16][2], const doub
       for (int kc = 0; kc < 4; ++kc) dmma_nv(acc[nt][0], acc[nt][1], a[kc], Lb[4 * kc]);  // B[k][n] = L[n][4kc + k]
     }
     __syncwarp();  // Xs is rewritten by the next block's gather
-    trsm_dmma_block<B + 1>(acc, Lo, DT, rdg, Xs, P, g, t);
+    trsm_dmma_block<B + 1, INV>(acc, Lo, DT, rdg, Xs, P, g, t, LinvT);
   }
 }
 
+template <bool INV>
 __global__ void __launch_bounds__(32 * TD_WARPS, 2) trsm_dmma_kernel(double* W, int64_t ld, int64_t k0, int64_t r0,
                                                                     const int* status) {
   pdl_enter();
@@ -1285,7 +1331,28 @@ __global__ void __launch_bounds__(32 * TD_WARPS, 2) trsm_dmma_kernel(double* W, 
     rdg[r] = rcp_pos(drr);
   }
   __syncthreads();  // (the strict upper halves of the DT blocks are never read)
-  trsm_dmma_block<0>(acc, Lo, DT, rdg, smtd + (TD_NOFF * TD_B * TD_P + 8 * TD_B * TD_B + NB) + warp * 8 * TD_P, P, g, t);
+  double* Xs = smtd + (TD_NOFF * TD_B * TD_P + 8 * TD_B * TD_B + NB) + warp * 8 * TD_P;
+  double* LinvT = smtd + (TD_NOFF * TD_B * TD_P + 8 * TD_B * TD_B + NB) + TD_WARPS * 8 * TD_P;
+  if constexpr (INV) {
+    // L_bb^-1 of the eight 16 x 16 diagonal blocks: lane c of a half-warp solves
+    // L x = e_c by substitution (x_i = 0 for i < c), quotients IEEE (div_pos)
+    const int b = 2 * warp + (lane >> 4), c = lane & 15;
+    const double* D = DT + b * TD_B * TD_B;  // D[k * 16 + i] = L[16b + i][16b + k]
+    double x[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      double sacc = 0.0;
+#pragma unroll
+      for (int k = 0; k < i; ++k) sacc = fma(D[k * TD_B + i], x[k], sacc);
+      const double q = (i == c) ? rdg[16 * b + i] : div_pos(-sacc, D[i * TD_B + i], rdg[16 * b + i]);
+      x[i] = (i < c) ? 0.0 : q;
+    }
+    double* Mo = LinvT + b * TD_B * TD_P;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) Mo[i * TD_P + c] = x[i];
+    __syncthreads();
+  }
+  trsm_dmma_block<0, INV>(acc, Lo, DT, rdg, Xs, P, g, t, LinvT);
 }
 
 // The lookahead update of ONE diagonal tile, split finely so the next POTRF
@@ -1365,8 +1432,9 @@ cudaError_t diag_tile_update(const double* A, int64_t lda, double* C, int64_t ld
 
 static int trsm_impl() {
   static const int v = [] {
-    const char* e = getenv("STAN_CL_TRSM_IMPL");  // 0 = substitution kernels (round 1/2), 1 = DMMA-blocked
-    return e ? atoi(e) : 1;
+    const char* e = getenv("STAN_CL_TRSM_IMPL");  // 0 = substitution kernels (round 1/2), 1 = DMMA-blocked,
+                                                   // 2 = DMMA-blocked with 16 x 16 diagonal-block inverses
+    return e ? atoi(e) : 2;
   }();
   return v;
 }
@@ -1375,15 +1443,17 @@ cudaError_t trsm_panel(double* W, int64_t ld, int64_t k0, int64_t r0, int64_t r1
                        cudaStream_t st) {
   if (r1 <= r0) return cudaSuccess;
   Prof prof_(PROF_TRSM, (double)(r1 - r0) * NB * NB, st, 16.0 * (r1 - r0) * NB + 4.0 * NB * NB);
-  if (trsm_impl() == 1 && (r1 - r0) % TD_ROWS == 0) {
-    static bool attr = false;
-    if (!attr) {
-      cudaError_t e = cudaFuncSetAttribute(trsm_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, TD_SMEM);
+  if (trsm_impl() >= 1 && (r1 - r0) % TD_ROWS == 0) {
+    static bool attr[2] = {false, false};
+    const bool inv = trsm_impl() == 2;
+    auto kern = inv ? trsm_dmma_kernel<true> : trsm_dmma_kernel<false>;
+    const int smem = inv ? TD_SMEM_INV : TD_SMEM;
+    if (!attr[inv]) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
       if (e != cudaSuccess) return e;
-      attr = true;
+      attr[inv] = true;
     }
-    return launch_pdl(trsm_dmma_kernel, (int)((r1 - r0) / TD_ROWS), 32 * TD_WARPS, TD_SMEM, st, W, ld, k0, r0,
-                      status);
+    return launch_pdl(kern, (int)((r1 - r0) / TD_ROWS), 32 * TD_WARPS, smem, st, W, ld, k0, r0, status);
   }
   // one launch for panels up to trsm128_maxm rows (latency-bound; measured
   // faster there), the two 64-wide substitutions + DMMA cross update above
