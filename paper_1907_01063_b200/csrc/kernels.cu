@@ -1136,13 +1136,14 @@ __global__ void __launch_bounds__(256, 2) trsm128_kernel(double* W, int64_t ld, 
   for (int q = 0; q < Q; ++q) P[p + 4 * q] = x[q];
 }
 
-// The 128-wide panel solve X L11^T = A21 blocked by 16 columns, all of it on
-// the FP64 tensor cores (one launch).  The columns are taken in 16-wide blocks
-// b = 0..7:
-//   x_J  = a_J L_JJ^-T                    INV: DMMA with the CTA's 16 x 16 inverse
-//                                         (PAPER.md:277's explicit inverse, at
-//                                         16-column granularity: DESIGN.md R11);
-//                                         else substitution, ascending j
+// The 128-wide panel solve X L11^T = A21 blocked by 16 columns with the
+// cross-block updates on the FP64 tensor cores (one launch).  The columns are
+// taken in 16-wide blocks b = 0..7:
+//   x_J  = a_J L_JJ^-T                    substitution, ascending j (default);
+//                                         INV (STAN_CL_TRSM_IMPL=2): DMMA with the
+//                                         CTA's 16 x 16 inverses -- faster, but
+//                                         over the 1e-11 bar on some inputs
+//                                         (R11)
 //   a_K -= x_J L_KJ^T   for K > J          DMMA.8x8x4, K = 16
 // A warp owns 8 rows; its 8 x 128 slice of the panel lives in registers in the
 // DMMA accumulator layout (lane (g, t): row g, columns 8 nt + 2t, +1 of every
@@ -1434,7 +1435,7 @@ static int trsm_impl() {
   static const int v = [] {
     const char* e = getenv("STAN_CL_TRSM_IMPL");  // 0 = substitution kernels (round 1/2), 1 = DMMA-blocked,
                                                    // 2 = DMMA-blocked with 16 x 16 diagonal-block inverses
-    return e ? atoi(e) : 2;
+    return e ? atoi(e) : 1;
   }();
   return v;
 }
