@@ -197,9 +197,9 @@ AdjPlan adj_plan(int64_t n) {
   p.part = al(part);
   p.tmp = al(4 * (size_t)p.B * p.B * sizeof(double));
   p.ctmp = al((size_t)p.N * p.B * sizeof(double));
-  // scratch of the streamed host path's per-block D^-1 (copy stream): its own
-  // region, since the reverse sweep already runs on the main stream meanwhile
-  p.hscr = al((size_t)NB * NB * sizeof(double));
+  // (formerly the copy stream's D^-1 scratch; the streamed host path now
+  // computes D^-1 in stream order with the sweep, from the Pbuf region)
+  p.hscr = 0;
   // pipelined sweep: three rotating [S; C_bar D^-1] buffers of (B + N) x B
   p.cs = 3 * al((size_t)(p.B + p.N) * p.B * sizeof(double));
   p.total = al(sizeof(int) * 64) + p.dinv + p.part + p.tmp + p.ctmp + p.hscr + p.cs;
@@ -692,7 +692,7 @@ int block_inverses(const double* Lw, int64_t ld, int64_t B, int64_t b0, int64_t 
 int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* status,
                     const AdjPlan& plan, const cudaEvent_t* rows_ready = nullptr,
                     const HostOut* out = nullptr, const cudaEvent_t* col_done = nullptr,
-                    const double* src = nullptr, int64_t lds = 0) {
+                    const double* src = nullptr, int64_t lds = 0, int64_t host_n = 0) {
   cudaStream_t st = g.stream;
   const int64_t B = plan.B;
   char* base = (char*)g.ws + al(sizeof(int) * 64);
@@ -715,6 +715,21 @@ int adjoint_inplace(const double* Lw, double* Wm, int64_t N, int64_t ld, int* st
     const int64_t j = k - B, m = N - k;
     if (rows_ready)
       for (int64_t r = j; r < k; r += NB) CK(cudaStreamWaitEvent(st, rows_ready[r / NB], 0));
+    if (rows_ready) {
+      // streamed host path: the rows of this block have arrived (the copy stream
+      // only copies); the upper triangle of the new L_bar tiles, the diagonal
+      // check and D^-1 of the block run here, in stream order with the sweep
+      // (as kernels on the copy stream beside the sweep they produced wrong
+      // A_bar in ~1 of 12 calls at n = 16384)
+      const int64_t nn = host_n;
+      for (int64_t r0 = j; r0 < k && r0 < nn; r0 += NB) {
+        const int64_t r1 = std::min(r0 + NB, nn);
+        CK(zero_tile_upper(Wm, ld, r0, (int)(r1 - r0), st));
+        CK(check_diag(Lw + r0 * ld + r0, r1 - r0, ld, status, st, r0));
+      }
+      int rc2 = block_inverses(Lw, ld, B, j / B, 1, Dinv, Pbuf, status, st);
+      if (rc2) return rc2;
+    }
     const double* D = Lw + j * ld + j;
     const double* Db = Dinv + (j / B) * B * B;
     const double* R = Lw + j * ld;       // L(j:k, 0:j)
@@ -1647,7 +1662,6 @@ int adjoint_host_enqueue(int64_t n, const double* L, const double* L_bar, double
   if (rc) return rc;
   if ((rc = ensure_copy(2 * nblk + 4))) return rc;
   int* status = (int*)g.ws;
-  double* Dinv = (double*)((char*)g.ws + al(sizeof(int) * 64));
   cudaStream_t st = g.stream;
   double *Lw = nullptr, *Wm = nullptr;
   if ((rc = ensure_mat(0, (size_t)N * N * sizeof(double), &Lw))) return rc;
@@ -1655,11 +1669,8 @@ int adjoint_host_enqueue(int64_t n, const double* L, const double* L_bar, double
   CK(cudaMemsetAsync(status, 0, sizeof(int), st));
   CK(init_pad(Lw, n, N, 1.0, st));
   CK(init_pad(Wm, n, N, 0.0, st));
-  const int64_t B = plan.B;
   cudaEvent_t* ready = g.xev.data() + 2;
   cudaEvent_t* col_done = ready + nblk;
-  // not Pbuf (the split-K partials of the sweep that runs concurrently on the main stream)
-  double* scratch = (double*)((char*)g.ws + al(sizeof(int) * 64) + plan.dinv + plan.part + plan.tmp + plan.ctmp);
   CK(cudaEventRecord(g.xev[0], st));
   CK(cudaStreamWaitEvent(g.h2d, g.xev[0], 0));
   for (int64_t b = nblk - 1; b >= 0; --b) {  // bottom-up: the order the reverse sweep needs
@@ -1669,17 +1680,11 @@ int adjoint_host_enqueue(int64_t n, const double* L, const double* L_bar, double
                            r1 - r0, cudaMemcpyHostToDevice, g.h2d));
       CK(cudaMemcpy2DAsync(Wm + r0 * N, N * sizeof(double), L_bar + r0 * n, n * sizeof(double),
                            r1 * sizeof(double), r1 - r0, cudaMemcpyHostToDevice, g.h2d));
-      CK(zero_tile_upper(Wm, N, r0, (int)(r1 - r0), g.h2d));  // only the lower triangle of L_bar is read
-      CK(check_diag(Lw + r0 * N + r0, r1 - r0, N, status, g.h2d, r0));
-    }
-    if (r0 % B == 0) {  // all rows of diagonal block r0 / B are in: its inverse
-      rc = block_inverses(Lw, N, B, r0 / B, 1, Dinv, scratch, status, g.h2d);
-      if (rc) return rc;
     }
     CK(cudaEventRecord(ready[b], g.h2d));
   }
   HostOut out{A_bar, n};
-  rc = adjoint_inplace(Lw, Wm, N, N, status, plan, ready, &out, col_done);
+  rc = adjoint_inplace(Lw, Wm, N, N, status, plan, ready, &out, col_done, nullptr, 0, n);
   if (rc) return rc;
   CK(cudaEventRecord(g.xev[1], g.d2h));
   CK(cudaStreamWaitEvent(st, g.xev[1], 0));

@@ -384,6 +384,24 @@ def test_graph_replay_same_buffers(sc, n):
         assert relf(Lh.numpy()[lo], oracle.cholesky(K)[lo]) <= L_BAR_TOL, it
 
 
+def test_host_adjoint_repeatable_fullsize(sc):
+    """The streamed host adjoint against the device adjoint, bit for bit, over
+    repeated calls at n = 16384: with its per-block kernels (tile zeroing,
+    diagonal check, D^-1) on the copy stream beside the sweep it returned wrong
+    entries in ~1 of 12 calls (round-2 stress test); they now run
+    in stream order with the sweep."""
+    n = 16384
+    x = torch.from_numpy(inputs.gp_x(n)).cuda()
+    L = sc.cholesky(sc.gp_exp_quad_cov(x, 1.0, 1.0, 1e-6))
+    W = torch.from_numpy(inputs.lbar(n)).cuda()
+    A0 = torch.tril(sc.cholesky_adjoint(L, W)).cpu()
+    Lh, Wh = L.cpu().pin_memory(), W.cpu().pin_memory()
+    Ah = torch.empty_like(Lh).pin_memory()
+    for it in range(16):
+        assert sc.cholesky_adjoint_host(Lh, Wh, Ah) == 0
+        assert torch.equal(torch.tril(Ah), A0), it
+
+
 def _forward_subprocess(env_extra, n, nb, exact=False):
     """L of the SE problem (or of the integer-exact family) at order n from a
     fresh process with the given environment."""
