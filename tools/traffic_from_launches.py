@@ -27,7 +27,7 @@ def classify(name: str):
         return "adj_gemm"
     m = re.search(r"(gemm_dmma_kernel|gemm_tma_kernel)<.*>, (\d), (\d), (\d)(?:, (\d))?>", name)
     if not m:
-        return re.match(r"(?:void )?(\w+)", name).group(1)
+        return re.match(r"(?:void )?(?:\w+::)*(\w+)", name).group(1)
     kern, a, b, mode, fused = m.group(1), m.group(2), m.group(3), m.group(4), m.group(5)
     key = (a, b, mode)
     if fused == "1":  # the adjoint's update of step s + C_bar D^-1 of step s+1 (adj_update_fused_trmm)
